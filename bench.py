@@ -1,0 +1,491 @@
+"""Benchmark of the NAR hot path on B200 (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload c2|c1|c3|c4] [--no-e2e] [--no-cpu]
+
+One step = one frame of the hot path over the workload's synthetic cloud,
+resident in HBM: render (project + early-z into the u64 keybuf) + resolve to
+the RGB+D G-buffer (+ the U-Net for c4).  N>1 (torchrun, one rank per GPU):
+each rank renders its own shard (weak scaling), keybufs are composited by an
+NCCL int64 MIN all-reduce in the sign-flipped key domain, every rank resolves
+the pixels it owns and an int32 SUM reduce of the channel bit patterns brings
+the G-buffer to rank 0.
+
+Keys in the JSON line: value = whole-job points/s (Gpts/s); e2e = the same
+metric through the reference-facing API (``rasterize`` on a pinned host
+PointCloud, H2D of the points and D2H of the FeatureImage inside the timed
+region); roofline = the render kernel against measured HBM bandwidth at
+12 algorithmic bytes per point; cpu_baseline = the reference's own Cython
+render kernel (oracle/_ref) with its chunked thread-pool dispatch plus the
+reference resolve, on the host cores, over a bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "points/sec rasterized (Gpts/s, % HBM roofline) and end-to-end fps at 1080p"
+BYTES_PER_POINT = 12  # f32 xyz, read once per frame
+
+WORKLOADS = {
+    # name: (points per GPU, width, height, description)
+    "c1": (1_000_000, 512, 512, "synthetic uniform cloud 1M points, single stream, 512x512 rasterize+resolve"),
+    "c2": (350_000_000, 1920, 1080, "synthetic 350M-point cloud, single stream, 1920x1080 rasterize+resolve"),
+    "c3": (400_000_000, 1920, 1080, "4 streams x 100M Lagrangian-like points, 1080p, RGB+D+Vel2D, one CUDA stream per data stream"),
+    "c4": (350_000_000, 1920, 1080, "350M terrain-like points rasterized + U-Net (random init) at 1080p"),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.sw_power_cap",
+              "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown", "power.draw"]
+
+    def __init__(self, device_index: int):
+        self.samples: list[tuple[float, list[str]]] = []
+        self.proc = None
+        try:
+            import torch
+
+            uuid = str(torch.cuda.get_device_properties(device_index).uuid)
+            sel = ["-i", uuid if uuid.startswith("GPU-") else f"GPU-{uuid}"]
+        except Exception:
+            sel = []
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", *sel, f"--query-gpu={','.join(self.FIELDS)}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+        t0 = time.time()
+        while not self.samples and time.time() - t0 < 10:
+            time.sleep(0.05)
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append((time.time(), [x.strip() for x in line.split(",")]))
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self, t0: float, t1: float) -> dict:
+        rows = [r for t, r in self.samples if t0 <= t <= t1 + 0.05]
+        if not rows and self.samples:  # region shorter than one period: nearest sample
+            rows = [min(self.samples, key=lambda s: abs(s[0] - (t0 + t1) / 2))[1]]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i] == "Active"})
+        pw = [float(r[6]) for r in rows if r[6].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(pw) if pw else None}
+
+
+def measured_peaks() -> tuple[dict, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text()), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# synthetic clouds (generated on the device)
+# ---------------------------------------------------------------------------
+def make_uniform(n, device, seed):
+    import torch
+
+    g = torch.Generator(device=device).manual_seed(seed)
+    pos = torch.empty((n, 3), dtype=torch.float32, device=device)
+    rgb = torch.empty((n, 3), dtype=torch.uint8, device=device)
+    step = 50_000_000
+    for lo in range(0, n, step):
+        hi = min(n, lo + step)
+        pos[lo:hi].uniform_(-1.0, 1.0, generator=g)
+        rgb[lo:hi] = torch.randint(0, 256, (hi - lo, 3), device=device, generator=g,
+                                   dtype=torch.int32).to(torch.uint8)
+    return pos, rgb
+
+
+def make_terrain(n, device, seed):
+    """Height field z = fractal value noise over (x, y) ~ U(-1,1)^2, rgb = slope shade."""
+    import torch
+
+    g = torch.Generator(device=device).manual_seed(seed)
+    pos = torch.empty((n, 3), dtype=torch.float32, device=device)
+    rgb = torch.empty((n, 3), dtype=torch.uint8, device=device)
+    lat = [torch.rand((2 ** (o + 2) + 1,) * 2, device=device, generator=g) for o in range(6)]
+
+    def noise(x, y):
+        z = torch.zeros_like(x)
+        for o, L in enumerate(lat):
+            r = L.shape[0] - 1
+            u, v = (x + 1) * 0.5 * r, (y + 1) * 0.5 * r
+            i0 = u.floor().clamp(0, r - 1).long()
+            j0 = v.floor().clamp(0, r - 1).long()
+            fu, fv = u - i0, v - j0
+            a = L[i0, j0] * (1 - fu) + L[i0 + 1, j0] * fu
+            b = L[i0, j0 + 1] * (1 - fu) + L[i0 + 1, j0 + 1] * fu
+            z += (a * (1 - fv) + b * fv) * 0.5 ** o
+        return z * 0.4
+
+    step = 25_000_000
+    for lo in range(0, n, step):
+        hi = min(n, lo + step)
+        xy = torch.rand((hi - lo, 2), device=device, generator=g) * 2 - 1
+        x, y = xy[:, 0], xy[:, 1]
+        z = noise(x, y)
+        dz = (noise(x + 1e-3, y) - z) * 1e3
+        pos[lo:hi, 0], pos[lo:hi, 1], pos[lo:hi, 2] = x, y, z
+        shade = (0.5 + 0.5 * torch.tanh(-dz)).clamp(0, 1)
+        rgb[lo:hi, 0] = (shade * 200 + 30).to(torch.uint8)
+        rgb[lo:hi, 1] = (shade * 170 + 50 * (z > 0.2)).clamp(0, 255).to(torch.uint8)
+        rgb[lo:hi, 2] = (shade * 120).to(torch.uint8)
+    return pos, rgb
+
+
+def make_trajectories(n, device, seed):
+    """storm_trajectories-like stream: Euler advection of seeds in
+    v = (-y, x, 0.1 sin z); velocity = tangent; constant per-stream hue."""
+    import torch
+
+    g = torch.Generator(device=device).manual_seed(seed)
+    steps = 100
+    seeds = n // steps
+    p = torch.rand((seeds, 3), device=device, generator=g) * 2 - 1
+    pos = torch.empty((seeds, steps, 3), dtype=torch.float32, device=device)
+    vel = torch.empty_like(pos)
+    dt = 0.02
+    for s in range(steps):
+        v = torch.stack([-p[:, 1], p[:, 0], 0.1 * torch.sin(p[:, 2])], dim=1)
+        pos[:, s], vel[:, s] = p, v
+        p = p + dt * v
+    hue = torch.tensor([[230, 60, 40], [40, 200, 80], [50, 90, 230], [220, 200, 40]],
+                       dtype=torch.uint8, device=device)[seed % 4]
+    rgb = hue.expand(seeds * steps, 3).contiguous()
+    return pos.reshape(-1, 3), rgb, vel.reshape(-1, 3)
+
+
+# ---------------------------------------------------------------------------
+# reference arm / CPU baseline
+# ---------------------------------------------------------------------------
+def reference_frame(pos_np, rgb_np, cam, threads):
+    """One reference frame on the CPU: the reference's Cython render kernel
+    (oracle/_ref) under its chunked thread-pool dispatch, then the reference
+    resolve including its whole-stream u8->f32 conversion (rasterizer.py:152)."""
+    import numpy as np
+
+    import oracle
+
+    i = cam.intrinsics
+    impl = "reference" if oracle.ref_native() is not None else "port"
+    kb = oracle.zbuffer_render(pos_np, cam.orientation, cam.position, i.focal_px, i.cx, i.cy,
+                               i.near, i.far, i.width, i.height, threads=threads, impl=impl)
+    covered = kb != oracle.EMPTY_KEY
+    win = (kb[covered] & np.uint64(0xFFFFFFFF)).astype(np.int64)
+    depth = np.zeros(kb.shape, np.float32)
+    depth[covered] = (kb[covered] >> np.uint64(32)).astype(np.uint32).view(np.float32)
+    data = np.zeros((kb.size, 4), np.float32)
+    rgbs = rgb_np.astype(np.float32) / 255.0
+    data[covered, 0:3] = rgbs[win, :3]
+    data[covered, 3] = np.float32(i.near) / depth[covered]
+    np.clip(data[:, 3], 0.0, 1.0, out=data[:, 3])
+    return impl
+
+
+def cpu_sample(n_total, W, H, seed=0):
+    import numpy as np
+
+    rng = np.random.default_rng(seed)
+    pos = rng.uniform(-1, 1, (n_total, 3)).astype(np.float32)
+    rgb = rng.integers(0, 256, (n_total, 3), dtype=np.uint8)
+    return pos, rgb
+
+
+def run_cpu_baseline(W, H, n_sample, passes=3):
+    import oracle
+    from paper_2407_19097_b200.geometry import Intrinsics, look_at
+
+    oracle.build()
+    threads = os.cpu_count() or 1
+    pos, rgb = cpu_sample(n_sample, W, H)
+    cam = look_at((0.0, -2.2, 1.0), (0, 0, 0), Intrinsics(width=W, height=H))
+    impl = reference_frame(pos[: n_sample // 10], rgb[: n_sample // 10], cam, threads)
+    t0 = time.perf_counter()
+    for _ in range(passes):
+        reference_frame(pos, rgb, cam, threads)
+    dt = (time.perf_counter() - t0) / passes
+    return {"value": n_sample / dt / 1e9, "unit": "Gpts/s", "cores": threads,
+            "kind": "reference" if impl == "reference" else "port",
+            "sample": f"{n_sample} uniform points at {W}x{H}, RGB+D render+resolve, "
+                      f"mean of {passes} frames ({dt:.2f} s/frame)"}
+
+
+def main_reference(args):
+    """--impl reference: the reference CPU implementation on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    from paper_2407_19097_b200.geometry import Intrinsics, look_at
+
+    n_pts, W, H, desc = WORKLOADS[args.workload]
+    oracle.build()
+    threads = os.cpu_count() or 1
+    n_sample = min(n_pts, 20_000_000)
+    pos, rgb = cpu_sample(n_sample, W, H)
+    cam = look_at((0.0, -2.2, 1.0), (0, 0, 0), Intrinsics(width=W, height=H))
+    for _ in range(args.warmup):
+        impl = reference_frame(pos, rgb, cam, threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        impl = reference_frame(pos, rgb, cam, threads)
+        times.append(time.perf_counter() - t0)
+    dt = sum(times) / len(times)
+    v = n_sample / dt / 1e9
+    kind = "reference" if impl == "reference" else "port"
+    sample = f"{n_sample} of {n_pts} points per step at {W}x{H} (RGB+D render+resolve)"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "Gpts/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": desc, "sample_points": n_sample, "width": W, "height": H},
+        "cpu_baseline": {"value": v, "unit": "Gpts/s", "cores": threads, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": v, "unit": "Gpts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def main_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2407_19097_b200 import _lib
+    from paper_2407_19097_b200.geometry import Intrinsics, PointCloud, Stream, look_at
+    from paper_2407_19097_b200.msr import DeviceCloud, Renderer, StreamSelection, rasterize
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    _lib.load()
+    n_pts, W, H, desc = WORKLOADS[args.workload]
+    if args.points:
+        n_pts = args.points
+
+    # ---- data (per-rank shard: weak scaling) --------------------------------
+    t_gen = time.time()
+    if args.workload == "c3":
+        clouds, streams = [], []
+        for s in range(4):
+            p, c, v = make_trajectories(n_pts // 4, dev, seed=rank * 4 + s)
+            clouds.append({"begin": rank * n_pts + s * (n_pts // 4), "positions": p,
+                           "streams": {"rgb": c, "velocity": v}})
+        from paper_2407_19097_b200.msr import _StreamMeta
+
+        meta = {"rgb": _StreamMeta("rgb", "u8", 3), "velocity": _StreamMeta("velocity", "f32", 3)}
+        cloud = DeviceCloud(clouds, meta, dev)
+        sel = StreamSelection(rgb=True, depth=True, vel2d=True)
+        eye = (0.0, -2.6, 1.4)
+    else:
+        gen = make_terrain if args.workload == "c4" else make_uniform
+        pos, rgb = gen(n_pts, dev, seed=1234 + rank)
+        cloud = DeviceCloud.from_tensors(pos, {"rgb": rgb}, begin=rank * n_pts)
+        sel = StreamSelection(rgb=True, depth=True)
+        eye = (0.0, -1.6, 1.2) if args.workload == "c4" else (0.0, -2.2, 1.0)
+    torch.cuda.synchronize()
+    log(f"[rank {rank}] generated {cloud.count / 1e6:.0f}M points in {time.time() - t_gen:.1f}s")
+    cam = look_at(eye, (0, 0, 0), Intrinsics(width=W, height=H))
+    r = Renderer(W, H, device=dev, signed_keys=world > 1, pad_multiple=16)
+    names = sel.channel_names(cloud)
+    out = r.alloc_outputs(len(names))
+    main = torch.cuda.current_stream(dev)
+
+    unet = None
+    if args.workload == "c4":
+        from paper_2407_19097_b200.neural import UNet, UNetConfig, init_params
+
+        cfg = UNetConfig(input_channels=len(names))
+        unet = UNet(cfg, init_params(cfg), device=dev)
+        ph, pw = out["data"].shape[:2]
+        unet_out = torch.empty((ph, pw, 3), dtype=torch.float32, device=dev)
+
+    def frame(ev_r0=None, ev_r1=None):
+        if ev_r0 is not None:
+            ev_r0.record(main)
+        r.render(cloud, cam)
+        if ev_r1 is not None:
+            ev_r1.record(main)
+        if world > 1:
+            dist.all_reduce(r.keybuf, op=dist.ReduceOp.MIN)
+            r.resolve(cloud, cam, sel, out=out, owner_only=True)
+            dist.reduce(out["data"].view(torch.int32), dst=0, op=dist.ReduceOp.SUM)
+        else:
+            r.resolve(cloud, cam, sel, out=out)
+        if unet is not None and rank == 0:
+            unet.forward_into(out["data"], unet_out)
+
+    for _ in range(args.warmup):
+        frame()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local) if rank == 0 else None
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.time()
+    e0.record(main)
+    for k in range(args.steps):
+        frame(*evs[k])
+    e1.record(main)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t1 = time.time()
+    total_ms = e0.elapsed_time(e1)
+    render_ms = [a.elapsed_time(b) for a, b in evs]
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    clocks = sampler.summary(t0, t1) if sampler else None
+    if sampler:
+        sampler.stop()
+    ms_step = total_ms / args.steps
+    pts_total = cloud.count * world
+    value = pts_total / (ms_step * 1e-3) / 1e9
+    render_avg = sum(render_ms) / len(render_ms)
+    peaks, peak_kind = measured_peaks()
+    achieved = cloud.count * BYTES_PER_POINT / (render_avg * 1e-3) / 1e9
+    launches_per_step = sum(1 + (1 if (sg["count"] % 1024) else 0) for sg in cloud.segments) + 1
+    if unet is not None:
+        launches_per_step += unet.launches_per_forward()
+
+    # ---- e2e through the reference-facing API (host buffers) -----------------
+    e2e = None
+    if not args.no_e2e and world == 1 and args.workload in ("c1", "c2"):
+        host_pos = torch.empty((cloud.count, 3), dtype=torch.float32, pin_memory=True)
+        host_rgb = torch.empty((cloud.count, 3), dtype=torch.uint8, pin_memory=True)
+        host_pos.copy_(cloud.segments[0]["positions"])
+        host_rgb.copy_(cloud.segments[0]["streams"]["rgb"])
+        pc = PointCloud.__new__(PointCloud)
+        pc.positions, pc.pinned = host_pos.numpy(), True
+        pc.streams = [Stream.__new__(Stream)]
+        pc.streams[0].name, pc.streams[0].format, pc.streams[0].data = "rgb", "u8", host_rgb.numpy()
+        k_e2e = max(2, min(args.steps, 5))
+        rasterize(pc, cam, sel)  # warm
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(main)
+        for _ in range(k_e2e):
+            fi = rasterize(pc, cam, sel)
+        b.record(main)
+        torch.cuda.synchronize()
+        e2e_ms = a.elapsed_time(b) / k_e2e
+        d2h = fi.data.nbytes + fi.coverage.nbytes + fi.index_plane.nbytes + fi.depth.nbytes
+        e2e = {"value": cloud.count / (e2e_ms * 1e-3) / 1e9, "unit": "Gpts/s",
+               "h2d_bytes_per_step": int(host_pos.numel() * 4 + host_rgb.numel()),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms,
+               "api": "paper_2407_19097_b200.msr.rasterize(pinned host PointCloud)"}
+        del host_pos, host_rgb, pc
+
+    cpu = None
+    if not args.no_cpu and world == 1 and rank == 0:
+        cpu = run_cpu_baseline(W, H, min(n_pts, 35_000_000))
+
+    traffic = None
+    tp = ROOT / "profiles" / "render_traffic.json"
+    if tp.exists():
+        try:
+            tj = json.loads(tp.read_text())
+            if tj.get("workload") == args.workload:
+                traffic = tj.get("bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "Gpts/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc, "points_per_gpu": cloud.count, "width": W, "height": H,
+                       "selection": list(names), "order": "storage (random)",
+                       "l2": f"inputs {cloud.count * 12 / 1e9:.1f} GB per GPU > 126 MB L2 (no flush needed)",
+                       "parallelism": f"points sharded over {world} GPU(s)" if world > 1 else "1 GPU"},
+            "fps": 1e3 / ms_step,
+            "render_ms": render_avg,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
+                         "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+                         "traffic": traffic, "peak_kind": peak_kind,
+                         "kernel": "render_tma_kernel", "bytes_per_point": BYTES_PER_POINT},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--points", type=int, default=0, help="override points per GPU")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        main_reference(args)
+    else:
+        main_ours(args)
+
+
+if __name__ == "__main__":
+    main()

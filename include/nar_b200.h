@@ -1,0 +1,170 @@
+/*
+ * nar_b200.h -- C ABI of the B200-native NAR hot path (MSR render + resolve,
+ * min-composite helpers, gated U-Net forward).
+ *
+ * Every entry point takes plain pointers and sizes, returns an int status
+ * (NAR_OK == 0) and never throws across the ABI; the message of the last
+ * failure on the calling thread is available from nar_last_error().
+ * Pointers documented as "device" must be CUDA device (or managed) memory;
+ * "host" pointers may be pageable or pinned.  `stream` is a cudaStream_t
+ * passed as void* (NULL = legacy default stream).
+ *
+ * Reference interfaces replaced (paths relative to the reference package
+ * root pkg/src/nar/):
+ *   nar_zbuffer_accumulate  <- _kernels/_native.pyx:32-77 `zbuffer_accumulate`
+ *                              (twin: _kernels/python_impl.py:17-53)
+ *   nar_render / nar_render_host
+ *                           <- _kernels/__init__.py:56-94 `zbuffer_render`
+ *                              (chunked private buffers + np.minimum.reduce)
+ *   nar_resolve             <- msr/rasterizer.py:140-178 (decode + channel fill),
+ *                              msr/velocity.py:17-48, geometry/camera.py:154-166
+ *   nar_unet_*              <- neural/model.py:135-204 (`conv1x1_head`,
+ *                              `build_pyramid`, `gated_conv`, `unet_forward`,
+ *                              `forward`), neural/autodiff.py:186-288
+ */
+#ifndef NAR_B200_H
+#define NAR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (mapped to nar errors by the Python shim) ---------------- */
+#define NAR_OK 0
+#define NAR_ERR_INVALID 1 /* bad argument            -> ValueError          */
+#define NAR_ERR_CUDA 2    /* CUDA runtime failure    -> RuntimeError        */
+#define NAR_ERR_CONFIG 3  /* inconsistent selection  -> ConfigurationError  */
+#define NAR_ERR_NOMEM 4   /* allocation failure      -> MemoryError         */
+
+/* python_impl.py:13 EMPTY_KEY */
+#define NAR_EMPTY_KEY 0xFFFFFFFFFFFFFFFFull
+/* Keys of the "signed" domain are key ^ NAR_SIGN_FLIP: unsigned order equals
+ * int64 order there, so an int64 MIN all-reduce composites them exactly. */
+#define NAR_SIGN_FLIP 0x8000000000000000ull
+
+#define NAR_KEYS_UNSIGNED 0
+#define NAR_KEYS_SIGNED 1
+
+#define NAR_MAX_SEGMENTS 8 /* point buffers rendered into one keybuf      */
+#define NAR_MAX_SCALARS 8  /* pointcloud.py:18 MAX_STREAMS                */
+#define NAR_MAX_CHANNELS 16 /* rasterizer.py:21 MAX_CHANNELS              */
+
+#define NAR_FMT_U8 0
+#define NAR_FMT_F32 1
+
+/* Pinhole camera as consumed by the render kernel (camera.py:26-72). */
+typedef struct nar_camera {
+  double R[9];      /* world->camera rotation, row major, rows right/down/forward */
+  double campos[3]; /* camera position in world space                             */
+  double f, cx, cy; /* focal length in px, principal point                        */
+  double near_, far_;
+  int32_t width, height;
+} nar_camera;
+
+/* ---- library ----------------------------------------------------------------- */
+const char* nar_version(void);
+const char* nar_last_error(void);
+int nar_device_count(int32_t* count);
+/* Host memory helpers (pinned allocations make H2D copies true async DMA). */
+int nar_host_alloc(void** ptr, size_t bytes);
+int nar_host_free(void* ptr);
+
+/* ---- host-parity twin of the reference FFI --------------------------------------
+ * Same arguments and semantics as `_native.zbuffer_accumulate` (_native.pyx:32):
+ * projects positions[n][3] (host f32, C-contiguous AoS), folds
+ * key = f32bits((float)uz) << 32 | ((base_index + i) & 0xFFFFFFFF) into
+ * keybuf[width*height] (host u64, in place) by unsigned minimum.
+ * Non-finite projections are culled as in python_impl.py:43-47. */
+int nar_zbuffer_accumulate(uint64_t* keybuf, const float* positions, int64_t n,
+                           uint64_t base_index, const double* R, const double* campos,
+                           double f, double cx, double cy, double near_, double far_,
+                           int32_t width, int32_t height);
+
+/* ---- device-resident render ----------------------------------------------------- */
+/* keybuf_dev[npix] = value (EMPTY_KEY, or EMPTY_KEY ^ SIGN_FLIP in the signed domain). */
+int nar_keybuf_fill(uint64_t* keybuf_dev, int64_t npix, uint64_t value, void* stream);
+/* Render n device-resident points (f32 AoS) into keybuf_dev.  key_domain selects
+ * unsigned keys (reference layout) or sign-flipped keys (NCCL int64 MIN). */
+int nar_render(uint64_t* keybuf_dev, const float* positions_dev, int64_t n,
+               uint64_t base_index, const nar_camera* cam, int32_t key_domain,
+               void* stream);
+/* Same as nar_render for host-resident points: streams them through device
+ * chunk buffers, overlapping the H2D copy of chunk k+1 with the render of k. */
+int nar_render_host(uint64_t* keybuf_dev, const float* positions_host, int64_t n,
+                    uint64_t base_index, const nar_camera* cam, int32_t key_domain,
+                    void* stream);
+
+/* ---- resolve ---------------------------------------------------------------------- */
+/* One contiguous point buffer (a "data stream" of the multi-stream config):
+ * global indices [begin, begin+count) live in rows [0, count) of these arrays. */
+typedef struct nar_segment {
+  int64_t begin;
+  int64_t count;
+  const float* positions;                 /* (count,3) f32, needed for vel2d */
+  const void* rgb;                        /* (count, rgb_arity)              */
+  const void* velocity;                   /* (count, vel_arity)              */
+  const void* scalars[NAR_MAX_SCALARS];   /* (count, scalar_arity[k])        */
+} nar_segment;
+
+/* Channel selection, rasterizer.py:27-72 StreamSelection (channel order is
+ * r,g,b | d | v2x,v2y,v2t,v2m | v3x,v3y,v3z,v3m | scalars | coverage). */
+typedef struct nar_selection {
+  int32_t rgb, depth, vel2d, vel3d, coverage_channel;
+  int32_t rgb_format, rgb_arity;
+  int32_t vel_format, vel_arity;
+  int32_t n_scalars;
+  int32_t scalar_format[NAR_MAX_SCALARS];
+  int32_t scalar_arity[NAR_MAX_SCALARS];
+  double velocity_scale;
+} nar_selection;
+
+typedef struct nar_resolve_out {
+  float* data;          /* (data_h, data_w, C) f32 FeatureImage.data, or NULL.
+                           data_h >= H, data_w >= W: pixels outside (H, W) are
+                           written as zeros, i.e. the buffer is already the
+                           zero-padded CNN input of model.py:207           */
+  int32_t data_h, data_w; /* 0 = (H, W)                                    */
+  uint8_t* coverage;    /* (H, W) u8, or NULL                              */
+  int64_t* index_plane; /* (H, W) i64, -1 = background, or NULL            */
+  float* depth;         /* (H, W) f32 view depth, 0 = background, or NULL  */
+  int32_t owner_only;   /* 1: winners outside the local segments give zero
+                           channels (sharded resolve before an int32 SUM
+                           reduce of the channel bit patterns)             */
+  int32_t clear_keybuf; /* 1: reset keybuf to EMPTY for the next frame    */
+} nar_resolve_out;
+
+int nar_resolve(uint64_t* keybuf_dev, const nar_camera* cam, int32_t key_domain,
+                const nar_selection* sel, const nar_segment* segments,
+                int32_t n_segments, const nar_resolve_out* out, void* stream);
+
+/* ---- gated U-Net (neural/model.py) -------------------------------------------------- */
+typedef struct nar_unet_config {
+  int32_t input_channels, levels, base_channels, channel_multiplier;
+  int32_t max_channels, output_channels, use_descriptor_head;
+} nar_unet_config;
+
+typedef struct nar_unet nar_unet; /* opaque: packed bf16 weights + plan */
+
+int nar_unet_create(const nar_unet_config* cfg, nar_unet** out);
+int nar_unet_destroy(nar_unet* net);
+/* Upload one f32 parameter from host memory, named as in model.py:70-100
+ * ("head.w", "enc0a.f_w", ..., "out.b"); conv weights are HWIO. */
+int nar_unet_set_param(nar_unet* net, const char* name, const float* host_data,
+                       int64_t numel);
+/* Device workspace needed by nar_unet_forward at (height, width). */
+int nar_unet_workspace_bytes(const nar_unet* net, int32_t height, int32_t width,
+                             size_t* bytes);
+/* forward(): in_dev is f32 NHWC (1,H,W,Cin) -- e.g. the padded buffer
+ * nar_resolve wrote -- and out_dev is f32 NHWC (1,H,W,output_channels).
+ * H and W must be multiples of 2^(levels-1) (model.py:148-151). */
+int nar_unet_forward(nar_unet* net, const float* in_dev, int32_t height, int32_t width,
+                     float* out_dev, void* workspace, size_t workspace_bytes,
+                     void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NAR_B200_H */

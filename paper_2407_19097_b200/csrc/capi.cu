@@ -1,0 +1,66 @@
+// capi.cu -- library-level C ABI: versioning, error reporting, pinned host
+// memory.  Errors never cross the ABI as exceptions: every entry point
+// returns a status and leaves a thread-local message (nar_last_error).
+#include <cuda_runtime.h>
+#include <stdio.h>
+
+#include <string>
+
+#include "common.cuh"
+#include "nar_b200.h"
+
+namespace nar {
+
+static thread_local std::string g_last_error;
+
+int set_error(int code, const char* msg) {
+  g_last_error = msg ? msg : "";
+  return code;
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) return NAR_OK;
+  std::string m = std::string(what) + ": " + cudaGetErrorString(e);
+  return set_error(NAR_ERR_CUDA, m.c_str());
+}
+
+}  // namespace nar
+
+extern "C" {
+
+const char* nar_version(void) { return "nar_b200 0.1.0 (sm_100a)"; }
+
+const char* nar_last_error(void) { return nar::g_last_error.c_str(); }
+
+int nar_device_count(int32_t* count) {
+  if (!count) return nar::set_error(NAR_ERR_INVALID, "NULL count");
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *count = 0;
+    return NAR_OK;
+  }
+  *count = n;
+  return NAR_OK;
+}
+
+int nar_host_alloc(void** ptr, size_t bytes) {
+  if (!ptr) return nar::set_error(NAR_ERR_INVALID, "NULL out pointer");
+  if (cudaHostAlloc(ptr, bytes ? bytes : 1, cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    return nar::set_error(NAR_ERR_NOMEM, "cudaHostAlloc failed");
+  }
+  return NAR_OK;
+}
+
+int nar_host_free(void* ptr) {
+  if (ptr && cudaFreeHost(ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return nar::set_error(NAR_ERR_CUDA, "cudaFreeHost failed");
+  }
+  return NAR_OK;
+}
+
+}  // extern "C"

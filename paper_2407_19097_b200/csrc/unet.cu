@@ -1,0 +1,540 @@
+// unet.cu -- gated U-Net forward (pkg/src/nar/neural/model.py:135-204) on B200.
+//
+// Plan (all activations NHWC bf16, channel counts padded to multiples of 8 so
+// every pixel row is a whole number of 16-byte chunks):
+//   head      : f32 in (H,W,Cin) -> y = x @ head.w + head.b (f32)  [model.py:135-143]
+//   pyramid   : 4 x 2x2 average pools of the f32 head output        [model.py:146-155]
+//   enc k     : a = gated(concat(pool(skip_{k-1}), pyr_k)); skip_k = gated(a)
+//   dec k     : a = gated(concat(up2(x), skip_k));     x = gated(a) [model.py:174-191]
+//   out       : sigmoid(x @ out.w + out.b) -> f32 (H,W,out)
+// A gated conv is one implicit GEMM with N = 2*Cout (f and g branches side by
+// side) and the elu(f + bf) * sigmoid(g + bg) epilogue fused; the operand
+// producer resolves concat / up2 / zero padding by address arithmetic.
+//
+// conv kernels: gated_conv_tc (tcgen05 + TMEM, unet_tc.cuh) is the hot path;
+// gated_conv_simt below is the CUDA-core version kept for on-device
+// cross-checking of the tensor-core kernel (NAR_UNET_SIMT=1).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "nar_b200.h"
+#include "unet_tc.cuh"
+
+namespace nar {
+
+static inline int rup(int x, int m) { return (x + m - 1) / m * m; }
+
+// ----------------------------------------------------------------------------
+// small kernels: head + level-0 pack, pyramid pool, encoder pool, out head
+// ----------------------------------------------------------------------------
+// y = x @ W + b per pixel in f32 (model.py:135-143); writes the f32 level-0
+// pyramid (for pooling) and its bf16 copy padded to cp channels.
+__global__ void head_kernel(const float* __restrict__ x, int64_t npix, int cin, int cp,
+                            const float* __restrict__ hw, const float* __restrict__ hb,
+                            int use_head, float* __restrict__ y32,
+                            __nv_bfloat16* __restrict__ y16) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= npix) return;
+  float v[16];
+  for (int c = 0; c < cin; ++c) v[c] = x[p * cin + c];
+  for (int j = 0; j < cp; ++j) {
+    float acc = 0.0f;
+    if (j < cin) {
+      if (use_head) {
+        acc = hb[j];
+        for (int c = 0; c < cin; ++c) acc = fmaf(v[c], hw[c * cin + j], acc);
+      } else {
+        acc = v[j];
+      }
+      y32[p * cin + j] = acc;
+    }
+    y16[p * cp + j] = __float2bfloat16_rn(acc);
+  }
+}
+
+// 2x2 average of an f32 (H,W,C) map (autodiff.py:231-245); writes f32 + bf16 (cp).
+__global__ void pool_f32_kernel(const float* __restrict__ src, int H, int W, int C, int cp,
+                                float* __restrict__ dst32, __nv_bfloat16* __restrict__ dst16) {
+  const int Ho = H / 2, Wo = W / 2;
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= (int64_t)Ho * Wo) return;
+  const int y = (int)(p / Wo), x = (int)(p % Wo);
+  const float* r0 = src + ((int64_t)(2 * y) * W + 2 * x) * C;
+  const float* r1 = r0 + (int64_t)W * C;
+  for (int c = 0; c < cp; ++c) {
+    float m = 0.0f;
+    if (c < C) {
+      m = ((r0[c] + r0[C + c]) + (r1[c] + r1[C + c])) * 0.25f;
+      dst32[p * C + c] = m;
+    }
+    dst16[p * cp + c] = __float2bfloat16_rn(m);
+  }
+}
+
+// 2x2 average of a bf16 (H,W,C) map into bf16 (H/2,W/2,C), 8 channels per thread.
+__global__ void pool_bf16_kernel(const __nv_bfloat16* __restrict__ src, int H, int W, int C,
+                                 __nv_bfloat16* __restrict__ dst) {
+  const int Ho = H / 2, Wo = W / 2, c8n = C / 8;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)Ho * Wo * c8n) return;
+  const int c8 = (int)(t % c8n);
+  const int64_t p = t / c8n;
+  const int y = (int)(p / Wo), x = (int)(p % Wo);
+  const __nv_bfloat16* a = src + ((int64_t)(2 * y) * W + 2 * x) * C + c8 * 8;
+  uint4 q[4];
+  q[0] = *reinterpret_cast<const uint4*>(a);
+  q[1] = *reinterpret_cast<const uint4*>(a + C);
+  q[2] = *reinterpret_cast<const uint4*>(a + (int64_t)W * C);
+  q[3] = *reinterpret_cast<const uint4*>(a + (int64_t)W * C + C);
+  uint4 o;
+  uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
+  for (int i = 0; i < 4; ++i) {
+    float2 s = make_float2(0.f, 0.f);
+    float2 v[4];
+    for (int j = 0; j < 4; ++j)
+      v[j] = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(&q[j])[i]);
+    s.x = ((v[0].x + v[1].x) + (v[2].x + v[3].x)) * 0.25f;
+    s.y = ((v[0].y + v[1].y) + (v[2].y + v[3].y)) * 0.25f;
+    __nv_bfloat162 r = __float22bfloat162_rn(s);
+    ow[i] = *reinterpret_cast<uint32_t*>(&r);
+  }
+  *reinterpret_cast<uint4*>(dst + p * C + c8 * 8) = o;
+}
+
+// logits = x @ out.w + out.b, sigmoid (model.py:189-191), f32 out.
+__global__ void out_head_kernel(const __nv_bfloat16* __restrict__ x, int64_t npix, int C,
+                                int cstride, const float* __restrict__ ow,
+                                const float* __restrict__ ob, int cout, float* __restrict__ out) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= npix) return;
+  const __nv_bfloat16* xp = x + p * cstride;
+  for (int j = 0; j < cout; ++j) {
+    float acc = ob[j];
+    for (int c = 0; c < C; ++c) acc = fmaf(__bfloat162float(xp[c]), ow[c * cout + j], acc);
+    out[p * cout + j] = 1.0f / (1.0f + expf(-acc));
+  }
+}
+
+// ----------------------------------------------------------------------------
+// CUDA-core gated conv (cross-check path)
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ float elu_f(float x) { return x > 0.0f ? x : expm1f(x); }
+__device__ __forceinline__ float sigmoid_f(float x) { return 1.0f / (1.0f + expf(-x)); }
+
+// One thread per (pixel, output channel j): f_j and g_j over 9 taps x cin.
+// Weights: wf/wg f32 [tap][cin_total][cout] (HWIO); bias f32.
+__global__ void gated_conv_simt(ConvArgs a) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t npix = (int64_t)a.H * a.W;
+  if (t >= npix * a.cout) return;
+  const int j = (int)(t % a.cout);
+  const int64_t p = t / a.cout;
+  const int y = (int)(p / a.W), x = (int)(p % a.W);
+  const int cin = a.ca + a.cb;
+  float f = a.bias_f[j], g = a.bias_g[j];
+  for (int ky = 0; ky < 3; ++ky) {
+    const int yy = y + ky - 1;
+    if (yy < 0 || yy >= a.H) continue;
+    for (int kx = 0; kx < 3; ++kx) {
+      const int xx = x + kx - 1;
+      if (xx < 0 || xx >= a.W) continue;
+      const int tap = ky * 3 + kx;
+      const __nv_bfloat16* pa;
+      if (a.a_up2)
+        pa = a.src_a + ((int64_t)(yy / 2) * (a.W / 2) + xx / 2) * a.ca_stride;
+      else
+        pa = a.src_a + ((int64_t)yy * a.W + xx) * a.ca_stride;
+      const float* wf = a.wf32 + ((int64_t)tap * cin) * a.cout + j;
+      const float* wg = a.wg32 + ((int64_t)tap * cin) * a.cout + j;
+      for (int c = 0; c < a.ca; ++c) {
+        const float v = __bfloat162float(pa[c]);
+        f = fmaf(v, wf[(int64_t)c * a.cout], f);
+        g = fmaf(v, wg[(int64_t)c * a.cout], g);
+      }
+      if (a.cb) {
+        const __nv_bfloat16* pb = a.src_b + ((int64_t)yy * a.W + xx) * a.cb_stride;
+        for (int c = 0; c < a.cb; ++c) {
+          const float v = __bfloat162float(pb[c]);
+          f = fmaf(v, wf[(int64_t)(a.ca + c) * a.cout], f);
+          g = fmaf(v, wg[(int64_t)(a.ca + c) * a.cout], g);
+        }
+      }
+    }
+  }
+  a.out[p * a.cout_stride + j] = __float2bfloat16_rn(elu_f(f) * sigmoid_f(g));
+  if (j == 0)  // zero the channel padding so tensor-core consumers read zeros
+    for (int c = a.cout; c < a.cout_stride; ++c) a.out[p * a.cout_stride + c] = __float2bfloat16_rn(0.f);
+}
+
+// ----------------------------------------------------------------------------
+// network object
+// ----------------------------------------------------------------------------
+struct Layer {
+  std::string name;
+  int ca, cb;   // real input channels from source A / source B
+  int cout;
+  // device weights
+  float* wf32 = nullptr;  // [9][ca+cb][cout]
+  float* wg32 = nullptr;
+  float* bf = nullptr;
+  float* bg = nullptr;
+  uint16_t* wtc = nullptr;  // tcgen05-packed bf16 weights (unet_tc.cuh layout)
+  size_t wtc_bytes = 0;
+  std::vector<float> hf, hg, hbf, hbg;  // host staging (HWIO)
+  bool set_f = false, set_g = false, set_bf = false, set_bg = false;
+};
+
+}  // namespace nar
+
+struct nar_unet {
+  nar_unet_config cfg;
+  std::vector<nar::Layer> layers;  // enc0a, enc0b, ..., enc4b, dec3a, ..., dec0b
+  std::map<std::string, int> index;
+  std::vector<float> head_w, head_b, out_w, out_b;
+  float *d_head_w = nullptr, *d_head_b = nullptr, *d_out_w = nullptr, *d_out_b = nullptr;
+  bool uploaded = false;
+  bool simt = false;
+};
+
+namespace nar {
+
+static int width_of(const nar_unet_config& c, int k) {
+  long w = c.base_channels;
+  for (int i = 0; i < k; ++i) w *= c.channel_multiplier;
+  return (int)(w < c.max_channels ? w : c.max_channels);
+}
+
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// channel stride of level-k activations (multiple of 16: whole K=16 MMA steps)
+static int stride_of(const nar_unet_config& c, int k) { return rup(width_of(c, k), 16); }
+
+// workspace carve-up for one (H, W)
+struct Plan {
+  int L;
+  int H[8], W[8];
+  int cinp;             // padded input channel count
+  size_t off_pyr32[8], off_pyr16[8], off_skip[8], off_pool[8], off_tmp[8], off_x[8];
+  size_t total;
+};
+
+static Plan make_plan(const nar_unet& n, int H, int W) {
+  Plan p;
+  p.L = n.cfg.levels;
+  p.cinp = rup(n.cfg.input_channels, 16);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + bytes, 256);
+    return o;
+  };
+  for (int k = 0; k < p.L; ++k) {
+    p.H[k] = H >> k;
+    p.W[k] = W >> k;
+    const size_t px = (size_t)p.H[k] * p.W[k];
+    const int w = stride_of(n.cfg, k);
+    p.off_pyr32[k] = take(px * n.cfg.input_channels * 4);
+    p.off_pyr16[k] = take(px * p.cinp * 2);
+    p.off_skip[k] = take(px * w * 2);
+    p.off_tmp[k] = take(px * w * 2);
+    p.off_x[k] = take(px * w * 2);
+    p.off_pool[k] = k + 1 < p.L ? take(px / 4 * w * 2) : 0;
+  }
+  p.total = off + 256;
+  return p;
+}
+
+static int upload(nar_unet* n) {
+  if (n->uploaded) return NAR_OK;
+  auto dup = [](const std::vector<float>& v, float** d) -> int {
+    if (cudaMalloc(d, v.size() * 4 + 4) != cudaSuccess) return 1;
+    cudaMemcpy(*d, v.data(), v.size() * 4, cudaMemcpyHostToDevice);
+    return 0;
+  };
+  const int cin = n->cfg.input_channels;
+  if (n->cfg.use_descriptor_head) {
+    if (n->head_w.size() != (size_t)cin * cin || n->head_b.size() != (size_t)cin)
+      return set_error(NAR_ERR_CONFIG, "head parameters not set");
+    if (dup(n->head_w, &n->d_head_w) || dup(n->head_b, &n->d_head_b))
+      return set_error(NAR_ERR_NOMEM, "weight upload failed");
+  }
+  if (n->out_w.empty() || n->out_b.empty())
+    return set_error(NAR_ERR_CONFIG, "out parameters not set");
+  if (dup(n->out_w, &n->d_out_w) || dup(n->out_b, &n->d_out_b))
+    return set_error(NAR_ERR_NOMEM, "weight upload failed");
+  for (auto& l : n->layers) {
+    if (!(l.set_f && l.set_g && l.set_bf && l.set_bg)) {
+      std::string m = "parameters of " + l.name + " not set";
+      return set_error(NAR_ERR_CONFIG, m.c_str());
+    }
+    if (dup(l.hf, &l.wf32) || dup(l.hg, &l.wg32) || dup(l.hbf, &l.bf) || dup(l.hbg, &l.bg))
+      return set_error(NAR_ERR_NOMEM, "weight upload failed");
+    std::vector<uint16_t> packed;
+    tc_pack_weights(l.hf, l.hg, l.ca, l.cb, l.cout, packed);
+    l.wtc_bytes = packed.size() * 2;
+    if (cudaMalloc(&l.wtc, l.wtc_bytes) != cudaSuccess)
+      return set_error(NAR_ERR_NOMEM, "weight upload failed");
+    cudaMemcpy(l.wtc, packed.data(), l.wtc_bytes, cudaMemcpyHostToDevice);
+  }
+  if (cudaGetLastError() != cudaSuccess) return set_error(NAR_ERR_CUDA, "weight upload failed");
+  n->uploaded = true;
+  return NAR_OK;
+}
+
+static int run_conv(nar_unet* n, Layer& l, const __nv_bfloat16* src_a, int ca_stride, int a_up2,
+                    const __nv_bfloat16* src_b, int cb_stride, int H, int W,
+                    __nv_bfloat16* out, cudaStream_t st) {
+  ConvArgs a;
+  memset(&a, 0, sizeof(a));
+  a.src_a = src_a;
+  a.src_b = src_b;
+  a.ca = l.ca;
+  a.cb = l.cb;
+  a.ca_stride = ca_stride;
+  a.cb_stride = cb_stride;
+  a.a_up2 = a_up2;
+  a.H = H;
+  a.W = W;
+  a.cout = l.cout;
+  a.cout_stride = rup(l.cout, 16);
+  a.wf32 = l.wf32;
+  a.wg32 = l.wg32;
+  a.bias_f = l.bf;
+  a.bias_g = l.bg;
+  a.wtc = reinterpret_cast<const __nv_bfloat16*>(l.wtc);
+  a.out = out;
+  if (n->simt) {
+    const int64_t tot = (int64_t)H * W * l.cout;
+    gated_conv_simt<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(a);
+    return check_launch(l.name.c_str());
+  }
+  return tc_launch_gated_conv(a, st);
+}
+
+}  // namespace nar
+
+using namespace nar;
+
+extern "C" {
+
+int nar_unet_create(const nar_unet_config* cfg, nar_unet** out) {
+  if (!cfg || !out) return set_error(NAR_ERR_INVALID, "NULL argument");
+  if (cfg->input_channels < 1 || cfg->input_channels > NAR_MAX_CHANNELS)
+    return set_error(NAR_ERR_CONFIG, "input_channels must be in [1, 16]");
+  if (cfg->levels < 1 || cfg->levels > 7) return set_error(NAR_ERR_CONFIG, "levels out of range");
+  if (cfg->output_channels < 1 || cfg->output_channels > 16)
+    return set_error(NAR_ERR_CONFIG, "output_channels out of range");
+  nar_unet* n = new nar_unet();
+  n->cfg = *cfg;
+  const char* env = getenv("NAR_UNET_SIMT");
+  n->simt = env && env[0] == '1';
+  const int cin = cfg->input_channels;
+  for (int k = 0; k < cfg->levels; ++k) {
+    const int w = width_of(*cfg, k);
+    if (w < 1 || w > 128) {
+      delete n;
+      return set_error(NAR_ERR_CONFIG, "level widths must be in [1, 128]");
+    }
+    Layer a;
+    a.name = "enc" + std::to_string(k) + "a";
+    a.ca = k == 0 ? cin : width_of(*cfg, k - 1);
+    a.cb = k == 0 ? 0 : cin;
+    a.cout = w;
+    Layer b;
+    b.name = "enc" + std::to_string(k) + "b";
+    b.ca = w;
+    b.cb = 0;
+    b.cout = w;
+    n->layers.push_back(a);
+    n->layers.push_back(b);
+  }
+  for (int k = cfg->levels - 2; k >= 0; --k) {
+    const int w = width_of(*cfg, k);
+    Layer a;
+    a.name = "dec" + std::to_string(k) + "a";
+    a.ca = width_of(*cfg, k + 1);
+    a.cb = w;
+    a.cout = w;
+    Layer b;
+    b.name = "dec" + std::to_string(k) + "b";
+    b.ca = w;
+    b.cb = 0;
+    b.cout = w;
+    n->layers.push_back(a);
+    n->layers.push_back(b);
+  }
+  for (size_t i = 0; i < n->layers.size(); ++i) n->index[n->layers[i].name] = (int)i;
+  *out = n;
+  return NAR_OK;
+}
+
+int nar_unet_destroy(nar_unet* n) {
+  if (!n) return NAR_OK;
+  cudaFree(n->d_head_w);
+  cudaFree(n->d_head_b);
+  cudaFree(n->d_out_w);
+  cudaFree(n->d_out_b);
+  for (auto& l : n->layers) {
+    cudaFree(l.wf32);
+    cudaFree(l.wg32);
+    cudaFree(l.bf);
+    cudaFree(l.bg);
+    cudaFree(l.wtc);
+  }
+  delete n;
+  return NAR_OK;
+}
+
+int nar_unet_set_param(nar_unet* n, const char* name, const float* host, int64_t numel) {
+  if (!n || !name || (!host && numel)) return set_error(NAR_ERR_INVALID, "NULL argument");
+  std::string s(name);
+  const int cin = n->cfg.input_channels;
+  auto want = [&](int64_t expect) -> int {
+    if (numel != expect) {
+      std::string m = "parameter " + s + " has " + std::to_string(numel) + " values, expected " +
+                      std::to_string(expect);
+      return set_error(NAR_ERR_CONFIG, m.c_str());
+    }
+    return NAR_OK;
+  };
+  int rc;
+  n->uploaded = false;
+  if (s == "head.w") {
+    if ((rc = want((int64_t)cin * cin))) return rc;
+    n->head_w.assign(host, host + numel);
+    return NAR_OK;
+  }
+  if (s == "head.b") {
+    if ((rc = want(cin))) return rc;
+    n->head_b.assign(host, host + numel);
+    return NAR_OK;
+  }
+  const int w0 = width_of(n->cfg, 0);
+  if (s == "out.w") {
+    if ((rc = want((int64_t)w0 * n->cfg.output_channels))) return rc;
+    n->out_w.assign(host, host + numel);
+    return NAR_OK;
+  }
+  if (s == "out.b") {
+    if ((rc = want(n->cfg.output_channels))) return rc;
+    n->out_b.assign(host, host + numel);
+    return NAR_OK;
+  }
+  const size_t dot = s.find('.');
+  if (dot == std::string::npos || !n->index.count(s.substr(0, dot))) {
+    std::string m = "unknown parameter " + s;
+    return set_error(NAR_ERR_CONFIG, m.c_str());
+  }
+  Layer& l = n->layers[n->index[s.substr(0, dot)]];
+  const std::string field = s.substr(dot + 1);
+  const int64_t wn = (int64_t)9 * (l.ca + l.cb) * l.cout;
+  if (field == "f_w") {
+    if ((rc = want(wn))) return rc;
+    l.hf.assign(host, host + numel);
+    l.set_f = true;
+  } else if (field == "g_w") {
+    if ((rc = want(wn))) return rc;
+    l.hg.assign(host, host + numel);
+    l.set_g = true;
+  } else if (field == "f_b") {
+    if ((rc = want(l.cout))) return rc;
+    l.hbf.assign(host, host + numel);
+    l.set_bf = true;
+  } else if (field == "g_b") {
+    if ((rc = want(l.cout))) return rc;
+    l.hbg.assign(host, host + numel);
+    l.set_bg = true;
+  } else {
+    std::string m = "unknown parameter " + s;
+    return set_error(NAR_ERR_CONFIG, m.c_str());
+  }
+  return NAR_OK;
+}
+
+int nar_unet_workspace_bytes(const nar_unet* n, int32_t height, int32_t width, size_t* bytes) {
+  if (!n || !bytes) return set_error(NAR_ERR_INVALID, "NULL argument");
+  const int div = 1 << (n->cfg.levels - 1);
+  if (height <= 0 || width <= 0 || height % div || width % div)
+    return set_error(NAR_ERR_INVALID, "spatial dims not divisible by 2^(levels-1)");
+  *bytes = make_plan(*n, height, width).total;
+  return NAR_OK;
+}
+
+int nar_unet_forward(nar_unet* n, const float* in, int32_t H, int32_t W, float* out, void* ws,
+                     size_t ws_bytes, void* stream) {
+  if (!n || !in || !out || !ws) return set_error(NAR_ERR_INVALID, "NULL argument");
+  const int div = 1 << (n->cfg.levels - 1);
+  if (H <= 0 || W <= 0 || H % div || W % div)
+    return set_error(NAR_ERR_INVALID, "spatial dims not divisible by 2^(levels-1)");
+  const Plan p = make_plan(*n, H, W);
+  if (ws_bytes < p.total) return set_error(NAR_ERR_INVALID, "workspace too small");
+  int rc = upload(n);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  auto bf = [&](size_t off) { return reinterpret_cast<__nv_bfloat16*>(base + off); };
+  auto f32 = [&](size_t off) { return reinterpret_cast<float*>(base + off); };
+  const int cin = n->cfg.input_channels, L = p.L;
+
+  const int64_t np0 = (int64_t)H * W;
+  head_kernel<<<(unsigned)((np0 + 255) / 256), 256, 0, st>>>(
+      in, np0, cin, p.cinp, n->d_head_w, n->d_head_b, n->cfg.use_descriptor_head,
+      f32(p.off_pyr32[0]), bf(p.off_pyr16[0]));
+  for (int k = 1; k < L; ++k) {
+    const int64_t npk = (int64_t)p.H[k] * p.W[k];
+    pool_f32_kernel<<<(unsigned)((npk + 255) / 256), 256, 0, st>>>(
+        f32(p.off_pyr32[k - 1]), p.H[k - 1], p.W[k - 1], cin, p.cinp, f32(p.off_pyr32[k]),
+        bf(p.off_pyr16[k]));
+  }
+  if ((rc = check_launch("pyramid"))) return rc;
+
+  int li = 0;
+  for (int k = 0; k < L; ++k) {
+    Layer& la = n->layers[li++];
+    Layer& lb = n->layers[li++];
+    if (k == 0) {
+      rc = run_conv(n, la, bf(p.off_pyr16[0]), p.cinp, 0, nullptr, 0, p.H[0], p.W[0],
+                    bf(p.off_tmp[0]), st);
+    } else {
+      rc = run_conv(n, la, bf(p.off_pool[k - 1]), stride_of(n->cfg, k - 1), 0,
+                    bf(p.off_pyr16[k]), p.cinp, p.H[k], p.W[k], bf(p.off_tmp[k]), st);
+    }
+    if (rc) return rc;
+    rc = run_conv(n, lb, bf(p.off_tmp[k]), stride_of(n->cfg, k), 0, nullptr, 0, p.H[k], p.W[k],
+                  bf(p.off_skip[k]), st);
+    if (rc) return rc;
+    if (k + 1 < L) {
+      const int w = stride_of(n->cfg, k);
+      const int64_t t = (int64_t)p.H[k + 1] * p.W[k + 1] * (w / 8);
+      pool_bf16_kernel<<<(unsigned)((t + 255) / 256), 256, 0, st>>>(
+          bf(p.off_skip[k]), p.H[k], p.W[k], w, bf(p.off_pool[k]));
+      if ((rc = check_launch("pool"))) return rc;
+    }
+  }
+  const __nv_bfloat16* x = bf(p.off_skip[L - 1]);
+  for (int k = L - 2; k >= 0; --k) {
+    Layer& la = n->layers[li++];
+    Layer& lb = n->layers[li++];
+    rc = run_conv(n, la, x, stride_of(n->cfg, k + 1), 1, bf(p.off_skip[k]), stride_of(n->cfg, k),
+                  p.H[k], p.W[k], bf(p.off_tmp[k]), st);
+    if (rc) return rc;
+    rc = run_conv(n, lb, bf(p.off_tmp[k]), stride_of(n->cfg, k), 0, nullptr, 0, p.H[k], p.W[k],
+                  bf(p.off_x[k]), st);
+    if (rc) return rc;
+    x = bf(p.off_x[k]);
+  }
+  out_head_kernel<<<(unsigned)((np0 + 127) / 128), 128, 0, st>>>(
+      x, np0, width_of(n->cfg, 0), stride_of(n->cfg, 0), n->d_out_w, n->d_out_b,
+      n->cfg.output_channels, out);
+  return check_launch("out_head");
+}
+
+}  // extern "C"

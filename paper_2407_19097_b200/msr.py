@@ -1,0 +1,444 @@
+"""Multi-Stream Rasterizer on B200: render (project + early-z) and resolve.
+
+Reference API kept (pkg/src/nar/msr/rasterizer.py:27-188):
+``StreamSelection``, ``FeatureImage``, ``rasterize(pc, cam, sel, threads=None,
+backend=None)``.  ``rasterize`` on a host ``PointCloud`` is the drop-in: it
+uploads the points (chunked H2D overlapped with the render kernel), renders
+into a device keybuf, resolves on the device and returns host planes that are
+bit-identical to the reference's for the rgb / d / scalar / coverage channels
+and the index / depth / coverage planes (vel channels: <= 1 f32 ulp, see
+DESIGN.md).
+
+The device-resident path for throughput (the benchmark's ``value``) is
+``DeviceCloud`` + ``Renderer``: the cloud is uploaded once, each frame runs
+``nar_render`` once per point buffer -- one CUDA stream per data stream, all
+folding into one keybuf with atomics -- then one ``nar_resolve`` launch that
+also re-clears the keybuf for the next frame.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._kernels import EMPTY_KEY, _resolve
+from .errors import ConfigurationError
+from .geometry import CameraPose, PointCloud
+
+MAX_CHANNELS = 16
+VEL2D_CHANNELS = ("v2x", "v2y", "v2t", "v2m")
+VEL3D_CHANNELS = ("v3x", "v3y", "v3z", "v3m")
+_FMT = {"u8": _lib.FMT_U8, "f32": _lib.FMT_F32}
+
+
+@dataclass(frozen=True)
+class StreamSelection:
+    """Which point attributes become raster channels (rasterizer.py:27-91)."""
+
+    rgb: bool = True
+    depth: bool = False
+    vel2d: bool = False
+    vel3d: bool = False
+    scalars: tuple[str, ...] = ()
+    coverage_channel: bool = False
+    velocity_scale: float = 1.0
+    rgb_stream: str = "rgb"
+    velocity_stream: str = "velocity"
+
+    def channel_names(self, pc=None) -> tuple[str, ...]:
+        out: list[str] = []
+        if self.rgb:
+            out.extend(("r", "g", "b"))
+        if self.depth:
+            out.append("d")
+        if self.vel2d:
+            out.extend(VEL2D_CHANNELS)
+        if self.vel3d:
+            out.extend(VEL3D_CHANNELS)
+        for name in self.scalars:
+            ar = pc.stream(name).arity if (pc is not None and pc.has_stream(name)) else 1
+            out.extend([name] if ar == 1 else [f"{name}{i}" for i in range(ar)])
+        if self.coverage_channel:
+            out.append("coverage")
+        return tuple(out)
+
+    def validate(self, pc) -> None:
+        if self.rgb and not pc.has_stream(self.rgb_stream):
+            raise ConfigurationError(f"selection needs stream {self.rgb_stream!r}")
+        if (self.vel2d or self.vel3d) and not pc.has_stream(self.velocity_stream):
+            raise ConfigurationError(f"selection needs stream {self.velocity_stream!r}")
+        for name in self.scalars:
+            if not pc.has_stream(name):
+                raise ConfigurationError(f"selection needs stream {name!r}")
+        n = len(self.channel_names(pc))
+        if n > MAX_CHANNELS:
+            raise ConfigurationError(f"{n} channels exceed the limit of {MAX_CHANNELS}")
+
+    def needed_streams(self) -> list[str]:
+        names = []
+        if self.rgb:
+            names.append(self.rgb_stream)
+        if self.vel2d or self.vel3d:
+            names.append(self.velocity_stream)
+        names.extend(self.scalars)
+        return list(dict.fromkeys(names))
+
+    def to_dict(self) -> dict:
+        return {"rgb": self.rgb, "depth": self.depth, "vel2d": self.vel2d, "vel3d": self.vel3d,
+                "scalars": list(self.scalars), "coverage_channel": self.coverage_channel,
+                "velocity_scale": self.velocity_scale, "rgb_stream": self.rgb_stream,
+                "velocity_stream": self.velocity_stream}
+
+    @staticmethod
+    def from_dict(d: dict) -> "StreamSelection":
+        d = dict(d)
+        d["scalars"] = tuple(d.get("scalars", ()))
+        return StreamSelection(**d)
+
+
+@dataclass(eq=False)
+class FeatureImage:
+    """Raster output (rasterizer.py:94-113): (H, W, C) f32 planes + bookkeeping."""
+
+    width: int
+    height: int
+    channel_names: tuple[str, ...]
+    data: np.ndarray
+    coverage: np.ndarray
+    index_plane: np.ndarray
+    depth: np.ndarray = field(default=None)
+
+    def plane(self, name: str) -> np.ndarray:
+        return self.data[:, :, self.channel_names.index(name)]
+
+    def rgb(self) -> np.ndarray:
+        if not {"r", "g", "b"} <= set(self.channel_names):
+            raise ConfigurationError("feature image has no RGB channels")
+        return np.stack([self.plane("r"), self.plane("g"), self.plane("b")], axis=-1)
+
+
+# ---------------------------------------------------------------------------
+# device-resident clouds
+# ---------------------------------------------------------------------------
+class _StreamMeta:
+    __slots__ = ("name", "format", "arity")
+
+    def __init__(self, name, fmt, arity):
+        self.name, self.format, self.arity = name, fmt, arity
+
+
+class DeviceCloud:
+    """Point buffers resident in HBM; each buffer is one data stream / segment.
+
+    ``segments[k]`` = dict(begin, positions (n,3) f32 tensor, streams {name: tensor}).
+    Segment k's points carry global indices ``begin .. begin+n-1`` (the base
+    index of the reference's chunked render, _kernels/__init__.py:81-87).
+    """
+
+    def __init__(self, segments: list[dict], meta: dict[str, _StreamMeta], device):
+        if len(segments) > _lib.MAX_SEGMENTS:
+            raise ConfigurationError(f"at most {_lib.MAX_SEGMENTS} point buffers per cloud")
+        self.segments = segments
+        self.meta = meta
+        self.device = device
+        for s in segments:
+            s.setdefault("count", int(s["positions"].shape[0]) if s.get("positions") is not None else 0)
+        self.count = sum(s["count"] for s in segments)
+        end = max((s["begin"] + s["count"] for s in segments), default=0)
+        if end > 1 << 32:
+            raise ConfigurationError("global point indices must fit in 32 bits")
+
+    # -- construction -------------------------------------------------------
+    @staticmethod
+    def _upload(arr: np.ndarray, device):
+        import torch
+
+        t = torch.from_numpy(np.ascontiguousarray(arr))
+        return t.to(device, non_blocking=True)
+
+    @classmethod
+    def from_host(cls, pc: PointCloud, device=None, streams: list[str] | None = None,
+                  begin: int = 0) -> "DeviceCloud":
+        return cls.from_clouds([pc], device=device, streams=streams, begins=[begin])
+
+    @classmethod
+    def from_clouds(cls, clouds: list[PointCloud], device=None, streams: list[str] | None = None,
+                    begins: list[int] | None = None) -> "DeviceCloud":
+        """Multi-stream cloud: one device buffer per input cloud.  Default base
+        indices are the running sums of the counts, so rendering equals the
+        reference ``rasterize`` of the concatenated cloud."""
+        import torch
+
+        device = torch.device(device or "cuda")
+        if begins is None:
+            begins, acc = [], 0
+            for pc in clouds:
+                begins.append(acc)
+                acc += pc.count
+        meta: dict[str, _StreamMeta] = {}
+        segs = []
+        for pc, b in zip(clouds, begins):
+            names = streams if streams is not None else pc.stream_names()
+            st = {}
+            for name in names:
+                s = pc.stream(name)
+                m = meta.setdefault(name, _StreamMeta(name, s.format, s.arity))
+                if (m.format, m.arity) != (s.format, s.arity):
+                    raise ConfigurationError(f"stream {name!r} differs between point buffers")
+                st[name] = cls._upload(s.data, device)
+            segs.append({"begin": int(b), "positions": cls._upload(pc.positions, device),
+                         "streams": st})
+        return cls(segs, meta, device)
+
+    @classmethod
+    def from_tensors(cls, positions, streams: dict | None = None, formats: dict | None = None,
+                     begin: int = 0) -> "DeviceCloud":
+        """Wrap device tensors generated in place (no host copy)."""
+        meta, st = {}, {}
+        for name, t in (streams or {}).items():
+            fmt = (formats or {}).get(name, "u8" if str(t.dtype) == "torch.uint8" else "f32")
+            meta[name] = _StreamMeta(name, fmt, int(t.shape[1]))
+            st[name] = t
+        return cls([{"begin": int(begin), "positions": positions, "streams": st}], meta,
+                   positions.device)
+
+    def has_stream(self, name: str) -> bool:
+        return name in self.meta
+
+    def stream(self, name: str) -> _StreamMeta:
+        if name not in self.meta:
+            raise KeyError(f"no stream named {name!r}")
+        return self.meta[name]
+
+
+@dataclass
+class DeviceFeatureImage:
+    """Device tensors of one resolved frame (see FeatureImage)."""
+
+    width: int
+    height: int
+    channel_names: tuple[str, ...]
+    data: object          # torch (data_h, data_w, C) f32 (padded extent)
+    coverage: object      # torch (H, W) u8
+    index_plane: object   # torch (H, W) i64
+    depth: object         # torch (H, W) f32
+
+    def to_host(self) -> FeatureImage:
+        d = self.data[: self.height, : self.width].cpu().numpy()
+        return FeatureImage(self.width, self.height, self.channel_names, np.ascontiguousarray(d),
+                            self.coverage.cpu().numpy(), self.index_plane.cpu().numpy(),
+                            self.depth.cpu().numpy())
+
+
+def _selection_struct(sel: StreamSelection, cloud) -> "_lib.Selection":
+    s = _lib.Selection()
+    s.rgb, s.depth, s.vel2d, s.vel3d = int(sel.rgb), int(sel.depth), int(sel.vel2d), int(sel.vel3d)
+    s.coverage_channel = int(sel.coverage_channel)
+    if sel.rgb:
+        m = cloud.stream(sel.rgb_stream)
+        s.rgb_format, s.rgb_arity = _FMT[m.format], m.arity
+        if not (m.arity == 1 or m.arity >= 3):
+            raise ValueError(f"rgb stream of arity {m.arity} cannot fill 3 channels")
+    if sel.vel2d or sel.vel3d:
+        m = cloud.stream(sel.velocity_stream)
+        s.vel_format, s.vel_arity = _FMT[m.format], m.arity
+    if len(sel.scalars) > _lib.MAX_SCALARS:
+        raise ConfigurationError("too many scalar streams")
+    s.n_scalars = len(sel.scalars)
+    for q, name in enumerate(sel.scalars):
+        m = cloud.stream(name)
+        s.scalar_format[q], s.scalar_arity[q] = _FMT[m.format], m.arity
+    s.velocity_scale = float(sel.velocity_scale)
+    return s
+
+
+def _segments_struct(cloud: DeviceCloud, sel: StreamSelection):
+    arr = (_lib.Segment * _lib.MAX_SEGMENTS)()
+    for k, sg in enumerate(cloud.segments):
+        a = arr[k]
+        a.begin = sg["begin"]
+        a.count = sg["count"]
+        a.positions = sg["positions"].data_ptr() if sg.get("positions") is not None else None
+        st = sg["streams"]
+        if sel.rgb:
+            a.rgb = st[sel.rgb_stream].data_ptr()
+        if sel.vel2d or sel.vel3d:
+            a.velocity = st[sel.velocity_stream].data_ptr()
+        for q, name in enumerate(sel.scalars):
+            a.scalars[q] = st[name].data_ptr()
+    return arr
+
+
+class Renderer:
+    """Per-resolution frame state: the u64 keybuf (kept EMPTY between frames)
+    and the CUDA streams used for multi-stream rendering."""
+
+    def __init__(self, width: int, height: int, device=None, signed_keys: bool = False,
+                 pad_multiple: int | None = None):
+        import torch
+
+        self.width, self.height = int(width), int(height)
+        self.device = torch.device(device or "cuda")
+        self.domain = _lib.KEYS_SIGNED if signed_keys else _lib.KEYS_UNSIGNED
+        self.empty = (_lib.EMPTY_KEY ^ _lib.SIGN_FLIP) if signed_keys else _lib.EMPTY_KEY
+        npix = self.width * self.height
+        self.keybuf = torch.empty(npix, dtype=torch.int64, device=self.device)
+        self.pad_multiple = pad_multiple
+        self._streams: list = []
+        self.clear()
+
+    @property
+    def npix(self) -> int:
+        return self.width * self.height
+
+    def clear(self, stream=None) -> None:
+        _lib.call("nar_keybuf_fill", self.keybuf.data_ptr(), self.npix,
+                  C.c_uint64(self.empty), _lib.stream_handle(stream))
+
+    def _check_cam(self, cam: CameraPose):
+        i = cam.intrinsics
+        if (i.width, i.height) != (self.width, self.height):
+            raise ValueError("camera resolution differs from the renderer's")
+        return cam.kernel_camera()
+
+    def render(self, cloud: DeviceCloud, cam: CameraPose, stream=None,
+               multi_stream: bool = True) -> None:
+        """Fold every point buffer of ``cloud`` into the keybuf; with several
+        buffers and ``multi_stream`` each renders on its own CUDA stream."""
+        import torch
+
+        kc = self._check_cam(cam)
+        main = stream or torch.cuda.current_stream(self.device)
+        segs = cloud.segments
+        if len(segs) <= 1 or not multi_stream:
+            for sg in segs:
+                _lib.call("nar_render", self.keybuf.data_ptr(), sg["positions"].data_ptr(),
+                          int(sg["positions"].shape[0]), C.c_uint64(sg["begin"]), C.byref(kc),
+                          self.domain, int(main.cuda_stream))
+            return
+        while len(self._streams) < len(segs):
+            self._streams.append(torch.cuda.Stream(self.device))
+        start = torch.cuda.Event()
+        start.record(main)
+        for sg, st in zip(segs, self._streams):
+            st.wait_event(start)
+            _lib.call("nar_render", self.keybuf.data_ptr(), sg["positions"].data_ptr(),
+                      int(sg["positions"].shape[0]), C.c_uint64(sg["begin"]), C.byref(kc),
+                      self.domain, int(st.cuda_stream))
+        for st in self._streams[: len(segs)]:
+            ev = torch.cuda.Event()
+            ev.record(st)
+            main.wait_event(ev)
+
+    def alloc_outputs(self, n_channels: int):
+        import torch
+
+        H, W = self.height, self.width
+        m = self.pad_multiple or 1
+        ph, pw = H + (-H) % m, W + (-W) % m
+        dev = self.device
+        return {"data": torch.empty((ph, pw, n_channels), dtype=torch.float32, device=dev),
+                "coverage": torch.empty((H, W), dtype=torch.uint8, device=dev),
+                "index_plane": torch.empty((H, W), dtype=torch.int64, device=dev),
+                "depth": torch.empty((H, W), dtype=torch.float32, device=dev)}
+
+    def resolve(self, cloud: DeviceCloud, cam: CameraPose, sel: StreamSelection, out=None,
+                stream=None, clear: bool = True, owner_only: bool = False) -> DeviceFeatureImage:
+        sel.validate(cloud)
+        kc = self._check_cam(cam)
+        names = sel.channel_names(cloud)
+        if out is None:
+            out = self.alloc_outputs(len(names))
+        ro = _lib.ResolveOut()
+        ro.data = out["data"].data_ptr()
+        ro.data_h, ro.data_w = int(out["data"].shape[0]), int(out["data"].shape[1])
+        ro.coverage = out["coverage"].data_ptr()
+        ro.index_plane = out["index_plane"].data_ptr()
+        ro.depth = out["depth"].data_ptr()
+        ro.owner_only, ro.clear_keybuf = int(owner_only), int(clear)
+        s = _selection_struct(sel, cloud)
+        segs = _segments_struct(cloud, sel)
+        _lib.call("nar_resolve", self.keybuf.data_ptr(), C.byref(kc), self.domain, C.byref(s),
+                  segs, len(cloud.segments), C.byref(ro), _lib.stream_handle(stream))
+        return DeviceFeatureImage(self.width, self.height, names, out["data"], out["coverage"],
+                                  out["index_plane"], out["depth"])
+
+    def rasterize(self, cloud: DeviceCloud, cam: CameraPose, sel: StreamSelection, out=None,
+                  stream=None) -> DeviceFeatureImage:
+        self.render(cloud, cam, stream=stream)
+        return self.resolve(cloud, cam, sel, out=out, stream=stream)
+
+    def keys(self) -> np.ndarray:
+        """Current keybuf as host uint64 in the reference (unsigned) layout."""
+        k = self.keybuf.cpu().numpy().view(np.uint64)
+        if self.domain == _lib.KEYS_SIGNED:
+            k = k ^ np.uint64(_lib.SIGN_FLIP)
+        return k
+
+
+_renderers: dict = {}
+
+
+def _renderer_for(width: int, height: int, device) -> Renderer:
+    key = (width, height, str(device))
+    r = _renderers.get(key)
+    if r is None:
+        if len(_renderers) > 8:
+            _renderers.clear()
+        r = _renderers[key] = Renderer(width, height, device)
+    return r
+
+
+def rasterize(pc: PointCloud, cam: CameraPose, sel: StreamSelection, threads: int | None = None,
+              backend: str | None = None) -> FeatureImage:
+    """Render + resolve a host point cloud on the GPU (rasterizer.py:123-188).
+
+    ``threads`` is accepted for signature compatibility and ignored.  Points
+    and the selected streams are copied host->device inside this call; pass a
+    ``PointCloud(..., pinned=True)`` for async DMA copies.
+    """
+    import torch
+
+    _resolve(backend)
+    sel.validate(pc)
+    intr = cam.intrinsics
+    W, H = intr.width, intr.height
+    dev = torch.device("cuda", torch.cuda.current_device())
+    r = _renderer_for(W, H, dev)
+    main = torch.cuda.current_stream(dev)
+    kc = cam.kernel_camera()
+    names = sel.needed_streams()
+    # Attribute streams go up on a side stream while the points stream through
+    # nar_render_host's chunk pipeline on the main stream.
+    side = torch.cuda.Stream(dev)
+    side.wait_stream(main)
+    with torch.cuda.stream(side):
+        segs_streams = {n: torch.from_numpy(pc.stream(n).data).to(dev, non_blocking=True)
+                        for n in names}
+        pos_dev = (torch.from_numpy(pc.positions).to(dev, non_blocking=True)
+                   if sel.vel2d else None)
+    if pos_dev is None:
+        _lib.call("nar_render_host", r.keybuf.data_ptr(), pc.positions.ctypes.data, pc.count,
+                  C.c_uint64(0), C.byref(kc), r.domain, int(main.cuda_stream))
+    else:
+        main.wait_stream(side)
+        _lib.call("nar_render", r.keybuf.data_ptr(), pos_dev.data_ptr(), pc.count, C.c_uint64(0),
+                  C.byref(kc), r.domain, int(main.cuda_stream))
+    main.wait_stream(side)
+    meta = {n: _StreamMeta(n, pc.stream(n).format, pc.stream(n).arity) for n in names}
+    cloud = DeviceCloud([{"begin": 0, "count": pc.count, "positions": pos_dev,
+                          "streams": segs_streams}], meta, dev)
+    res = r.resolve(cloud, cam, sel, stream=main)
+    host = {}
+    for k in ("data", "coverage", "index_plane", "depth"):
+        t = getattr(res, k)
+        host[k] = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        host[k].copy_(t, non_blocking=True)
+    main.synchronize()  # also keeps the uploaded tensors alive until consumed
+    names_out = sel.channel_names(pc)
+    return FeatureImage(W, H, names_out, host["data"].numpy()[:H, :W].copy(),
+                        host["coverage"].numpy().copy(), host["index_plane"].numpy().copy(),
+                        host["depth"].numpy().copy())

@@ -1,0 +1,246 @@
+"""Gated U-Net post-processing network on B200 tcgen05 tensor cores.
+
+Reference API kept (pkg/src/nar/neural/model.py): ``UNetConfig``,
+``init_params``, ``pad_to_multiple``, ``build_pyramid``-compatible shapes and
+``forward(features, params, config)``.  The forward pass runs entirely in
+libnar_b200.so (``nar_unet_*``): bf16 activations and weights, f32
+accumulation in TMEM, one implicit-GEMM kernel per gated conv with the
+elu(f)*sigmoid(g) epilogue fused, concat / 2x2 average-pool / nearest
+upsample fused into the operand loads.  Parity contract vs the f32 reference:
+PSNR >= 50 dB and max |err| <= 2e-2 (tests/test_unet_gpu.py).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import hashlib
+import json
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import ConfigurationError
+
+PYRAMID_LEVELS = 5
+
+
+@dataclass(frozen=True)
+class UNetConfig:
+    """Network shape (model.py:26-62); widths min(base * mult^k, max)."""
+
+    input_channels: int
+    channel_names: tuple[str, ...] = ()
+    levels: int = PYRAMID_LEVELS
+    base_channels: int = 16
+    channel_multiplier: int = 2
+    max_channels: int = 128
+    output_channels: int = 3
+    use_descriptor_head: bool = True
+    init_seed: int = 0
+
+    def width(self, level: int) -> int:
+        return min(self.base_channels * self.channel_multiplier ** level, self.max_channels)
+
+    def to_dict(self) -> dict:
+        return {"input_channels": self.input_channels, "channel_names": list(self.channel_names),
+                "levels": self.levels, "base_channels": self.base_channels,
+                "channel_multiplier": self.channel_multiplier, "max_channels": self.max_channels,
+                "output_channels": self.output_channels,
+                "use_descriptor_head": self.use_descriptor_head, "init_seed": self.init_seed}
+
+    @staticmethod
+    def from_dict(d: dict) -> "UNetConfig":
+        d = dict(d)
+        d["channel_names"] = tuple(d.get("channel_names", ()))
+        return UNetConfig(**d)
+
+    def hash(self) -> str:
+        return hashlib.sha256(json.dumps(self.to_dict(), sort_keys=True).encode()).hexdigest()
+
+
+def layer_names(cfg: UNetConfig) -> list[str]:
+    enc = [f"enc{k}{s}" for k in range(cfg.levels) for s in "ab"]
+    dec = [f"dec{k}{s}" for k in range(cfg.levels - 2, -1, -1) for s in "ab"]
+    return enc + dec
+
+
+def layer_shapes(cfg: UNetConfig) -> dict[str, tuple[int, int]]:
+    """(c_in, c_out) of every gated conv (model.py:89-97)."""
+    cin, w = cfg.input_channels, cfg.width
+    out = {}
+    for k in range(cfg.levels):
+        out[f"enc{k}a"] = (cin if k == 0 else w(k - 1) + cin, w(k))
+        out[f"enc{k}b"] = (w(k), w(k))
+    for k in range(cfg.levels - 2, -1, -1):
+        out[f"dec{k}a"] = (w(k + 1) + w(k), w(k))
+        out[f"dec{k}b"] = (w(k), w(k))
+    return out
+
+
+def init_params(config: UNetConfig) -> dict[str, np.ndarray]:
+    """Seeded parameters with the reference's draw order (model.py:70-100):
+    Kaiming-uniform conv weights (bound sqrt(6/fan_in), HWIO), zero f biases,
+    +1 gate biases, identity descriptor head."""
+    rng = np.random.default_rng(config.init_seed)
+    params: dict[str, np.ndarray] = {}
+    c = config.input_channels
+    if config.use_descriptor_head:
+        params["head.w"] = np.eye(c, dtype=np.float32)
+        params["head.b"] = np.zeros(c, np.float32)
+    shapes = layer_shapes(config)
+    for name in layer_names(config):
+        ci, co = shapes[name]
+        bound = np.sqrt(6.0 / (9 * ci))
+        params[f"{name}.f_w"] = rng.uniform(-bound, bound, (3, 3, ci, co)).astype(np.float32)
+        params[f"{name}.f_b"] = np.zeros(co, np.float32)
+        params[f"{name}.g_w"] = rng.uniform(-bound, bound, (3, 3, ci, co)).astype(np.float32)
+        params[f"{name}.g_b"] = np.ones(co, np.float32)
+    w0 = config.width(0)
+    bound = np.sqrt(6.0 / w0)
+    params["out.w"] = rng.uniform(-bound, bound, (w0, config.output_channels)).astype(np.float32)
+    params["out.b"] = np.zeros(config.output_channels, np.float32)
+    return params
+
+
+def pad_to_multiple(img: np.ndarray, multiple: int = 16):
+    """Zero-pad (H, W, C) bottom/right to multiples (model.py:207-215);
+    returns (padded, (H, W))."""
+    h, w = img.shape[:2]
+    ph, pw = (-h) % multiple, (-w) % multiple
+    if ph or pw:
+        img = np.pad(img, ((0, ph), (0, pw)) + ((0, 0),) * (img.ndim - 2))
+    return img, (h, w)
+
+
+# ---------------------------------------------------------------------------
+# device network (libnar_b200.so nar_unet_*)
+# ---------------------------------------------------------------------------
+def _config_struct(cfg: UNetConfig) -> "_lib.UNetConfigC":
+    c = _lib.UNetConfigC()
+    c.input_channels, c.levels = cfg.input_channels, cfg.levels
+    c.base_channels, c.channel_multiplier = cfg.base_channels, cfg.channel_multiplier
+    c.max_channels, c.output_channels = cfg.max_channels, cfg.output_channels
+    c.use_descriptor_head = int(cfg.use_descriptor_head)
+    return c
+
+
+class UNet:
+    """Packed bf16 weights on the device plus a reusable workspace.
+
+    ``params`` is the reference parameter dict (HWIO f32 numpy arrays, names as
+    in model.py:70-100); they are validated and packed once at construction.
+    """
+
+    def __init__(self, config: UNetConfig, params: dict, device=None):
+        import torch
+
+        self.config = config
+        self.device = torch.device(device or "cuda")
+        lib = _lib.load()
+        h = C.c_void_p()
+        _lib.check(lib.nar_unet_create(C.byref(_config_struct(config)), C.byref(h)))
+        self._h = h
+        expected = set(["out.w", "out.b"])
+        if config.use_descriptor_head:
+            expected |= {"head.w", "head.b"}
+        for n in layer_names(config):
+            expected |= {f"{n}.f_w", f"{n}.f_b", f"{n}.g_w", f"{n}.g_b"}
+        missing = expected - set(params)
+        if missing:
+            raise ConfigurationError(f"missing parameters: {sorted(missing)[:4]}")
+        with torch.cuda.device(self.device):
+            for name in sorted(expected):
+                v = params[name]
+                if hasattr(v, "detach"):
+                    v = v.detach().cpu().numpy()
+                elif hasattr(v, "data") and not isinstance(v, np.ndarray):
+                    v = v.data  # reference autodiff Tensor
+                a = np.ascontiguousarray(v, dtype=np.float32)
+                _lib.check(lib.nar_unet_set_param(self._h, name.encode(), a.ctypes.data, a.size))
+        self._ws = {}
+
+    def launches_per_forward(self) -> int:
+        L = self.config.levels
+        return 1 + (L - 1) + 2 * L + 2 * (L - 1) + (L - 1) + 1
+
+    def _workspace(self, H: int, W: int):
+        import torch
+
+        key = (H, W)
+        if key not in self._ws:
+            n = C.c_size_t(0)
+            _lib.check(_lib.load().nar_unet_workspace_bytes(self._h, H, W, C.byref(n)))
+            self._ws[key] = torch.empty(int(n.value), dtype=torch.uint8, device=self.device)
+        return self._ws[key]
+
+    def forward_into(self, x, out, stream=None) -> None:
+        """x: device f32 (H, W, Cin) (or (1,H,W,Cin)); out: device f32 (H, W, out)."""
+        H, W = int(x.shape[-3]), int(x.shape[-2])
+        if int(x.shape[-1]) != self.config.input_channels:
+            raise ConfigurationError(
+                f"model expects {self.config.input_channels} channels, "
+                f"features have {int(x.shape[-1])}")
+        if not (x.is_contiguous() and out.is_contiguous()):
+            raise ValueError("forward_into needs contiguous tensors")
+        ws = self._workspace(H, W)
+        _lib.check(_lib.load().nar_unet_forward(self._h, x.data_ptr(), H, W, out.data_ptr(),
+                                                ws.data_ptr(), ws.numel(),
+                                                _lib.stream_handle(stream)))
+
+    def __call__(self, x):
+        import torch
+
+        x = x.to(self.device, torch.float32).contiguous()
+        squeeze = x.dim() == 3
+        if squeeze:
+            x = x[None]
+        outs = []
+        for img in x:
+            o = torch.empty(img.shape[:2] + (self.config.output_channels,), dtype=torch.float32,
+                            device=self.device)
+            self.forward_into(img, o)
+            outs.append(o)
+        y = torch.stack(outs)
+        return y[0] if squeeze else y
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None) and _lib._lib is not None:
+                _lib._lib.nar_unet_destroy(self._h)
+        except Exception:
+            pass
+
+
+_nets: dict = {}
+
+
+def forward(features, params: dict, config: UNetConfig):
+    """Full inference path (model.py:194-204): descriptor head, pyramid, U-Net.
+
+    ``features``: (N, H, W, C) f32 numpy array / reference Tensor (returns
+    numpy) or CUDA tensor (returns a CUDA tensor).  H and W must be multiples
+    of 2^(levels-1); use ``pad_to_multiple`` first, as the reference does.
+    """
+    import torch
+
+    data = getattr(features, "data", features) if not hasattr(features, "device") else features
+    shape = tuple(data.shape)
+    if shape[-1] != config.input_channels:
+        raise ConfigurationError(f"model expects {config.input_channels} channels, "
+                                 f"features have {shape[-1]}")
+    div = 2 ** (config.levels - 1)
+    if shape[-3] % div or shape[-2] % div:
+        raise ValueError(f"spatial dims {shape[-3]}x{shape[-2]} not divisible by {div}")
+    key = (id(params), config)
+    ent = _nets.get(key)
+    if ent is None or ent[0] is not params:
+        if len(_nets) > 4:
+            _nets.clear()
+        ent = _nets[key] = (params, UNet(config, params))
+    net = ent[1]
+    if isinstance(data, torch.Tensor):
+        return net(data)
+    x = torch.from_numpy(np.ascontiguousarray(data, dtype=np.float32))
+    y = net(x.to(net.device))
+    return y.cpu().numpy()

@@ -1,0 +1,112 @@
+"""CPU-side checks of the drop-in boundary: the C-ABI library loads, exports
+every symbol include/nar_b200.h declares, and the host-side API mirrors the
+reference's names, channel layout and error behaviour.  No kernel launches."""
+
+import ctypes as C
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_2407_19097_b200 import _kernels, _lib
+from paper_2407_19097_b200.errors import ConfigurationError
+from paper_2407_19097_b200.geometry import Intrinsics, PointCloud, Stream, look_at
+from paper_2407_19097_b200.msr import StreamSelection
+
+HEADER = Path(__file__).resolve().parents[1] / "include" / "nar_b200.h"
+
+
+def header_functions():
+    text = re.sub(r"/\*.*?\*/", "", HEADER.read_text(), flags=re.S)
+    return sorted(set(re.findall(r"\b(nar_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_builds_and_loads():
+    from paper_2407_19097_b200 import build
+
+    build.build()
+    lib = _lib.load()
+    assert b"sm_100a" in lib.nar_version()
+
+
+def test_every_declared_symbol_is_exported_and_bound():
+    lib = C.CDLL(str(_lib.LIB_PATH))
+    declared = header_functions()
+    assert len(declared) >= 15
+    for name in declared:
+        assert hasattr(lib, name), f"{name} declared but not exported"
+        assert name in _lib.SIGNATURES, f"{name} has no ctypes signature"
+    assert set(_lib.SIGNATURES) == set(declared)
+
+
+def test_header_structs_match_ctypes():
+    # sizes of the ABI structs as laid out by the C compiler
+    assert C.sizeof(_lib.Camera) == 8 * 17 + 8
+    assert C.sizeof(_lib.Segment) == 8 * (5 + _lib.MAX_SCALARS)
+    assert C.sizeof(_lib.ResolveOut) == 8 + 8 + 8 * 3 + 8
+
+
+def test_no_device_means_clean_status():
+    n = C.c_int32(-1)
+    rc = _lib.load().nar_device_count(C.byref(n))
+    assert rc == 0 and n.value >= 0
+
+
+def test_backend_names():
+    assert _kernels.BACKEND == "cuda"
+    with pytest.raises(ValueError):
+        _kernels._resolve("native")
+    with pytest.raises(ValueError):
+        _kernels._resolve("python")
+    assert _kernels.EMPTY_KEY == np.uint64(2 ** 64 - 1)
+
+
+def test_invalid_arguments_map_to_value_error():
+    kb = np.zeros(4, np.uint64)
+    with pytest.raises(ValueError):
+        _kernels.zbuffer_accumulate(kb, np.zeros((3, 3), np.float64), 0, np.eye(3), np.zeros(3),
+                                    1, 1, 1, 0.1, 10, 2, 2)
+    with pytest.raises(ValueError):  # C-ABI side validation, before any CUDA call
+        _lib.check(_lib.load().nar_zbuffer_accumulate(kb.ctypes.data, None, 0, 0, None, None, 1.0,
+                                                      1.0, 1.0, 0.1, 10.0, 2, 2))
+
+
+def test_channel_layout_is_reference_order():
+    rng = np.random.default_rng(0)
+    pc = PointCloud(rng.uniform(size=(5, 3)),
+                    [Stream("rgb", "u8", np.zeros((5, 3))), Stream("velocity", "f32", np.zeros((5, 3))),
+                     Stream("temp", "f32", np.zeros((5, 1))), Stream("mask", "u8", np.zeros((5, 2)))])
+    sel = StreamSelection(rgb=True, depth=True, vel2d=True, vel3d=True, scalars=("temp", "mask"),
+                          coverage_channel=True)
+    assert sel.channel_names(pc) == ("r", "g", "b", "d", "v2x", "v2y", "v2t", "v2m", "v3x", "v3y",
+                                     "v3z", "v3m", "temp", "mask0", "mask1", "coverage")
+    sel.validate(pc)
+    with pytest.raises(ConfigurationError):
+        StreamSelection(scalars=("nope",)).validate(pc)
+    with pytest.raises(ConfigurationError):
+        StreamSelection(rgb=True, rgb_stream="x").validate(pc)
+    big = StreamSelection(rgb=True, depth=True, vel2d=True, vel3d=True,
+                          scalars=("temp", "mask", "temp"), coverage_channel=True)
+    with pytest.raises(ConfigurationError):
+        big.validate(pc)
+
+
+def test_camera_contract():
+    cam = look_at((0, -2.2, 1.0), (0, 0, 0), Intrinsics(width=512, height=512))
+    R = cam.orientation
+    assert np.allclose(R @ R.T, np.eye(3))
+    kc = cam.kernel_camera()
+    assert kc.width == 512 and kc.cx == 256.0
+    assert kc.f == pytest.approx(256.0 / np.tan(np.radians(30.0)))
+    with pytest.raises(ValueError):
+        Intrinsics(near=0.0)
+
+
+def test_pointcloud_limits():
+    from paper_2407_19097_b200.errors import CapacityError
+
+    with pytest.raises(CapacityError):
+        PointCloud(np.zeros((1, 3)), [Stream(f"s{i}", "u8", np.zeros((1, 1))) for i in range(9)])
+    with pytest.raises(ValueError):
+        PointCloud(np.zeros((2, 3)), [Stream("rgb", "u8", np.zeros((3, 3)))])

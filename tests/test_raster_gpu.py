@@ -1,0 +1,228 @@
+"""Parity of the CUDA MSR path (render + resolve) against the reference.
+
+Golden fixtures come from the real reference (tests/golden/make_golden.py);
+larger randomized sweeps compare against the oracle restatement, which
+tests/test_oracle.py pins to those fixtures.  Bar: bit-exact keybufs, index /
+depth / coverage planes and rgb / d / scalar / coverage channels; vel2d /
+vel3d channels within 1 f32 ulp (BLAS / libm ordering).
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import random_case, ulp_diff_f32
+
+pytestmark = pytest.mark.gpu
+
+VEL = slice(4, 12)          # v2x..v3m in the full 16-channel selection
+EXACT = [0, 1, 2, 3, 12, 13, 14, 15]
+
+
+def check_feature_image(fi, ref_data, ref_index, ref_depth, ref_cov):
+    assert np.array_equal(fi.index_plane, ref_index)
+    assert np.array_equal(fi.depth, ref_depth)
+    assert np.array_equal(fi.coverage, ref_cov)
+    C = ref_data.shape[-1]
+    if C == 16:
+        assert np.array_equal(fi.data[..., EXACT], ref_data[..., EXACT])
+        assert ulp_diff_f32(fi.data[..., VEL], ref_data[..., VEL]).max() <= 1
+    else:
+        assert np.array_equal(fi.data, ref_data)
+
+
+def test_kat(cuda, golden):
+    from paper_2407_19097_b200.geometry import CameraPose, Intrinsics, PointCloud, Stream
+    from paper_2407_19097_b200.msr import StreamSelection, rasterize
+
+    g = golden("raster_kat")
+    cam = CameraPose(g["camera/pos"], g["camera/R"], Intrinsics(width=16, height=16))
+    for name in ("empty", "depth", "tie"):
+        pc = PointCloud(g[f"{name}/positions"], [Stream("rgb", "u8", g[f"{name}/rgb"])])
+        fi = rasterize(pc, cam, StreamSelection(rgb=True, depth=True))
+        check_feature_image(fi, g[f"{name}/data"], g[f"{name}/index_plane"], g[f"{name}/depth"],
+                            g[f"{name}/coverage"])
+
+
+@pytest.mark.parametrize("ci", range(6))
+def test_golden_random(cuda, golden, ci):
+    from paper_2407_19097_b200 import _kernels
+    from paper_2407_19097_b200.msr import rasterize
+
+    pc, cam, sel, g, p = random_case(golden, ci)
+    i = cam.intrinsics
+    kb = _kernels.zbuffer_render(pc.positions, cam.orientation, cam.position, i.focal_px, i.cx,
+                                 i.cy, i.near, i.far, i.width, i.height)
+    assert np.array_equal(kb, g[p + "keybuf"])
+    fi = rasterize(pc, cam, sel)
+    check_feature_image(fi, g[p + "data"], g[p + "index_plane"], g[p + "depth"], g[p + "coverage"])
+
+
+def test_nonfinite(cuda, golden):
+    from paper_2407_19097_b200 import _kernels
+    from paper_2407_19097_b200.geometry import Intrinsics
+
+    g = golden("raster_nonfinite")
+    i = Intrinsics(width=64, height=64)
+    kb = _kernels.zbuffer_render(g["positions"], g["R"], g["campos"], i.focal_px, i.cx, i.cy,
+                                 i.near, i.far, 64, 64)
+    assert np.array_equal(kb, g["keybuf"])
+
+
+def test_c1_checksum(cuda, golden):
+    """Config C1 (1M uniform, 512^2): sha256 of the reference keybuf."""
+    import hashlib
+
+    from paper_2407_19097_b200 import _kernels
+    from paper_2407_19097_b200.geometry import Intrinsics, look_at
+
+    g = golden("raster_c1_hash")
+    pos = np.random.default_rng(0).uniform(-1, 1, (1_000_000, 3)).astype(np.float32)
+    cam = look_at((0.0, -2.2, 1.0), (0, 0, 0), Intrinsics(width=512, height=512))
+    i = cam.intrinsics
+    kb = _kernels.zbuffer_render(pos, cam.orientation, cam.position, i.focal_px, i.cx, i.cy,
+                                 i.near, i.far, 512, 512)
+    assert hashlib.sha256(kb.tobytes()).digest() == g["keybuf_sha256"].tobytes()
+
+
+def _random_scene(seed, n, W, H):
+    from paper_2407_19097_b200.geometry import Intrinsics, PointCloud, Stream, look_at
+
+    rng = np.random.default_rng(seed)
+    scale = 10.0 ** rng.uniform(-2, 3)
+    pos = (rng.uniform(-1, 1, (n, 3)) * scale).astype(np.float32)
+    k = n // 20
+    pos[rng.integers(0, n, k)] = pos[rng.integers(0, n, k)]
+    eye = rng.normal(size=3)
+    eye = eye / np.linalg.norm(eye) * scale * rng.uniform(0.5, 4.0)
+    cam = look_at(eye, rng.uniform(-0.2, 0.2, 3) * scale,
+                  Intrinsics(fov_y_deg=rng.uniform(20, 120), width=W, height=H,
+                             near=float(scale * rng.uniform(1e-4, 0.5))))
+    pc = PointCloud(pos, [Stream("rgb", "u8", rng.integers(0, 256, (n, 3), dtype=np.uint8)),
+                          Stream("velocity", "f32", rng.normal(size=(n, 3)) * scale)])
+    return pc, cam
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_sweep_vs_oracle(cuda, seed):
+    """SPEC acceptance #1 style sweep: 10^3..10^5 points, random cameras and
+    scales (incl. cameras inside the cloud), bit-identical keybufs."""
+    from paper_2407_19097_b200.msr import StreamSelection, rasterize
+
+    rng = np.random.default_rng(1000 + seed)
+    n = int(10 ** rng.uniform(3, 5))
+    W, H = int(rng.integers(1, 200)), int(rng.integers(1, 200))
+    pc, cam = _random_scene(seed, n, W, H)
+    sel = StreamSelection(rgb=True, depth=True, vel2d=True, vel3d=True, velocity_scale=2.5)
+    ref = oracle.rasterize(pc, cam, sel)
+    fi = rasterize(pc, cam, sel)
+    assert np.array_equal(fi.index_plane, ref["index_plane"])
+    assert np.array_equal(fi.depth, ref["depth"])
+    assert np.array_equal(fi.data[..., :4], ref["data"][..., :4])
+    assert ulp_diff_f32(fi.data[..., 4:], ref["data"][..., 4:]).max() <= 1
+
+
+def test_unaligned_and_tail(cuda):
+    """Views at odd offsets (no 16-byte alignment) take the non-TMA kernel;
+    counts not a multiple of the tile take the tail kernel."""
+    from paper_2407_19097_b200 import _kernels
+
+    pc, cam = _random_scene(7, 50_001, 97, 61)
+    i = cam.intrinsics
+    buf = np.empty((pc.count + 1) * 3 + 1, np.float32)
+    view = buf[1:1 + pc.count * 3].reshape(-1, 3)
+    view[...] = pc.positions
+    assert view.ctypes.data % 16 != 0
+    args = (cam.orientation, cam.position, i.focal_px, i.cx, i.cy, i.near, i.far, 97, 61)
+    ref = oracle.zbuffer_render(pc.positions, *args)
+    kb = np.full(97 * 61, _kernels.EMPTY_KEY, np.uint64)
+    _kernels.zbuffer_accumulate(kb, view, 0, *args)
+    assert np.array_equal(kb, ref)
+    assert np.array_equal(_kernels.zbuffer_render(pc.positions, *args), ref)
+
+
+def test_base_index_and_accumulate_in_place(cuda):
+    """zbuffer_accumulate folds into an existing buffer with a base index, like
+    the reference's per-chunk calls (_kernels/__init__.py:84-87)."""
+    from paper_2407_19097_b200 import _kernels
+
+    pc, cam = _random_scene(3, 30_000, 64, 64)
+    i = cam.intrinsics
+    args = (cam.orientation, cam.position, i.focal_px, i.cx, i.cy, i.near, i.far, 64, 64)
+    kb = np.full(64 * 64, _kernels.EMPTY_KEY, np.uint64)
+    for lo, hi in [(0, 10_000), (10_000, 25_000), (25_000, 30_000)]:
+        _kernels.zbuffer_accumulate(kb, np.ascontiguousarray(pc.positions[lo:hi]), lo, *args)
+    assert np.array_equal(kb, oracle.zbuffer_render(pc.positions, *args))
+    # index wrap: base_index above 2^32 keeps the low 32 bits
+    kb2 = np.full(64 * 64, _kernels.EMPTY_KEY, np.uint64)
+    _kernels.zbuffer_accumulate(kb2, pc.positions, (1 << 32) + 5, *args)
+    ref2 = np.full(64 * 64, _kernels.EMPTY_KEY, np.uint64)
+    oracle.zbuffer_accumulate(ref2, pc.positions, (1 << 32) + 5, *args)
+    assert np.array_equal(kb2, ref2)
+
+
+def test_device_multistream_equals_concatenated(cuda):
+    """C3 semantics: 4 point buffers on 4 CUDA streams == rasterize of the
+    concatenation with base indices 0, n0, n0+n1, ..."""
+    import torch
+
+    from paper_2407_19097_b200.geometry import PointCloud, Stream
+    from paper_2407_19097_b200.msr import DeviceCloud, Renderer, StreamSelection
+
+    parts = []
+    for s in range(4):
+        pc, cam = _random_scene(50, 20_000 + 1000 * s, 120, 90)
+        parts.append(pc)
+    allpos = np.concatenate([p.positions for p in parts])
+    whole = PointCloud(allpos, [Stream("rgb", "u8", np.concatenate([p.stream("rgb").data for p in parts])),
+                                Stream("velocity", "f32", np.concatenate([p.stream("velocity").data for p in parts]))])
+    sel = StreamSelection(rgb=True, depth=True, vel2d=True)
+    ref = oracle.rasterize(whole, cam, sel)
+    dc = DeviceCloud.from_clouds(parts, device=cuda)
+    r = Renderer(120, 90, device=cuda)
+    for signed in (False, True):
+        r = Renderer(120, 90, device=cuda, signed_keys=signed)
+        for _ in range(2):  # second frame checks the fused keybuf re-clear
+            img = r.rasterize(dc, cam, sel).to_host()
+            torch.cuda.synchronize()
+            assert np.array_equal(img.index_plane, ref["index_plane"])
+            assert np.array_equal(img.data[..., :4], ref["data"][..., :4])
+            assert ulp_diff_f32(img.data[..., 4:], ref["data"][..., 4:]).max() <= 1
+        r.render(dc, cam)
+        assert np.array_equal(r.keys(), ref["keybuf"])
+        r.clear()
+
+
+def test_large_scale_properties(cuda):
+    """Full-size property check (50M points at 1080p): shard composite equals
+    the whole render, and every covered pixel's winner is the min key of the
+    points that project there (sampled exhaustively via the oracle on a subset)."""
+    import torch
+
+    from paper_2407_19097_b200.geometry import Intrinsics, look_at
+    from paper_2407_19097_b200.msr import DeviceCloud, Renderer
+
+    n = 50_000_000
+    g = torch.Generator(device=cuda).manual_seed(5)
+    pos = torch.rand((n, 3), device=cuda, generator=g) * 2 - 1
+    cam = look_at((0.0, -2.2, 1.0), (0, 0, 0), Intrinsics(width=1920, height=1080))
+    whole = Renderer(1920, 1080, device=cuda)
+    whole.render(DeviceCloud.from_tensors(pos), cam)
+    kw = whole.keys()
+    parts = Renderer(1920, 1080, device=cuda)
+    bounds = [0, 12_345_678, 30_000_000, n]
+    for lo, hi in zip(bounds[:-1], bounds[1:]):
+        parts.render(DeviceCloud.from_tensors(pos[lo:hi], begin=lo), cam)
+    assert np.array_equal(parts.keys(), kw)
+    # exact check on a random contiguous window of 2M points against the oracle
+    lo = 17_000_000
+    sub = pos[lo:lo + 2_000_000].cpu().numpy()
+    i = cam.intrinsics
+    ref = np.full(1920 * 1080, oracle.EMPTY_KEY, np.uint64)
+    oracle.zbuffer_accumulate(ref, sub, lo, cam.orientation, cam.position, i.focal_px, i.cx,
+                              i.cy, i.near, i.far, 1920, 1080)
+    sub_r = Renderer(1920, 1080, device=cuda)
+    sub_r.render(DeviceCloud.from_tensors(pos[lo:lo + 2_000_000], begin=lo), cam)
+    assert np.array_equal(sub_r.keys(), ref)
+    # min-composite property: whole <= every sub-render
+    assert np.all(kw <= sub_r.keys())
