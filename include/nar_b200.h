@@ -91,6 +91,17 @@ int nar_keybuf_fill(uint64_t* keybuf_dev, int64_t npix, uint64_t value, void* st
 int nar_render(uint64_t* keybuf_dev, const float* positions_dev, int64_t n,
                uint64_t base_index, const nar_camera* cam, int32_t key_domain,
                void* stream);
+/* Hierarchical-Z render: as nar_render, but the points are split into passes
+ * and every pass after the first rejects points behind the coarse max depth
+ * (2^k x 2^k pixel blocks) rebuilt from the keybuf into hiz_scratch_dev
+ * (nar_hiz_scratch_bytes).  keybuf_has_frame != 0 means the keybuf already
+ * holds keys of this frame (e.g. other point buffers rendered before), so
+ * the first pass may use the coarse test too.  Results are identical to
+ * nar_render: the test only skips points that cannot win. */
+int nar_hiz_scratch_bytes(int32_t width, int32_t height, size_t* bytes);
+int nar_render_hiz(uint64_t* keybuf_dev, uint16_t* hiz_scratch_dev, const float* positions_dev,
+                   int64_t n, uint64_t base_index, const nar_camera* cam, int32_t key_domain,
+                   int32_t keybuf_has_frame, void* stream);
 /* Same as nar_render for host-resident points: streams them through device
  * chunk buffers, overlapping the H2D copy of chunk k+1 with the render of k. */
 int nar_render_host(uint64_t* keybuf_dev, const float* positions_host, int64_t n,

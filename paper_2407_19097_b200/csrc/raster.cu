@@ -14,7 +14,9 @@
 //               key = f32bits(depth) << 32 | (index & 0xFFFFFFFF).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <mutex>
@@ -34,6 +36,10 @@ struct DevCam {
   double f, cx, cy, nr, fr;
   double wd, hd;
   int32_t w, h;
+  // certified fast pixel path (see project_fast)
+  double cxh, cyh;       // cx + 0.5, cy + 0.5
+  double fr_[6];         // f * R rows 0, 1
+  int32_t fast;          // camera within the bound's domain
 };
 
 static DevCam make_devcam(const nar_camera& cam) {
@@ -49,6 +55,13 @@ static DevCam make_devcam(const nar_camera& cam) {
   k.hd = (double)cam.height;
   k.w = cam.width;
   k.h = cam.height;
+  for (int i = 0; i < 6; ++i) k.fr_[i] = cam.f * cam.R[i];
+  k.cxh = cam.cx + 0.5;
+  k.cyh = cam.cy + 0.5;
+  k.fast = (fabs(cam.f) <= 1048576.0 && fabs(cam.cx) < 32768.0 && fabs(cam.cy) < 32768.0 &&
+            cam.width <= 65536 && cam.height <= 65536)
+               ? 1
+               : 0;
   return k;
 }
 
@@ -77,6 +90,65 @@ __device__ __forceinline__ bool project_point(float x, float y, float z, const D
   return true;
 }
 
+// Certified fast projection.  The depth uz (cull test and key) is computed
+// exactly as the reference does.  The pixel snap T = fl(fl(cx + fl(f * fl(ux
+// / uz))) + 0.5) is replaced by T' = fma(fux', r, cx + 0.5) with fux' a DFMA
+// chain over the host-rounded rows f*R and r = 1/uz from rcp.approx + two
+// Newton steps.  For |T'| < 2^16, |cx|, |cy| < 2^15 and f <= 2^20 (checked on
+// the host: DevCam::fast) the distance |T' - T| is below 2^-28 (DESIGN.md,
+// "certified pixel snap"), so floor(T') == floor(T) whenever T' is at least
+// 1.5 * 2^-24 from an integer.  The rare "uncertain" points are re-projected
+// exactly.
+// Returns 0 = culled, 1 = certain (ix, iy, dbits valid), 2 = uncertain.
+__device__ __forceinline__ double rcp_approx_f64(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
+
+__device__ __forceinline__ bool snap_certain(double t, int& i) {
+  // q = round(t * 2^24) from the low bits of t + 1.5*2^28 (exact for |t| < 2^27);
+  // floor(t) = q >> 24 unless t is within ~2^-23 of an integer, which the
+  // caller treats as uncertain.
+  const double s = __dadd_rn(t, 402653184.0);
+  const long long q = __double_as_longlong(s) - 0x41B8000000000000LL;
+  i = (int)(q >> 24);
+  return ((uint32_t)q & 0xFFFFFFu) - 2u < 0xFFFFFDu;  // fraction in [2, 2^24 - 2] * 2^-24
+}
+
+__device__ __forceinline__ int project_fast(float x, float y, float z, const DevCam& k,
+                                            uint32_t& ix_out, uint32_t& iy_out, uint32_t& dbits) {
+  const double w0 = __dsub_rn((double)x, k.c[0]);
+  const double w1 = __dsub_rn((double)y, k.c[1]);
+  const double w2 = __dsub_rn((double)z, k.c[2]);
+  const double uz =
+      __dadd_rn(__dadd_rn(__dmul_rn(w0, k.r[6]), __dmul_rn(w1, k.r[7])), __dmul_rn(w2, k.r[8]));
+  const bool in_depth = uz > k.nr && uz < k.fr;  // python_impl.py:43 (NaN culled)
+  dbits = __float_as_uint(__double2float_rn(uz));
+  double r = rcp_approx_f64(uz);
+  double e = __fma_rn(-uz, r, 1.0);
+  r = __fma_rn(r, e, r);
+  e = __fma_rn(-uz, r, 1.0);
+  r = __fma_rn(r, e, r);
+  // f * ux and f * uy with f folded into the rotation rows (host-rounded)
+  const double fx = __fma_rn(w2, k.fr_[2], __fma_rn(w1, k.fr_[1], __dmul_rn(w0, k.fr_[0])));
+  const double fy = __fma_rn(w2, k.fr_[5], __fma_rn(w1, k.fr_[4], __dmul_rn(w0, k.fr_[3])));
+  const double tx = __fma_rn(fx, r, k.cxh);
+  const double ty = __fma_rn(fy, r, k.cyh);
+  // |t| < 2^16 on the high word (integer pipe; NaN fails)
+  const bool sane = (((uint32_t)__double2hiint(tx) & 0x7FFFFFFFu) < 0x40F00000u) &&
+                    (((uint32_t)__double2hiint(ty) & 0x7FFFFFFFu) < 0x40F00000u);
+  int ix, iy;
+  const bool cx_ok = snap_certain(tx, ix);
+  const bool cy_ok = snap_certain(ty, iy);
+  const bool certain = k.fast && sane && cx_ok && cy_ok;
+  const bool inside = (uint32_t)ix < (uint32_t)k.w && (uint32_t)iy < (uint32_t)k.h;
+  ix_out = (uint32_t)ix;
+  iy_out = (uint32_t)iy;
+  // 0 = culled, 1 = certain hit, 2 = uncertain (in depth range, snap not certified)
+  return (int)in_depth * (certain ? (int)inside : 2);
+}
+
 template <bool kSigned>
 __device__ __forceinline__ void fold_key(uint64_t* keybuf, uint32_t pix, uint64_t key) {
   if (kSigned) {
@@ -89,75 +161,280 @@ __device__ __forceinline__ void fold_key(uint64_t* keybuf, uint32_t pix, uint64_
   }
 }
 
-// ----------------------------------------------------------------------------
-// render: persistent CTAs, TMA bulk-copy ring of point tiles in smem
-// ----------------------------------------------------------------------------
-constexpr int kRenderThreads = 256;
-constexpr int kPtsPerThread = 4;
-constexpr int kTilePts = kRenderThreads * kPtsPerThread;  // 1024 points
-constexpr int kTileBytes = kTilePts * 12;                 // 12 KB
-constexpr int kStages = 4;
-constexpr int kRenderSmem = kStages * kTileBytes + 64;
-
+// Atomic half of fold_key, given a previously loaded current value.
 template <bool kSigned>
-__global__ void __launch_bounds__(kRenderThreads, 4)
-    render_tma_kernel(uint64_t* __restrict__ keybuf, const float* __restrict__ pos,
-                      int64_t n_tiles, uint64_t base_index, const DevCam cam) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  float* ring = reinterpret_cast<float*>(smem);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kTileBytes);
-  const int tid = threadIdx.x;
-
-  if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
-    fence_mbar_init();
+__device__ __forceinline__ void fold_loaded(uint64_t* keybuf, uint32_t pix, uint64_t key,
+                                            uint64_t cur) {
+  if (kSigned) {
+    const long long k = (long long)(key ^ NAR_SIGN_FLIP);
+    if (k < (long long)cur) atomicMin(reinterpret_cast<long long*>(keybuf) + pix, k);
+  } else {
+    if (key < cur) atomicMin(reinterpret_cast<unsigned long long*>(keybuf) + pix,
+                             (unsigned long long)key);
   }
-  __syncthreads();
+}
 
-  const int64_t first = blockIdx.x;
-  const int64_t stride = gridDim.x;
-  // prologue: fill the ring
-  if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      const int64_t t = first + (int64_t)s * stride;
-      if (t < n_tiles) {
-        mbar_expect_tx(&full[s], kTileBytes);
-        bulk_g2s(ring + s * (kTilePts * 3), pos + t * (int64_t)(kTilePts * 3), kTileBytes,
+// ----------------------------------------------------------------------------
+// render: persistent CTAs, every warp streams its own 128-point chunks through
+// a private ring of TMA bulk copies (no cross-warp coupling on the data path)
+// ----------------------------------------------------------------------------
+#ifndef NAR_RENDER_WARPS
+#define NAR_RENDER_WARPS 24
+#endif
+#ifndef NAR_RENDER_PPT
+#define NAR_RENDER_PPT 2
+#endif
+constexpr int kRenderWarps = NAR_RENDER_WARPS;
+constexpr int kRenderThreads = kRenderWarps * 32;
+constexpr int kPtsPerThread = NAR_RENDER_PPT;
+constexpr int kChunkPts = 32 * kPtsPerThread;                // points per warp step
+constexpr int kChunkBytes = kChunkPts * 12;
+constexpr int kWarpStages = 6;
+constexpr int kRingBytes = kRenderWarps * kWarpStages * kChunkBytes;
+constexpr int kQueueBytes = kRenderWarps * 32 * 16;
+constexpr int kHizMaxEntries = 32768;                        // 64 KB coarse depth (u16)
+constexpr int kRenderSmem =
+    kRingBytes + kQueueBytes + kHizMaxEntries * 2 + kRenderWarps * kWarpStages * 8 + 128;
+constexpr int kTilePts = kChunkPts;  // granularity of the TMA path (tail -> simple kernel)
+
+// Chunk schedule of one launch: linear chunk slots j in [j0, j1) map to
+// chunks of the cloud by mode 0: j; 1 (Hi-Z seed pass): j*S; 2 (the rest):
+// j + j/(S-1) + 1, i.e. every chunk that is not a multiple of S.
+constexpr int kHizSeedStride = 16;  // S
+struct ChunkMap {
+  int64_t j0, j1;  // chunk slots (< 2^32: point indices are 32-bit)
+  int32_t mode;
+  __device__ __forceinline__ int64_t chunk(int64_t j) const {
+    const uint32_t u = (uint32_t)j;
+    return mode == 0 ? j
+                     : (mode == 1 ? (int64_t)u * kHizSeedStride
+                                  : (int64_t)u + u / (kHizSeedStride - 1) + 1);
+  }
+};
+
+// Hierarchical-Z: zq[b] = ceil(max f32 depth bits in coarse block b / 2^16)
+// over 2^shift x 2^shift pixels; a point with (depth bits >> 16) > zq[b] is
+// behind every pixel of the block (strictly deeper), so it cannot win.
+struct HizArgs {
+  const uint16_t* zmax;  // NULL: no coarse test in this pass
+  int32_t shift, zw, entries;
+};
+
+struct QEntry {
+  float x, y, z;
+  uint32_t idx;
+};
+
+// Exact re-projection of up to 32 queued uncertain points, one per lane.
+template <bool kSigned>
+__device__ __forceinline__ void flush_queue(const QEntry* q, int n, int lane, uint64_t* keybuf,
+                                            const DevCam& cam) {
+  __syncwarp();
+  if (lane < n) {
+    const QEntry e = q[lane];
+    uint32_t pix, db;
+    if (project_point(e.x, e.y, e.z, cam, pix, db))
+      fold_key<kSigned>(keybuf, pix, ((uint64_t)db << 32) | e.idx);
+  }
+  __syncwarp();
+}
+
+// Per warp step (one 128-point chunk, 4 points per lane):
+// (1) certified fast projection; uncertain points go to the warp's queue and
+//     are re-projected exactly once 32 have gathered;
+// (2) Hi-Z test against the smem coarse depth -- occluded points stop here;
+// (3) hand the ring slot back to TMA (chunk k + kWarpStages);
+// (4) fold the PREVIOUS chunk's survivors, whose keybuf reads were issued one
+//     step ago, so the random-L2 read latency overlaps a chunk of math;
+// (5) issue this chunk's keybuf reads.
+template <bool kSigned, bool kDedup>
+__global__ void __launch_bounds__(kRenderThreads, 1)
+    render_tma_kernel(uint64_t* __restrict__ keybuf, const float* __restrict__ pos,
+                      const ChunkMap cm, uint64_t base_index, const DevCam cam, const HizArgs hz) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float* ring = reinterpret_cast<float*>(smem) + warp * (kWarpStages * kChunkPts * 3);
+  QEntry* wq = reinterpret_cast<QEntry*>(smem + kRingBytes) + warp * 32;
+  uint16_t* zs = reinterpret_cast<uint16_t*>(smem + kRingBytes + kQueueBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytes + kQueueBytes +
+                                               kHizMaxEntries * 2) + warp * kWarpStages;
+
+  const int64_t c_first = cm.j0 + (int64_t)blockIdx.x * kRenderWarps + warp;
+  const int64_t c_stride = (int64_t)gridDim.x * kRenderWarps;
+  const int64_t n_chunks = cm.j1;
+  if (lane == 0) {
+    for (int s = 0; s < kWarpStages; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+    for (int s = 0; s < kWarpStages; ++s) {
+      const int64_t c = c_first + (int64_t)s * c_stride;
+      if (c < n_chunks) {
+        mbar_expect_tx(&full[s], kChunkBytes);
+        bulk_g2s(ring + s * (kChunkPts * 3), pos + cm.chunk(c) * (kChunkPts * 3), kChunkBytes,
                  &full[s]);
       }
     }
   }
+  const bool use_hiz = hz.zmax != nullptr;
+  if (use_hiz) {
+    const uint4* src = reinterpret_cast<const uint4*>(hz.zmax);
+    uint4* dst = reinterpret_cast<uint4*>(zs);
+    for (int i = tid; i < (hz.entries + 7) / 8; i += kRenderThreads) dst[i] = __ldcg(src + i);
+    __syncthreads();
+  }
+  __syncwarp();
 
-  int it = 0;
-  for (int64_t t = first; t < n_tiles; t += stride, ++it) {
-    const int s = it % kStages;
-    const uint32_t phase = (uint32_t)(it / kStages) & 1u;
-    mbar_wait(&full[s], phase);
-    const float* tile = ring + s * (kTilePts * 3);
-    const uint64_t tile_base = base_index + (uint64_t)t * kTilePts;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  int qn = 0;  // warp-uniform queue fill
+  uint32_t ppix[kPtsPerThread];
+  uint64_t pkey[kPtsPerThread], pcur[kPtsPerThread];
+  uint32_t pmask = 0;
+#pragma unroll
+  for (int j = 0; j < kPtsPerThread; ++j) {
+    ppix[j] = 0;
+    pkey[j] = 0;
+    pcur[j] = 0;
+  }
 
-    uint32_t pix[kPtsPerThread];
-    uint64_t key[kPtsPerThread];
-    bool ok[kPtsPerThread];
+  int k = 0;
+#pragma unroll 2
+  for (int64_t c = c_first; c < n_chunks; c += c_stride, ++k) {
+    const int s = k % kWarpStages;
+    mbar_wait(&full[s], (uint32_t)(k / kWarpStages) & 1u);
+    const float* chunk = ring + s * (kChunkPts * 3);
+    const uint64_t cbase = base_index + (uint64_t)cm.chunk(c) * kChunkPts;
+
+    // (1) projections: straight-line, interleavable across the 4 points
+    float px[kPtsPerThread], py[kPtsPerThread], pz[kPtsPerThread];
+    uint32_t ixs[kPtsPerThread], iys[kPtsPerThread], dbs[kPtsPerThread];
+    int sts[kPtsPerThread];
 #pragma unroll
     for (int j = 0; j < kPtsPerThread; ++j) {
-      const int p = j * kRenderThreads + tid;
-      uint32_t db = 0;
-      ok[j] = project_point(tile[3 * p], tile[3 * p + 1], tile[3 * p + 2], cam, pix[j], db);
-      key[j] = ((uint64_t)db << 32) | ((tile_base + (uint64_t)p) & 0xFFFFFFFFull);
+      const int p = j * 32 + lane;
+      px[j] = chunk[3 * p];
+      py[j] = chunk[3 * p + 1];
+      pz[j] = chunk[3 * p + 2];
     }
-    __syncthreads();  // everyone is done reading stage s
-    if (tid == 0) {
-      const int64_t nt = t + (int64_t)kStages * stride;
-      if (nt < n_tiles) {
-        mbar_expect_tx(&full[s], kTileBytes);
-        bulk_g2s(ring + s * (kTilePts * 3), pos + nt * (int64_t)(kTilePts * 3), kTileBytes,
+    __syncwarp();
+    if (lane == 0) {  // (3) slot s is consumed: refill it with chunk k + kWarpStages
+      const int64_t cn = c + (int64_t)kWarpStages * c_stride;
+      if (cn < n_chunks) {
+        fence_proxy_async_smem();
+        mbar_expect_tx(&full[s], kChunkBytes);
+        bulk_g2s(ring + s * (kChunkPts * 3), pos + cm.chunk(cn) * (kChunkPts * 3), kChunkBytes,
                  &full[s]);
       }
     }
 #pragma unroll
     for (int j = 0; j < kPtsPerThread; ++j)
-      if (ok[j]) fold_key<kSigned>(keybuf, pix[j], key[j]);
+      sts[j] = project_fast(px[j], py[j], pz[j], cam, ixs[j], iys[j], dbs[j]);
+
+    // (2) Hi-Z, optional warp pre-dedup of same-pixel hits, uncertain queue
+    uint32_t pix[kPtsPerThread], idxs[kPtsPerThread];
+    uint64_t key[kPtsPerThread];
+    uint32_t okmask = 0, umask = 0;
+#pragma unroll
+    for (int j = 0; j < kPtsPerThread; ++j) {
+      const int p = j * 32 + lane;
+      int st = sts[j];
+      const uint32_t db = dbs[j];
+      if (use_hiz && st == 1) {
+        const uint32_t zb = (iys[j] >> hz.shift) * (uint32_t)hz.zw + (ixs[j] >> hz.shift);
+        st = (db >> 16) > zs[zb] ? 0 : 1;  // behind every pixel of its coarse block
+      }
+      pix[j] = iys[j] * (uint32_t)cam.w + ixs[j];
+      const uint32_t idx = (uint32_t)((cbase + (uint64_t)p) & 0xFFFFFFFFull);
+      key[j] = ((uint64_t)db << 32) | idx;
+      if (kDedup) {
+        // lanes hitting the same pixel: only the (depth, index)-minimum survives
+        const uint32_t active = __ballot_sync(0xffffffffu, st == 1);
+        if (st == 1) {
+          const uint32_t grp = __match_any_sync(active, pix[j]);
+          if (grp != (1u << lane)) {
+            const uint32_t dmin = __reduce_min_sync(grp, db);
+            const uint32_t imin = __reduce_min_sync(grp, db == dmin ? idx : 0xFFFFFFFFu);
+            if (db != dmin || idx != imin) st = 0;
+          }
+        }
+      }
+      if (st == 1) okmask |= 1u << j;
+      if (st == 2) umask |= 1u << j;
+      idxs[j] = idx;
+    }
+    if (__any_sync(0xffffffffu, umask != 0u)) {
+#pragma unroll
+      for (int j = 0; j < kPtsPerThread; ++j) {
+        const uint32_t b = __ballot_sync(0xffffffffu, (umask >> j) & 1u);
+        if (b) {
+          const int nb = __popc(b);
+          if (qn + nb > 32) {
+            flush_queue<kSigned>(wq, qn, lane, keybuf, cam);
+            qn = 0;
+          }
+          if ((umask >> j) & 1u)
+            wq[qn + __popc(b & lt_mask)] = QEntry{px[j], py[j], pz[j], idxs[j]};
+          qn += nb;
+        }
+      }
+    }
+    // (4) + (5)
+#pragma unroll
+    for (int j = 0; j < kPtsPerThread; ++j)
+      if ((pmask >> j) & 1u) fold_loaded<kSigned>(keybuf, ppix[j], pkey[j], pcur[j]);
+#pragma unroll
+    for (int j = 0; j < kPtsPerThread; ++j) {
+      if ((okmask >> j) & 1u)
+        pcur[j] = __ldcg(reinterpret_cast<const unsigned long long*>(keybuf) + pix[j]);
+      ppix[j] = pix[j];
+      pkey[j] = key[j];
+    }
+    pmask = okmask;
+  }
+#pragma unroll
+  for (int j = 0; j < kPtsPerThread; ++j)
+    if ((pmask >> j) & 1u) fold_loaded<kSigned>(keybuf, ppix[j], pkey[j], pcur[j]);
+  flush_queue<kSigned>(wq, qn, lane, keybuf, cam);
+}
+
+// Coarse max depth of the current keybuf: 2^shift threads per coarse block,
+// one pixel row each (independent loads), max-reduced with warp shuffles.
+template <bool kSigned>
+__global__ void __launch_bounds__(256)
+    hiz_kernel(const uint64_t* __restrict__ keybuf, int W, int H, int shift, int zw, int zh,
+               uint16_t* __restrict__ zmax) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int side = 1 << shift;
+  const int b = (int)(t >> shift), row = (int)(t & (side - 1));
+  const bool valid = b < zw * zh;
+  uint32_t m = 0;
+  if (valid) {
+    const int bx = b % zw, by = b / zw;
+    const int y = (by << shift) + row, x0 = bx << shift;
+    if (y < H) {
+      const unsigned long long* p = reinterpret_cast<const unsigned long long*>(keybuf) +
+                                    (size_t)y * W + x0;
+      const int n = min(side, W - x0);
+#pragma unroll 8
+      for (int i = 0; i < n; ++i) {
+        uint64_t k = __ldcg(p + i);
+        if (kSigned) k ^= NAR_SIGN_FLIP;
+        m = max(m, (uint32_t)(k >> 32));
+      }
+    }
+  }
+  for (int o = 1; o < side; o <<= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (valid && row == 0) {
+    const uint32_t q = (m >> 16) + ((m & 0xFFFFu) != 0u);  // round up: conservative
+    zmax[b] = (uint16_t)(q > 0xFFFFu ? 0xFFFFu : q);
+  }
+}
+
+static void hiz_geometry(int W, int H, int& shift, int& zw, int& zh) {
+  shift = 3;  // <= 5 (one warp per coarse block row set) for any image < 2^32 pixels
+  for (;;) {
+    zw = (W + (1 << shift) - 1) >> shift;
+    zh = (H + (1 << shift) - 1) >> shift;
+    if ((int64_t)zw * zh <= kHizMaxEntries) return;
+    ++shift;
   }
 }
 
@@ -336,6 +613,7 @@ __global__ void __launch_bounds__(256)
 static int g_num_sms = 0;
 static int g_render_blocks_per_sm = 0;
 static std::once_flag g_init_once;
+static bool g_dedup = false;  // warp pre-dedup of same-pixel hits (NAR_RENDER_DEDUP=1 enables)
 
 static int device_init() {
   int err = 0;
@@ -343,36 +621,76 @@ static int device_init() {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) { err = 1; return; }
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(render_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kRenderSmem);
-    cudaFuncSetAttribute(render_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kRenderSmem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_render_blocks_per_sm,
-                                                  render_tma_kernel<false>, kRenderThreads,
-                                                  kRenderSmem);
-    if (g_render_blocks_per_sm < 1) g_render_blocks_per_sm = 1;
+    cudaFuncSetAttribute(render_tma_kernel<false, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, kRenderSmem);
+    cudaFuncSetAttribute(render_tma_kernel<true, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, kRenderSmem);
+    cudaFuncSetAttribute(render_tma_kernel<false, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, kRenderSmem);
+    cudaFuncSetAttribute(render_tma_kernel<true, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, kRenderSmem);
+    const char* dd = getenv("NAR_RENDER_DEDUP");
+    g_dedup = dd && dd[0] == '1';
+    g_render_blocks_per_sm = 1;
   });
   if (err || g_num_sms == 0) return set_error(NAR_ERR_CUDA, "no CUDA device");
   return NAR_OK;
 }
 
+// Renders n points.  With a Hi-Z scratch (zmax), the aligned part is split
+// into passes; before every pass but the first (and before the first too when
+// `refresh_first`, i.e. the keybuf already holds this frame's keys) the coarse
+// depth is rebuilt from the keybuf and the pass rejects points behind it.
 static int launch_render(uint64_t* keybuf, const float* pos, int64_t n, uint64_t base,
-                         const DevCam& cam, bool sgn, cudaStream_t st) {
+                         const DevCam& cam, bool sgn, cudaStream_t st, uint16_t* zmax = nullptr,
+                         bool refresh_first = false) {
   if (n <= 0) return NAR_OK;
   int rc = device_init();
   if (rc) return rc;
   int64_t done = 0;
+  int shift = 3, zw = 1, zh = 1;
+  hiz_geometry(cam.w, cam.h, shift, zw, zh);
+  auto refresh = [&]() {
+    const int64_t nt = ((int64_t)zw * zh) << shift;
+    const unsigned g = (unsigned)((nt + 255) / 256);
+    if (sgn)
+      hiz_kernel<true><<<g, 256, 0, st>>>(keybuf, cam.w, cam.h, shift, zw, zh, zmax);
+    else
+      hiz_kernel<false><<<g, 256, 0, st>>>(keybuf, cam.w, cam.h, shift, zw, zh, zmax);
+  };
   if ((reinterpret_cast<uintptr_t>(pos) & 15) == 0) {
     const int64_t n_tiles = n / kTilePts;
     if (n_tiles > 0) {
-      const int64_t cap = (int64_t)g_num_sms * g_render_blocks_per_sm;
-      const int grid = (int)(n_tiles < cap ? n_tiles : cap);
-      if (sgn)
-        render_tma_kernel<true><<<grid, kRenderThreads, kRenderSmem, st>>>(keybuf, pos, n_tiles,
-                                                                           base, cam);
-      else
-        render_tma_kernel<false><<<grid, kRenderThreads, kRenderSmem, st>>>(keybuf, pos, n_tiles,
-                                                                            base, cam);
+      const int64_t sms = g_num_sms;
+      auto kern = sgn ? (g_dedup ? render_tma_kernel<true, true> : render_tma_kernel<true, false>)
+                      : (g_dedup ? render_tma_kernel<false, true> : render_tma_kernel<false, false>);
+      auto run = [&](ChunkMap cm, bool with_hiz) {
+        HizArgs hz{nullptr, shift, zw, zw * zh};
+        if (with_hiz) {
+          refresh();
+          hz.zmax = zmax;
+        }
+        const int64_t nj = cm.j1 - cm.j0;
+        const int64_t need = (nj + kRenderWarps - 1) / kRenderWarps;
+        const int grid = (int)(need < sms ? need : sms);
+        if (grid > 0) kern<<<grid, kRenderThreads, kRenderSmem, st>>>(keybuf, pos, cm, base, cam, hz);
+      };
+      // Hi-Z schedule: a seed pass over every S-th chunk (spread over the whole
+      // cloud, so the coarse depth covers the screen even for spatially sorted
+      // input), then the remaining chunks in passes, each after a refresh.
+      const int64_t S = kHizSeedStride;
+      const int64_t min_pass = sms * kRenderWarps * 32;  // ~32 steps per warp per pass
+      if (zmax && n_tiles >= S * min_pass / 4) {
+        const int64_t n_seed = (n_tiles + S - 1) / S;
+        run(ChunkMap{0, n_seed, 1}, refresh_first);
+        const int64_t n_rest = n_tiles - n_seed;
+        int64_t passes = n_rest / min_pass;
+        passes = passes < 1 ? 1 : (passes > 6 ? 6 : passes);
+        for (int64_t p = 0; p < passes; ++p)
+          run(ChunkMap{n_rest * p / passes, n_rest * (p + 1) / passes, 2}, true);
+      } else {
+        run(ChunkMap{0, n_tiles, 0}, zmax && refresh_first);
+      }
       done = n_tiles * kTilePts;
     }
   }
@@ -407,6 +725,7 @@ static int render_host_impl(uint64_t* keybuf_dev, const float* pos_host, int64_t
   const int64_t chunk = n < kChunk ? ((n + kTilePts - 1) / kTilePts) * kTilePts : kChunk;
   const int nbuf = n > chunk ? 2 : 1;
   float* dbuf[2] = {nullptr, nullptr};
+  uint16_t* zmax = nullptr;
   cudaStream_t cp = nullptr;
   cudaEvent_t copied[2] = {nullptr, nullptr}, done[2] = {nullptr, nullptr};
   int rc = NAR_OK;
@@ -416,6 +735,9 @@ static int render_host_impl(uint64_t* keybuf_dev, const float* pos_host, int64_t
       break;
     }
   }
+  if (!rc && n > chunk &&
+      cudaMallocAsync(reinterpret_cast<void**>(&zmax), (size_t)kHizMaxEntries * 2, st) != cudaSuccess)
+    rc = set_error(NAR_ERR_NOMEM, "cudaMallocAsync of Hi-Z scratch failed");
   if (!rc && cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking) != cudaSuccess)
     rc = set_error(NAR_ERR_CUDA, "stream creation failed");
   for (int b = 0; b < 2 && !rc; ++b) {
@@ -437,12 +759,14 @@ static int render_host_impl(uint64_t* keybuf_dev, const float* pos_host, int64_t
       }
       cudaEventRecord(copied[b], cp);
       cudaStreamWaitEvent(st, copied[b], 0);
-      rc = launch_render(keybuf_dev, dbuf[b], cnt, base + (uint64_t)off, cam, sgn, st);
+      // chunk k > 0 is tested against the coarse depth of chunks 0..k-1
+      rc = launch_render(keybuf_dev, dbuf[b], cnt, base + (uint64_t)off, cam, sgn, st, zmax, k > 0);
       cudaEventRecord(done[b], st);
     }
   }
   for (int b = 0; b < nbuf; ++b)
     if (dbuf[b]) cudaFreeAsync(dbuf[b], st);
+  if (zmax) cudaFreeAsync(zmax, st);
   for (int b = 0; b < 2; ++b) {
     if (copied[b]) cudaEventDestroy(copied[b]);
     if (done[b]) cudaEventDestroy(done[b]);
@@ -478,6 +802,27 @@ int nar_render(uint64_t* keybuf_dev, const float* positions_dev, int64_t n, uint
   if (n > 0 && (!keybuf_dev || !positions_dev)) return set_error(NAR_ERR_INVALID, "NULL buffer");
   return launch_render(keybuf_dev, positions_dev, n, base_index, make_devcam(*cam),
                        key_domain == NAR_KEYS_SIGNED, (cudaStream_t)stream);
+}
+
+int nar_hiz_scratch_bytes(int32_t width, int32_t height, size_t* bytes) {
+  if (!bytes || width <= 0 || height <= 0) return set_error(NAR_ERR_INVALID, "bad arguments");
+  int shift, zw, zh;
+  hiz_geometry(width, height, shift, zw, zh);
+  *bytes = (size_t)kHizMaxEntries * 2;
+  return NAR_OK;
+}
+
+int nar_render_hiz(uint64_t* keybuf_dev, uint16_t* hiz_scratch_dev, const float* positions_dev,
+                   int64_t n, uint64_t base_index, const nar_camera* cam, int32_t key_domain,
+                   int32_t keybuf_has_frame, void* stream) {
+  int rc = validate_camera(cam);
+  if (rc) return rc;
+  if (n < 0) return set_error(NAR_ERR_INVALID, "negative point count");
+  if (n > 0 && (!keybuf_dev || !positions_dev || !hiz_scratch_dev))
+    return set_error(NAR_ERR_INVALID, "NULL buffer");
+  return launch_render(keybuf_dev, positions_dev, n, base_index, make_devcam(*cam),
+                       key_domain == NAR_KEYS_SIGNED, (cudaStream_t)stream, hiz_scratch_dev,
+                       keybuf_has_frame != 0);
 }
 
 int nar_render_host(uint64_t* keybuf_dev, const float* positions_host, int64_t n,

@@ -286,6 +286,10 @@ class Renderer:
         self.empty = (_lib.EMPTY_KEY ^ _lib.SIGN_FLIP) if signed_keys else _lib.EMPTY_KEY
         npix = self.width * self.height
         self.keybuf = torch.empty(npix, dtype=torch.int64, device=self.device)
+        nb = C.c_size_t(0)
+        _lib.check(_lib.load().nar_hiz_scratch_bytes(self.width, self.height, C.byref(nb)))
+        self.hiz = torch.empty(int(nb.value) // 4, dtype=torch.int32, device=self.device)
+        self.use_hiz = True
         self.pad_multiple = pad_multiple
         self._streams: list = []
         self.clear()
@@ -313,11 +317,21 @@ class Renderer:
         kc = self._check_cam(cam)
         main = stream or torch.cuda.current_stream(self.device)
         segs = cloud.segments
+
+        def launch(sg, st, has_frame):
+            n = int(sg["positions"].shape[0])
+            if self.use_hiz:
+                _lib.call("nar_render_hiz", self.keybuf.data_ptr(), self.hiz.data_ptr(),
+                          sg["positions"].data_ptr(), n, C.c_uint64(sg["begin"]), C.byref(kc),
+                          self.domain, int(has_frame), int(st.cuda_stream))
+            else:
+                _lib.call("nar_render", self.keybuf.data_ptr(), sg["positions"].data_ptr(), n,
+                          C.c_uint64(sg["begin"]), C.byref(kc), self.domain,
+                          int(st.cuda_stream))
+
         if len(segs) <= 1 or not multi_stream:
-            for sg in segs:
-                _lib.call("nar_render", self.keybuf.data_ptr(), sg["positions"].data_ptr(),
-                          int(sg["positions"].shape[0]), C.c_uint64(sg["begin"]), C.byref(kc),
-                          self.domain, int(main.cuda_stream))
+            for k, sg in enumerate(segs):
+                launch(sg, main, k > 0)
             return
         while len(self._streams) < len(segs):
             self._streams.append(torch.cuda.Stream(self.device))
@@ -325,9 +339,7 @@ class Renderer:
         start.record(main)
         for sg, st in zip(segs, self._streams):
             st.wait_event(start)
-            _lib.call("nar_render", self.keybuf.data_ptr(), sg["positions"].data_ptr(),
-                      int(sg["positions"].shape[0]), C.c_uint64(sg["begin"]), C.byref(kc),
-                      self.domain, int(st.cuda_stream))
+            launch(sg, st, False)
         for st in self._streams[: len(segs)]:
             ev = torch.cuda.Event()
             ev.record(st)
@@ -425,8 +437,8 @@ def rasterize(pc: PointCloud, cam: CameraPose, sel: StreamSelection, threads: in
                   C.c_uint64(0), C.byref(kc), r.domain, int(main.cuda_stream))
     else:
         main.wait_stream(side)
-        _lib.call("nar_render", r.keybuf.data_ptr(), pos_dev.data_ptr(), pc.count, C.c_uint64(0),
-                  C.byref(kc), r.domain, int(main.cuda_stream))
+        _lib.call("nar_render_hiz", r.keybuf.data_ptr(), r.hiz.data_ptr(), pos_dev.data_ptr(),
+                  pc.count, C.c_uint64(0), C.byref(kc), r.domain, 0, int(main.cuda_stream))
     main.wait_stream(side)
     meta = {n: _StreamMeta(n, pc.stream(n).format, pc.stream(n).arity) for n in names}
     cloud = DeviceCloud([{"begin": 0, "count": pc.count, "positions": pos_dev,
