@@ -35,47 +35,77 @@ static inline int rup(int x, int m) { return (x + m - 1) / m * m; }
 // ----------------------------------------------------------------------------
 // small kernels: head + level-0 pack, pyramid pool, encoder pool, out head
 // ----------------------------------------------------------------------------
-// y = x @ W + b per pixel in f32 (model.py:135-143); writes the f32 level-0
-// pyramid (for pooling) and its bf16 copy padded to cp channels.
-__global__ void head_kernel(const float* __restrict__ x, int64_t npix, int cin, int cp,
-                            const float* __restrict__ hw, const float* __restrict__ hb,
-                            int use_head, float* __restrict__ y32,
-                            __nv_bfloat16* __restrict__ y16) {
-  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (p >= npix) return;
-  float v[16];
-  for (int c = 0; c < cin; ++c) v[c] = x[p * cin + c];
-  for (int j = 0; j < cp; ++j) {
-    float acc = 0.0f;
-    if (j < cin) {
-      if (use_head) {
-        acc = hb[j];
-        for (int c = 0; c < cin; ++c) acc = fmaf(v[c], hw[c * cin + j], acc);
-      } else {
-        acc = v[j];
-      }
-      y32[p * cin + j] = acc;
-    }
-    y16[p * cp + j] = __float2bfloat16_rn(acc);
-  }
-}
+// Descriptor head + feature pyramid in one pass (model.py:135-155): one CTA
+// per (T x T) level-0 tile, T = 2^(levels-1).  Each thread applies the
+// per-pixel affine head y = x @ W + b in f32; the pyramid levels are 2x2
+// averages of the previous level computed in f32 in shared memory (the
+// reference pools the f32 head output), and every level is written once as
+// bf16 NHWC padded to cp channels (zeros in the padding).
+struct PyrOut {
+  __nv_bfloat16* lvl[8];
+};
 
-// 2x2 average of an f32 (H,W,C) map (autodiff.py:231-245); writes f32 + bf16 (cp).
-__global__ void pool_f32_kernel(const float* __restrict__ src, int H, int W, int C, int cp,
-                                float* __restrict__ dst32, __nv_bfloat16* __restrict__ dst16) {
-  const int Ho = H / 2, Wo = W / 2;
-  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (p >= (int64_t)Ho * Wo) return;
-  const int y = (int)(p / Wo), x = (int)(p % Wo);
-  const float* r0 = src + ((int64_t)(2 * y) * W + 2 * x) * C;
-  const float* r1 = r0 + (int64_t)W * C;
-  for (int c = 0; c < cp; ++c) {
-    float m = 0.0f;
-    if (c < C) {
-      m = ((r0[c] + r0[C + c]) + (r1[c] + r1[C + c])) * 0.25f;
-      dst32[p * C + c] = m;
+__global__ void head_pyramid_kernel(const float* __restrict__ x, int H, int W, int cin, int cp,
+                                    const float* __restrict__ hw, const float* __restrict__ hb,
+                                    int use_head, int levels, PyrOut out) {
+  extern __shared__ float tile[];  // (T*T + T*T/4 + ...) x cin floats
+  const int T = 1 << (levels - 1);
+  const int tx = blockIdx.x, ty = blockIdx.y;
+  const int t = threadIdx.x;
+  const int ly = t / T, lx = t % T;
+  const int y = ty * T + ly, xx = tx * T + lx;
+  // level 0
+  float v[16];
+  const float* px = x + ((size_t)y * W + xx) * cin;
+  for (int c = 0; c < cin; ++c) v[c] = px[c];
+  float* cur = tile;
+  __nv_bfloat16* o0 = out.lvl[0] + ((size_t)y * W + xx) * cp;
+  for (int j = 0; j < cp; j += 2) {
+    float r0 = 0.f, r1 = 0.f;
+    for (int h = 0; h < 2; ++h) {
+      const int jj = j + h;
+      float acc = 0.f;
+      if (jj < cin) {
+        if (use_head) {
+          acc = hb[jj];
+          for (int c = 0; c < cin; ++c) acc = fmaf(v[c], hw[c * cin + jj], acc);
+        } else {
+          acc = v[jj];
+        }
+        cur[t * cin + jj] = acc;
+      }
+      (h == 0 ? r0 : r1) = acc;
     }
-    dst16[p * cp + c] = __float2bfloat16_rn(m);
+    *reinterpret_cast<__nv_bfloat162*>(o0 + j) = __floats2bfloat162_rn(r0, r1);
+  }
+  __syncthreads();
+  // levels 1..L-1
+  int side = T;
+  for (int k = 1; k < levels; ++k) {
+    const int ns = side >> 1;
+    float* nxt = cur + side * side * cin;
+    if (t < ns * ns) {
+      const int qy = t / ns, qx = t % ns;
+      const int Wk = W >> k;
+      __nv_bfloat16* ok = out.lvl[k] + ((size_t)(ty * ns + qy) * Wk + (tx * ns + qx)) * cp;
+      for (int c = 0; c < cp; c += 2) {
+        float r[2];
+        for (int h = 0; h < 2; ++h) {
+          const int cc = c + h;
+          float m = 0.f;
+          if (cc < cin) {
+            const float* a0 = cur + ((2 * qy) * side + 2 * qx) * cin + cc;
+            m = ((a0[0] + a0[cin]) + (a0[side * cin] + a0[side * cin + cin])) * 0.25f;
+            nxt[(qy * ns + qx) * cin + cc] = m;
+          }
+          r[h] = m;
+        }
+        *reinterpret_cast<__nv_bfloat162*>(ok + c) = __floats2bfloat162_rn(r[0], r[1]);
+      }
+    }
+    __syncthreads();
+    cur = nxt;
+    side = ns;
   }
 }
 
@@ -109,7 +139,7 @@ __global__ void pool_bf16_kernel(const __nv_bfloat16* __restrict__ src, int H, i
   *reinterpret_cast<uint4*>(dst + p * C + c8 * 8) = o;
 }
 
-// logits = x @ out.w + out.b, sigmoid (model.py:189-191), f32 out.
+// logits = x @ out.w + out.b, sigmoid (model.py:189-191), f32 out (SIMT path).
 __global__ void out_head_kernel(const __nv_bfloat16* __restrict__ x, int64_t npix, int C,
                                 int cstride, const float* __restrict__ ow,
                                 const float* __restrict__ ob, int cout, float* __restrict__ out) {
@@ -222,7 +252,7 @@ struct Plan {
   int L;
   int H[8], W[8];
   int cinp;             // padded input channel count
-  size_t off_pyr32[8], off_pyr16[8], off_skip[8], off_pool[8], off_tmp[8], off_x[8];
+  size_t off_pyr16[8], off_skip[8], off_pool[8], off_tmp[8], off_x[8];
   size_t total;
 };
 
@@ -241,7 +271,6 @@ static Plan make_plan(const nar_unet& n, int H, int W) {
     p.W[k] = W >> k;
     const size_t px = (size_t)p.H[k] * p.W[k];
     const int w = stride_of(n.cfg, k);
-    p.off_pyr32[k] = take(px * n.cfg.input_channels * 4);
     p.off_pyr16[k] = take(px * p.cinp * 2);
     p.off_skip[k] = take(px * w * 2);
     p.off_tmp[k] = take(px * w * 2);
@@ -289,9 +318,14 @@ static int upload(nar_unet* n) {
   return NAR_OK;
 }
 
+// One gated conv.  pool_out (optional): also write the 2x2 average pool of
+// the output; head_out (optional): write sigmoid(out @ out.w + out.b) in f32
+// (model.py:189-191) -- on the tensor-core path both are fused into the
+// epilogue (out may then be NULL), on the SIMT path they run as kernels.
 static int run_conv(nar_unet* n, Layer& l, const __nv_bfloat16* src_a, int ca_stride, int a_up2,
                     const __nv_bfloat16* src_b, int cb_stride, int H, int W,
-                    __nv_bfloat16* out, cudaStream_t st) {
+                    __nv_bfloat16* out, cudaStream_t st, __nv_bfloat16* pool_out = nullptr,
+                    float* head_out = nullptr, __nv_bfloat16* scratch = nullptr) {
   ConvArgs a;
   memset(&a, 0, sizeof(a));
   a.src_a = src_a;
@@ -311,12 +345,41 @@ static int run_conv(nar_unet* n, Layer& l, const __nv_bfloat16* src_a, int ca_st
   a.bias_g = l.bg;
   a.wtc = reinterpret_cast<const __nv_bfloat16*>(l.wtc);
   a.out = out;
+  const int cst = a.cout_stride;
+  auto pool_kernel = [&](const __nv_bfloat16* src) {
+    const int64_t t = (int64_t)(H / 2) * (W / 2) * (cst / 8);
+    pool_bf16_kernel<<<(unsigned)((t + 255) / 256), 256, 0, st>>>(src, H, W, cst, pool_out);
+  };
+  auto head_kernel = [&](const __nv_bfloat16* src) {
+    const int64_t np = (int64_t)H * W;
+    out_head_kernel<<<(unsigned)((np + 127) / 128), 128, 0, st>>>(
+        src, np, l.cout, cst, n->d_out_w, n->d_out_b, n->cfg.output_channels, head_out);
+  };
   if (n->simt) {
+    if (!a.out) a.out = scratch;
     const int64_t tot = (int64_t)H * W * l.cout;
     gated_conv_simt<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(a);
+    if (pool_out) pool_kernel(a.out);
+    if (head_out) head_kernel(a.out);
     return check_launch(l.name.c_str());
   }
-  return tc_launch_gated_conv(a, st);
+  const bool fuse_pool = pool_out && (tc_rows_for(l.cout) % 2 == 0);
+  if (fuse_pool) a.pool_out = pool_out;
+  if (head_out) {
+    a.head_out = head_out;
+    a.head_w = n->d_out_w;
+    a.head_b = n->d_out_b;
+    a.head_n = n->cfg.output_channels;
+    if (a.head_n > 4) {  // beyond the fused epilogue's register budget
+      a.head_out = nullptr;
+      if (!a.out) a.out = scratch;
+    }
+  }
+  int rc = tc_launch_gated_conv(a, st);
+  if (rc) return rc;
+  if (pool_out && !fuse_pool) pool_kernel(a.out);
+  if (head_out && !a.head_out) head_kernel(a.out);
+  return check_launch(l.name.c_str());
 }
 
 }  // namespace nar
@@ -481,20 +544,18 @@ int nar_unet_forward(nar_unet* n, const float* in, int32_t H, int32_t W, float* 
   cudaStream_t st = (cudaStream_t)stream;
   uint8_t* base = static_cast<uint8_t*>(ws);
   auto bf = [&](size_t off) { return reinterpret_cast<__nv_bfloat16*>(base + off); };
-  auto f32 = [&](size_t off) { return reinterpret_cast<float*>(base + off); };
   const int cin = n->cfg.input_channels, L = p.L;
 
-  const int64_t np0 = (int64_t)H * W;
-  head_kernel<<<(unsigned)((np0 + 255) / 256), 256, 0, st>>>(
-      in, np0, cin, p.cinp, n->d_head_w, n->d_head_b, n->cfg.use_descriptor_head,
-      f32(p.off_pyr32[0]), bf(p.off_pyr16[0]));
-  for (int k = 1; k < L; ++k) {
-    const int64_t npk = (int64_t)p.H[k] * p.W[k];
-    pool_f32_kernel<<<(unsigned)((npk + 255) / 256), 256, 0, st>>>(
-        f32(p.off_pyr32[k - 1]), p.H[k - 1], p.W[k - 1], cin, p.cinp, f32(p.off_pyr32[k]),
-        bf(p.off_pyr16[k]));
+  {
+    const int T = 1 << (L - 1);
+    PyrOut po;
+    for (int k = 0; k < L; ++k) po.lvl[k] = bf(p.off_pyr16[k]);
+    size_t sm = 0;
+    for (int k = 0, side = T; k < L; ++k, side >>= 1) sm += (size_t)side * side * cin * 4;
+    head_pyramid_kernel<<<dim3(W / T, H / T), T * T, sm, st>>>(
+        in, H, W, cin, p.cinp, n->d_head_w, n->d_head_b, n->cfg.use_descriptor_head, L, po);
+    if ((rc = check_launch("head_pyramid"))) return rc;
   }
-  if ((rc = check_launch("pyramid"))) return rc;
 
   int li = 0;
   for (int k = 0; k < L; ++k) {
@@ -508,16 +569,12 @@ int nar_unet_forward(nar_unet* n, const float* in, int32_t H, int32_t W, float* 
                     bf(p.off_pyr16[k]), p.cinp, p.H[k], p.W[k], bf(p.off_tmp[k]), st);
     }
     if (rc) return rc;
+    const bool last = L == 1;
     rc = run_conv(n, lb, bf(p.off_tmp[k]), stride_of(n->cfg, k), 0, nullptr, 0, p.H[k], p.W[k],
-                  bf(p.off_skip[k]), st);
+                  last ? nullptr : bf(p.off_skip[k]), st,
+                  k + 1 < L ? bf(p.off_pool[k]) : nullptr, last ? out : nullptr,
+                  bf(p.off_skip[k]));
     if (rc) return rc;
-    if (k + 1 < L) {
-      const int w = stride_of(n->cfg, k);
-      const int64_t t = (int64_t)p.H[k + 1] * p.W[k + 1] * (w / 8);
-      pool_bf16_kernel<<<(unsigned)((t + 255) / 256), 256, 0, st>>>(
-          bf(p.off_skip[k]), p.H[k], p.W[k], w, bf(p.off_pool[k]));
-      if ((rc = check_launch("pool"))) return rc;
-    }
   }
   const __nv_bfloat16* x = bf(p.off_skip[L - 1]);
   for (int k = L - 2; k >= 0; --k) {
@@ -526,15 +583,14 @@ int nar_unet_forward(nar_unet* n, const float* in, int32_t H, int32_t W, float* 
     rc = run_conv(n, la, x, stride_of(n->cfg, k + 1), 1, bf(p.off_skip[k]), stride_of(n->cfg, k),
                   p.H[k], p.W[k], bf(p.off_tmp[k]), st);
     if (rc) return rc;
+    // dec0b: the out head (1x1 conv + sigmoid) is fused into the epilogue
     rc = run_conv(n, lb, bf(p.off_tmp[k]), stride_of(n->cfg, k), 0, nullptr, 0, p.H[k], p.W[k],
-                  bf(p.off_x[k]), st);
+                  k == 0 ? nullptr : bf(p.off_x[k]), st, nullptr, k == 0 ? out : nullptr,
+                  bf(p.off_x[k]));
     if (rc) return rc;
     x = bf(p.off_x[k]);
   }
-  out_head_kernel<<<(unsigned)((np0 + 127) / 128), 128, 0, st>>>(
-      x, np0, width_of(n->cfg, 0), stride_of(n->cfg, 0), n->d_out_w, n->d_out_b,
-      n->cfg.output_channels, out);
-  return check_launch("out_head");
+  return NAR_OK;
 }
 
 }  // extern "C"

@@ -7,23 +7,34 @@
 //   K = 9 taps x input channels (16-channel chunks).
 //
 // CTA roles (288 threads, 1 CTA per SM, persistent over tiles):
-//   warps 0-3  producer: per (tile, 16-channel chunk) stage, cp.async gathers
-//              the (R+2) x 130 pixel halo of the chunk into shared memory in
-//              the UMMA no-swizzle K-major layout [row][k8][px][16 B] (zero
-//              fill for padding, address math for concat / up2); thread 0
-//              streams the chunk's pre-packed weights with a TMA bulk copy.
+//   warps 0-3  producer.  Lane 0 of warp 0 issues, per (tile, 16-channel
+//              chunk) stage, two TMA tensor loads (one per 8-channel slab) of
+//              the (R+2) x 130 pixel halo straight into the UMMA no-swizzle
+//              K-major layout [k8][row][px][16 B]; TMA zero-fills the image
+//              border ("same" padding) and the concat is just a second tensor
+//              map.  For the decoder's up2(srcA) chunks the low-resolution
+//              halo is TMA-loaded into a staging area and the 128 producer
+//              threads replicate it 2x2 into the halo.  A TMA bulk copy
+//              streams the chunk's pre-packed weights.
 //   warp 8     MMA issuer (one elected thread) + TMEM owner: for each of the
 //              9 taps and R rows one tcgen05.mma (M=128, N, K=16) whose A
 //              descriptor is the halo row shifted by the tap (a 16-byte start
 //              address offset: pixels are contiguous 16 B rows, SBO = 128 B).
 //   warps 4-7  epilogue: tcgen05.ld the f and g accumulators of their TMEM
-//              lane quarter, apply the gate, store bf16 NHWC.
+//              lane quarter, apply the gate; store bf16 NHWC, and optionally
+//              the 2x2 average pool of the output (encoder skips feeding the
+//              next level) and/or the final 1x1 out head + sigmoid
+//              (model.py:189-191) in f32 instead of the bf16 activation.
 // Accumulators are double buffered in TMEM (2 x R x N <= 512 columns) so the
 // epilogue of tile i overlaps the MMAs of tile i+1.
 #pragma once
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include <stdint.h>
+#include <stdio.h>
+#include <string.h>
 
 #include <vector>
 
@@ -42,21 +53,40 @@ struct ConvArgs {
   const float* bias_f;
   const float* bias_g;
   const __nv_bfloat16* wtc;    // tcgen05 path: packed (see tc_pack_weights)
-  __nv_bfloat16* out;
+  __nv_bfloat16* out;          // bf16 output, or NULL (out head only)
+  __nv_bfloat16* pool_out;     // 2x2-average-pooled output (H/2, W/2, cout_stride), or NULL
+  const float* head_w;         // fused out head: (cout, head_n) f32, or NULL
+  const float* head_b;
+  float* head_out;             // (H, W, head_n) f32
+  int head_n;
 };
 
-constexpr int kTcThreads = 288;
+constexpr int kTcThreads = 416;  // 4 producer + 8 epilogue + 1 MMA warps
+constexpr int kMmaWarp = 12;
 constexpr int kHaloPx = 130;
-constexpr int kHaloRowBytes = 2 * kHaloPx * 16;  // two 8-channel slabs
+constexpr int kHaloRowBytes = kHaloPx * 16;  // one 8-channel slab row
+constexpr int kLowPx = 66;                   // low-res pixels behind a 130-px halo
 
 __host__ __device__ constexpr int tc_rows(int N) { return N >= 256 ? 1 : (256 / N > 8 ? 8 : 256 / N); }
-__host__ __device__ constexpr int tc_a_bytes(int N) { return (tc_rows(N) + 2) * kHaloRowBytes; }
+__host__ __device__ constexpr int tc_low_rows(int N) { return tc_rows(N) / 2 + 2; }
+// TMA tensor-load destinations must be 128-byte aligned: slabs are padded.
+__host__ __device__ constexpr int tc_r128(int x) { return (x + 127) / 128 * 128; }
+__host__ __device__ constexpr int tc_slab(int N) { return tc_r128((tc_rows(N) + 2) * kHaloRowBytes); }
+__host__ __device__ constexpr int tc_a_bytes(int N) { return 2 * tc_slab(N); }
 __host__ __device__ constexpr int tc_b_bytes(int N) { return 9 * N * 32; }
+// staging: one TMA box of whole 16-channel chunks (32 B per pixel), either the
+// (R+2) x 130 halo or, for up2 sources, the low-res (LR x 66) halo
+__host__ __device__ constexpr int tc_stg_bytes(int N) { return tc_r128((tc_rows(N) + 2) * kHaloPx * 32); }
 __host__ __device__ constexpr int tc_stage_bytes(int N) { return tc_a_bytes(N) + tc_b_bytes(N); }
 __host__ __device__ constexpr int tc_stages(int N) {
-  return (200 * 1024) / tc_stage_bytes(N) > 4 ? 4 : (200 * 1024) / tc_stage_bytes(N);
+  return (200 * 1024 - 2 * tc_stg_bytes(N)) / tc_stage_bytes(N) > 4
+             ? 4
+             : (200 * 1024 - 2 * tc_stg_bytes(N)) / tc_stage_bytes(N);
 }
-__host__ __device__ constexpr int tc_smem(int N) { return tc_stages(N) * tc_stage_bytes(N) + 256; }
+constexpr int kTcParamFloats = 144 + 144 + 128 * 4 + 4;  // bias_f, bias_g, head_w, head_b
+__host__ __device__ constexpr int tc_smem(int N) {
+  return tc_stages(N) * tc_stage_bytes(N) + 2 * tc_stg_bytes(N) + 512 + kTcParamFloats * 4;
+}
 
 // Host: pack HWIO f32 weights into bf16 [chunk q][tap][k8][n][8] where
 // n < Coutp indexes f outputs and n >= Coutp g outputs (zero padded).
@@ -90,7 +120,7 @@ inline void tc_pack_weights(const std::vector<float>& wf, const std::vector<floa
 }
 
 // ---------------------------------------------------------------------------
-// device helpers (tcgen05 / TMEM / cp.async)
+// device helpers (tcgen05 / TMEM / TMA)
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   // SWIZZLE_NONE K-major: start>>4 [0,14), LBO>>4 [16,30), SBO>>4 [32,46),
@@ -146,24 +176,36 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
-               "r"(valid ? 16 : 0)
-               : "memory");
+// 3-D TMA tensor load (tile mode) into shared memory, completing on `bar`.
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
 
 __device__ __forceinline__ float tanh_approx(float x) {
@@ -182,22 +224,37 @@ __device__ __forceinline__ float gate(float f, float g) {
 // the kernel
 // ---------------------------------------------------------------------------
 template <int N>
-__global__ void __launch_bounds__(kTcThreads, 1) gated_conv_tc(const ConvArgs a) {
+__global__ void __launch_bounds__(kTcThreads, 1)
+    gated_conv_tc(const ConvArgs a, const __grid_constant__ CUtensorMap tma_a,
+                  const __grid_constant__ CUtensorMap tma_b) {
   constexpr int R = tc_rows(N);
+  constexpr int LR = tc_low_rows(N);
   constexpr int S = tc_stages(N);
   constexpr int A_BYTES = tc_a_bytes(N);
   constexpr int B_BYTES = tc_b_bytes(N);
-  constexpr int STAGE = A_BYTES + B_BYTES;
+  constexpr int STG_BYTES = tc_stg_bytes(N);
+  constexpr int STAGE = tc_stage_bytes(N);
+  constexpr int SLAB = tc_slab(N);
+  static_assert(A_BYTES % 128 == 0 && B_BYTES % 128 == 0 && STG_BYTES % 128 == 0, "align");
+  constexpr uint32_t STG_TX = (R + 2) * kHaloPx * 32;  // bytes of a direct halo box
+  constexpr uint32_t LOW_TX = LR * kLowPx * 32;        // bytes of an up2 low-res box
   constexpr int COUTP = N / 2;
   constexpr uint32_t IDESC = umma_idesc_bf16(128, N);
   static_assert(2 * R * N <= 512, "TMEM budget");
+  static_assert(S >= 2, "pipeline depth");
 
-  extern __shared__ __align__(128) uint8_t smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * STAGE);
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* stg_buf = smem + S * STAGE;  // 2 staging buffers
+  uint64_t* full = reinterpret_cast<uint64_t*>(stg_buf + 2 * STG_BYTES);
   uint64_t* empty = full + S;
-  uint64_t* tfull = empty + S;
+  uint64_t* stg = empty + S;  // 2 used
+  uint64_t* tfull = stg + S;
   uint64_t* tempty = tfull + 2;
   uint32_t* tbase_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* sbias_f = reinterpret_cast<float*>(stg_buf + 2 * STG_BYTES + 512);
+  float* sbias_g = sbias_f + 144;
+  float* shead_w = sbias_g + 144;
+  float* shead_b = shead_w + 512;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles_x = (a.W + 127) / 128;
@@ -207,16 +264,26 @@ __global__ void __launch_bounds__(kTcThreads, 1) gated_conv_tc(const ConvArgs a)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 129);
+      mbar_init(&full[s], 2);
       mbar_init(&empty[s], 1);
+      mbar_init(&stg[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 4);
+      mbar_init(&tempty[b], 8);
     }
     fence_mbar_init();
+    prefetch_tmap(&tma_a);
+    if (nqb) prefetch_tmap(&tma_b);
   }
-  if (warp == 8) {
+  for (int i = threadIdx.x; i < 144; i += kTcThreads) {
+    sbias_f[i] = i < a.cout ? a.bias_f[i] : 0.0f;
+    sbias_g[i] = i < a.cout ? a.bias_g[i] : 0.0f;
+  }
+  if (a.head_out)
+    for (int i = threadIdx.x; i < a.cout * a.head_n; i += kTcThreads) shead_w[i] = a.head_w[i];
+  if (a.head_out && threadIdx.x < a.head_n) shead_b[threadIdx.x] = a.head_b[threadIdx.x];
+  if (warp == kMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
                      smem_u32(tbase_slot))
                  : "memory");
@@ -229,54 +296,71 @@ __global__ void __launch_bounds__(kTcThreads, 1) gated_conv_tc(const ConvArgs a)
 
   if (warp < 4) {
     // ------------------------------ producer ------------------------------
+    // Stage `it` = (tile, chunk q).  Lane 0 of warp 0 TMA-loads the chunk's
+    // halo box (whole 16-channel pixels, 32 B wide) into staging buffer it&1
+    // one stage ahead, and streams the weights; the 128 producer threads then
+    // reshape staging -> the UMMA layout [k8][row][px][16 B] (replicating
+    // 2x2 for up2 sources) and release the stage to the MMA warp.
     const int t = threadIdx.x;
-    int it = 0;
-    int pending = -1;  // stage whose cp.async group is still in flight
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int n_it = my_tiles * nq;
+    auto issue_staging = [&](int it) {
+      const int tile = blockIdx.x + (it / nq) * gridDim.x, q = it % nq;
       const int y0 = (tile / tiles_x) * R, x0 = (tile % tiles_x) * 128;
-      for (int q = 0; q < nq; ++q, ++it) {
-        const int s = it % S;
-        const uint32_t ph = (uint32_t)(it / S) & 1u;
+      const bool in_a = q < nqa;
+      const int cbase = 16 * (in_a ? q : q - nqa);
+      uint8_t* buf = stg_buf + (it & 1) * STG_BYTES;
+      if (in_a && a.a_up2) {
+        mbar_expect_tx(&stg[it & 1], LOW_TX);
+        tma_load_3d(buf, &tma_a, cbase, (x0 - 1) >> 1, (y0 - 1) >> 1, &stg[it & 1]);
+      } else {
+        mbar_expect_tx(&stg[it & 1], STG_TX);
+        tma_load_3d(buf, in_a ? &tma_a : &tma_b, cbase, x0 - 1, y0 - 1, &stg[it & 1]);
+      }
+    };
+    if (t == 0 && n_it > 0) issue_staging(0);
+    for (int it = 0; it < n_it; ++it) {
+      const int tile = blockIdx.x + (it / nq) * gridDim.x, q = it % nq;
+      const int y0 = (tile / tiles_x) * R, x0 = (tile % tiles_x) * 128;
+      const int s = it % S;
+      const uint32_t ph = (uint32_t)(it / S) & 1u;
+      uint8_t* stA = smem + s * STAGE;
+      uint8_t* stB = stA + A_BYTES;
+      const uint8_t* buf = stg_buf + (it & 1) * STG_BYTES;
+      const bool up2 = q < nqa && a.a_up2;
+      if (t == 0) {
+        if (it + 1 < n_it) issue_staging(it + 1);  // overlaps this stage's reshape
         mbar_wait(&empty[s], ph ^ 1u);
-        uint8_t* stA = smem + s * STAGE;
-        if (t == 0) {
-          mbar_expect_tx(&full[s], B_BYTES);
-          bulk_g2s(stA + A_BYTES, a.wtc + (size_t)q * (B_BYTES / 2), B_BYTES, &full[s]);
-        }
-        const bool in_a = q < nqa;
-        const __nv_bfloat16* src = in_a ? a.src_a : a.src_b;
-        const int cst = in_a ? a.ca_stride : a.cb_stride;
-        const int cbase = 16 * (in_a ? q : q - nqa);
-        const bool up2 = in_a && a.a_up2;
-        const int ws = up2 ? a.W / 2 : a.W;
-        const uint32_t dst0 = smem_u32(stA);
-        constexpr int ITEMS = (R + 2) * kHaloPx * 2;
+        mbar_expect_tx(&full[s], B_BYTES);
+        bulk_g2s(stB, a.wtc + (size_t)q * (B_BYTES / 2), B_BYTES, &full[s]);
+      }
+      mbar_wait(&empty[s], ph ^ 1u);
+      mbar_wait(&stg[it & 1], (uint32_t)(it >> 1) & 1u);
+      constexpr int ITEMS = 2 * (R + 2) * kHaloPx;
+      if (up2) {
+        const int ly0 = (y0 - 1) >> 1, lx0 = (x0 - 1) >> 1;
         for (int i = t; i < ITEMS; i += 128) {
           const int k8 = i & 1;
           const int j = (i >> 1) % kHaloPx;
           const int row = (i >> 1) / kHaloPx;
-          const int y = y0 - 1 + row, x = x0 - 1 + j;
-          const bool ok = y >= 0 && y < a.H && x >= 0 && x < a.W;
-          const int ys = up2 ? (y >> 1) : y, xs = up2 ? (x >> 1) : x;
-          const __nv_bfloat16* g =
-              src + ((size_t)(ok ? ys : 0) * ws + (ok ? xs : 0)) * cst + cbase + 8 * k8;
-          cp_async16(dst0 + row * kHaloRowBytes + k8 * (kHaloPx * 16) + j * 16, g, ok);
+          const int ly = ((y0 - 1 + row) >> 1) - ly0;
+          const int lx = ((x0 - 1 + j) >> 1) - lx0;
+          const uint4 v = *reinterpret_cast<const uint4*>(buf + (ly * kLowPx + lx) * 32 + k8 * 16);
+          *reinterpret_cast<uint4*>(stA + k8 * SLAB + row * kHaloRowBytes + j * 16) = v;
         }
-        cp_async_commit();
-        if (pending >= 0) {
-          cp_async_wait<1>();
-          fence_proxy_async();
-          mbar_arrive(&full[pending]);
+      } else {
+        for (int i = t; i < ITEMS; i += 128) {
+          const int k8 = i & 1;
+          const int rj = i >> 1;  // row * 130 + j
+          const uint4 v = *reinterpret_cast<const uint4*>(buf + rj * 32 + k8 * 16);
+          *reinterpret_cast<uint4*>(stA + k8 * SLAB + rj * 16) = v;
         }
-        pending = s;
       }
+      fence_proxy_async_smem();
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (t == 0) mbar_arrive(&full[s]);
     }
-    if (pending >= 0) {
-      cp_async_wait<0>();
-      fence_proxy_async();
-      mbar_arrive(&full[pending]);
-    }
-  } else if (warp == 8) {
+  } else if (warp == kMmaWarp) {
     // ------------------------------ MMA issuer -----------------------------
     int it = 0, tl = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tl) {
@@ -298,7 +382,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) gated_conv_tc(const ConvArgs a)
 #pragma unroll
             for (int r = 0; r < R; ++r) {
               const uint64_t adesc =
-                  umma_desc(sa + (r + ky) * kHaloRowBytes + kx * 16, kHaloPx * 16, 128);
+                  umma_desc(sa + (r + ky) * kHaloRowBytes + kx * 16, SLAB, 128);
               umma_bf16(dcol + r * N, adesc, bdesc, IDESC, (q > 0 || tap > 0) ? 1u : 0u);
             }
           }
@@ -310,8 +394,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) gated_conv_tc(const ConvArgs a)
     }
   } else {
     // ------------------------------ epilogue -------------------------------
-    const int quarter = warp & 3;  // TMEM lanes 32*quarter .. +31
+    // 8 warps: warp w covers TMEM lanes 32*(w%4)..+31 (pixels) and the row
+    // groups g with g % 2 == (w-4)/4 (a group is one row, or two for pooling).
+    // Channels are processed 16 at a time (one x16 TMEM load per branch and
+    // row, one wait), biases held in registers across the rows.
+    const int quarter = warp & 3;
+    const int half = (warp - 4) >> 2;
     const int m = quarter * 32 + lane;
+    const bool do_pool = a.pool_out != nullptr;  // requires R even (host-checked)
+    const bool do_head = a.head_out != nullptr;
+    const int rstep = do_pool ? 2 : 1;
+    constexpr int RPW = R > 1 ? R / 2 : 1;  // rows per warp, upper bound
+    const int nch = (a.cout_stride + 15) / 16;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     int tl = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tl) {
       const int b = tl & 1;
@@ -319,33 +414,118 @@ __global__ void __launch_bounds__(kTcThreads, 1) gated_conv_tc(const ConvArgs a)
       mbar_wait(&tfull[b], ((uint32_t)tl >> 1) & 1u);
       tc_fence_after();
       const int x = x0 + m;
-#pragma unroll 1
-      for (int r = 0; r < R; ++r) {
-        const int y = y0 + r;
-        const uint32_t col = tbase + (uint32_t)(b * R * N + r * N) + ((uint32_t)(quarter * 32) << 16);
-        __nv_bfloat16* dst = a.out + ((size_t)y * a.W + x) * a.cout_stride;
-        const bool ok = y < a.H && x < a.W;
-#pragma unroll 1
-        for (int c8 = 0; c8 < a.cout_stride / 8; ++c8) {
-          float f[8], g[8];
-          if (c8 * 8 < COUTP) {
-            tmem_ld8(col + c8 * 8, f);
-            tmem_ld8(col + COUTP + c8 * 8, g);
-            tmem_wait_ld();
-          }
-          uint4 pk;
-          uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
+      const bool xok = x < a.W;
+      float logit[RPW][4];
+      if (do_head) {
 #pragma unroll
-          for (int e = 0; e < 8; e += 2) {
-            const int j = c8 * 8 + e;
-            float o0 = 0.0f, o1 = 0.0f;
-            if (j < a.cout) o0 = gate(f[e] + __ldg(a.bias_f + j), g[e] + __ldg(a.bias_g + j));
-            if (j + 1 < a.cout)
-              o1 = gate(f[e + 1] + __ldg(a.bias_f + j + 1), g[e + 1] + __ldg(a.bias_g + j + 1));
-            __nv_bfloat162 h = __floats2bfloat162_rn(o0, o1);
-            pw[e / 2] = *reinterpret_cast<uint32_t*>(&h);
+        for (int i = 0; i < RPW; ++i)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) logit[i][k] = 0.0f;
+      }
+#pragma unroll 1
+      for (int ch = 0; ch < nch; ++ch) {
+        const int c0 = ch * 16;
+        const bool two = c0 + 8 < COUTP;  // second 8-channel group has accumulators
+        float bfv[16], bgv[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          bfv[e] = sbias_f[c0 + e];
+          bgv[e] = sbias_g[c0 + e];
+        }
+        int slot = 0;
+#pragma unroll 1
+        for (int r = half * rstep; r < R; r += 2 * rstep, slot += rstep) {
+          float o[2][16];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            if (h == 1 && !do_pool) break;
+            float f[16], g[16];
+            const uint32_t col = tbase + (uint32_t)(b * R * N + (r + h) * N + c0) + lane_off;
+            if (two) {
+              tmem_ld16(col, f);
+              tmem_ld16(col + COUTP, g);
+            } else {
+              tmem_ld8(col, f);
+              tmem_ld8(col + COUTP, g);
+#pragma unroll
+              for (int e = 8; e < 16; ++e) f[e] = g[e] = 0.0f;
+            }
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+              o[h][e] = (c0 + e < a.cout) ? gate(f[e] + bfv[e], g[e] + bgv[e]) : 0.0f;
+            const int y = y0 + r + h;
+            const bool ok = y < a.H && xok;
+            if (a.out != nullptr && ok) {
+              __nv_bfloat16* dst = a.out + ((size_t)y * a.W + x) * a.cout_stride + c0;
+#pragma unroll
+              for (int g8 = 0; g8 < 2; ++g8) {
+                if (g8 == 1 && c0 + 8 >= a.cout_stride) break;
+                uint4 pk;
+                uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+                for (int e = 0; e < 8; e += 2) {
+                  __nv_bfloat162 hh = __floats2bfloat162_rn(o[h][g8 * 8 + e], o[h][g8 * 8 + e + 1]);
+                  pw[e / 2] = *reinterpret_cast<uint32_t*>(&hh);
+                }
+                *reinterpret_cast<uint4*>(dst + g8 * 8) = pk;
+              }
+            }
+            if (do_head) {
+#pragma unroll
+              for (int e = 0; e < 16; ++e)
+                if (c0 + e < a.cout)
+#pragma unroll
+                  for (int k = 0; k < 4; ++k)
+                    if (k < a.head_n)
+                      logit[slot + h][k] =
+                          fmaf(o[h][e], shead_w[(c0 + e) * a.head_n + k], logit[slot + h][k]);
+            }
           }
-          if (ok) *reinterpret_cast<uint4*>(dst + c8 * 8) = pk;
+          if (do_pool) {
+            // 2x2 average of the f32 outputs: rows r, r+1 here, columns m, m+1 via shuffle
+            float v[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              v[e] = o[0][e] + o[1][e];
+              v[e] += __shfl_xor_sync(0xffffffffu, v[e], 1);
+            }
+            const int y = y0 + r;
+            if ((m & 1) == 0 && y < a.H && xok) {
+              __nv_bfloat16* dst = a.pool_out +
+                                   ((size_t)(y >> 1) * (a.W >> 1) + (x >> 1)) * a.cout_stride + c0;
+#pragma unroll
+              for (int g8 = 0; g8 < 2; ++g8) {
+                if (g8 == 1 && c0 + 8 >= a.cout_stride) break;
+                uint4 pk;
+                uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+                for (int e = 0; e < 8; e += 2) {
+                  __nv_bfloat162 hh = __floats2bfloat162_rn(0.25f * v[g8 * 8 + e],
+                                                            0.25f * v[g8 * 8 + e + 1]);
+                  pw[e / 2] = *reinterpret_cast<uint32_t*>(&hh);
+                }
+                *reinterpret_cast<uint4*>(dst + g8 * 8) = pk;
+              }
+            }
+          }
+        }
+      }
+      if (do_head) {
+        int slot = 0;
+#pragma unroll 1
+        for (int r = half * rstep; r < R; r += 2 * rstep, slot += rstep) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            if (h == 1 && !do_pool) break;
+            const int y = y0 + r + h;
+            if (y < a.H && xok) {
+              float* dst = a.head_out + ((size_t)y * a.W + x) * a.head_n;
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                if (k < a.head_n) dst[k] = 1.0f / (1.0f + __expf(-(logit[slot + h][k] + shead_b[k])));
+            }
+          }
         }
       }
       tc_fence_before();
@@ -356,31 +536,83 @@ __global__ void __launch_bounds__(kTcThreads, 1) gated_conv_tc(const ConvArgs a)
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 8) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase)
                  : "memory");
   }
 }
 
+// ---------------------------------------------------------------------------
+// host launch
+// ---------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 tc_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// NHWC bf16 tensor (h, w, cs) -> 3-D map over (channel, x, y), box {16, bw, bh}.
+static int tc_make_map(CUtensorMap* m, const void* base, int cs, int w, int h, int bw, int bh) {
+  auto fn = tc_encode_fn();
+  if (!fn) return set_error(NAR_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {(cuuint64_t)cs, (cuuint64_t)w, (cuuint64_t)h};
+  cuuint64_t strides[2] = {(cuuint64_t)cs * 2, (cuuint64_t)cs * 2 * (cuuint64_t)w};
+  cuuint32_t box[3] = {16, (cuuint32_t)bw, (cuuint32_t)bh};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                  box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(NAR_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  return NAR_OK;
+}
+
 template <int N>
 static int tc_launch_n(const ConvArgs& a, cudaStream_t st) {
   static bool attr_done = false;
   if (!attr_done) {
-    if (cudaFuncSetAttribute(gated_conv_tc<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             tc_smem(N)) != cudaSuccess)
-      return set_error(NAR_ERR_CUDA, "cannot set conv smem size");
+    const cudaError_t e = cudaFuncSetAttribute(
+        gated_conv_tc<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem(N));
+    if (e != cudaSuccess) {
+      char msg[160];
+      snprintf(msg, sizeof(msg), "cannot set conv smem size %d: %s", tc_smem(N),
+               cudaGetErrorString(e));
+      return set_error(NAR_ERR_CUDA, msg);
+    }
     attr_done = true;
+  }
+  constexpr int R = tc_rows(N);
+  if (a.pool_out && (R & 1)) return set_error(NAR_ERR_CONFIG, "fused pool needs an even row tile");
+  CUtensorMap ma, mb;
+  int rc;
+  if (a.a_up2)
+    rc = tc_make_map(&ma, a.src_a, a.ca_stride, a.W / 2, a.H / 2, kLowPx, tc_low_rows(N));
+  else
+    rc = tc_make_map(&ma, a.src_a, a.ca_stride, a.W, a.H, kHaloPx, R + 2);
+  if (rc) return rc;
+  if (a.cb) {
+    rc = tc_make_map(&mb, a.src_b, a.cb_stride, a.W, a.H, kHaloPx, R + 2);
+    if (rc) return rc;
+  } else {
+    mb = ma;
   }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int R = tc_rows(N);
   const int tiles = ((a.W + 127) / 128) * ((a.H + R - 1) / R);
   const int grid = tiles < sms ? tiles : sms;
-  gated_conv_tc<N><<<grid, kTcThreads, tc_smem(N), st>>>(a);
+  gated_conv_tc<N><<<grid, kTcThreads, tc_smem(N), st>>>(a, ma, mb);
   return check_launch("gated_conv_tc");
 }
+
+inline int tc_rows_for(int cout) { return tc_rows(2 * ((cout + 7) / 8 * 8)); }
 
 inline int tc_launch_gated_conv(const ConvArgs& a, cudaStream_t st) {
   const int coutp = (a.cout + 7) / 8 * 8;
@@ -388,6 +620,8 @@ inline int tc_launch_gated_conv(const ConvArgs& a, cudaStream_t st) {
     return set_error(NAR_ERR_CONFIG, "conv output stride must be a multiple of 8 >= Coutp");
   if (a.ca_stride % 16 || (a.cb && a.cb_stride % 16))
     return set_error(NAR_ERR_CONFIG, "conv input strides must be multiples of 16");
+  if (a.head_out && (a.head_n < 1 || a.head_n > 4))
+    return set_error(NAR_ERR_CONFIG, "fused out head supports 1..4 outputs");
   switch (2 * coutp) {
     case 16: return tc_launch_n<16>(a, st);
     case 32: return tc_launch_n<32>(a, st);

@@ -161,8 +161,12 @@ class UNet:
         self._ws = {}
 
     def launches_per_forward(self) -> int:
+        """Kernels per forward on the tensor-core path: head+pyramid, the gated
+        convs, plus one standalone pool for levels whose row tile is odd."""
         L = self.config.levels
-        return 1 + (L - 1) + 2 * L + 2 * (L - 1) + (L - 1) + 1
+        odd_pool = sum(1 for k in range(L - 1)
+                       if 2 * (-(-self.config.width(k) // 8) * 8) >= 256)
+        return 1 + 2 * L + 2 * (L - 1) + odd_pool
 
     def _workspace(self, H: int, W: int):
         import torch
