@@ -333,7 +333,14 @@ def main_ours(args):
     torch.cuda.synchronize()
     log(f"[rank {rank}] generated {cloud.count / 1e6:.0f}M points in {time.time() - t_gen:.1f}s")
     cam = look_at(eye, (0, 0, 0), Intrinsics(width=W, height=H))
-    r = Renderer(W, H, device=dev, signed_keys=world > 1, pad_multiple=16)
+    if world > 1:
+        from paper_2407_19097_b200.parallel import ShardedRenderer
+
+        sr = ShardedRenderer(W, H, device=dev, pad_multiple=16)
+        r = sr.r
+    else:
+        sr = None
+        r = Renderer(W, H, device=dev, pad_multiple=16)
     names = sel.channel_names(cloud)
     out = r.alloc_outputs(len(names))
     main = torch.cuda.current_stream(dev)
@@ -354,9 +361,11 @@ def main_ours(args):
         if ev_r1 is not None:
             ev_r1.record(main)
         if world > 1:
-            dist.all_reduce(r.keybuf, op=dist.ReduceOp.MIN)
+            from paper_2407_19097_b200.parallel import composite_keys, reduce_planes
+
+            composite_keys(r.keybuf)
             r.resolve(cloud, cam, sel, out=out, owner_only=True)
-            dist.reduce(out["data"].view(torch.int32), dst=0, op=dist.ReduceOp.SUM)
+            reduce_planes(out["data"], dst=0)
         else:
             r.resolve(cloud, cam, sel, out=out)
         if unet is not None and rank == 0:
@@ -428,6 +437,38 @@ def main_ours(args):
                "api": "paper_2407_19097_b200.msr.rasterize(pinned host PointCloud)"}
         del host_pos, host_rgb, pc
 
+    # ---- full NAR frame on the same cloud: render + resolve + U-Net ----------
+    pipeline = None
+    if world == 1 and args.workload in ("c2", "c3") and not args.no_pipeline:
+        from paper_2407_19097_b200.neural import UNet, UNetConfig, init_params
+
+        cfg = UNetConfig(input_channels=len(names))
+        net = UNet(cfg, init_params(cfg), device=dev)
+        ph, pw = out["data"].shape[:2]
+        y = torch.empty((ph, pw, 3), dtype=torch.float32, device=dev)
+        for _ in range(3):
+            frame()
+            net.forward_into(out["data"], y)
+        torch.cuda.synchronize()
+        kp = max(3, min(args.steps, 20))
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(kp)]
+        for k in range(kp):
+            ev[k][0].record(main)
+            frame()
+            ev[k][1].record(main)
+            net.forward_into(out["data"], y)
+            ev[k][2].record(main)
+        torch.cuda.synchronize()
+        fr = sorted(a.elapsed_time(c) for a, _, c in ev)
+        un = sorted(b.elapsed_time(c) for _, b, c in ev)
+        med = fr[len(fr) // 2]
+        pipeline = {"workload": f"{desc} + U-Net (random init, {len(names)} input channels) at {pw}x{ph}",
+                    "ms_per_frame_median": med, "fps": 1e3 / med,
+                    "unet_ms_median": un[len(un) // 2],
+                    "unet_tflops": (413.7e9 / 1e12 / (un[len(un) // 2] * 1e-3))
+                    if len(names) == 4 else None,
+                    "frames": kp}
+
     cpu = None
     if not args.no_cpu and world == 1 and rank == 0:
         cpu = run_cpu_baseline(W, H, min(n_pts, 35_000_000))
@@ -460,6 +501,7 @@ def main_ours(args):
                          "kernel": "render_tma_kernel", "bytes_per_point": BYTES_PER_POINT},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "pipeline": pipeline,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
         }
@@ -478,6 +520,7 @@ def main():
     ap.add_argument("--points", type=int, default=0, help="override points per GPU")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-pipeline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -1,0 +1,117 @@
+"""Multi-process (world_size 2, gloo, CPU) checks of the sharded composite.
+
+The GPU render/resolve kernels cannot run here, so each rank produces its
+shard's keybuf and owner-only planes with the CPU oracle; the product's
+composite (int64 MIN all-reduce in the signed key domain) and plane reduction
+(int32 SUM of float bit patterns) must then reproduce the single-process
+reference exactly -- the property the NCCL path relies on.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _scene():
+    from paper_2407_19097_b200.geometry import Intrinsics, PointCloud, Stream, look_at
+
+    rng = np.random.default_rng(123)
+    n = 40_000
+    pos = rng.uniform(-1, 1, (n, 3)).astype(np.float32)
+    pos[rng.integers(0, n, 2000)] = pos[rng.integers(0, n, 2000)]  # cross-shard ties
+    vel = rng.normal(size=(n, 3)).astype(np.float32)
+    vel[::7] = -0.0
+    pc = PointCloud(pos, [Stream("rgb", "u8", rng.integers(0, 256, (n, 3), dtype=np.uint8)),
+                          Stream("velocity", "f32", vel)])
+    cam = look_at((0.3, -2.4, 1.1), (0, 0, 0), Intrinsics(width=96, height=72))
+    return pc, cam
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2407_19097_b200 import parallel
+        from paper_2407_19097_b200.msr import StreamSelection
+
+        pc, cam = _scene()
+        i = cam.intrinsics
+        lo, hi = parallel.shard_range(pc.count, rank, world)
+        kb = np.full(i.width * i.height, oracle.EMPTY_KEY, np.uint64)
+        oracle.zbuffer_accumulate(kb, pc.positions[lo:hi], lo, cam.orientation, cam.position,
+                                  i.focal_px, i.cx, i.cy, i.near, i.far, i.width, i.height)
+        t = torch.from_numpy(parallel.to_signed(kb).copy())
+        parallel.composite_keys(t)
+        comp = parallel.from_signed(t.numpy())
+        # owner-only resolve of the composited frame, emulated with the oracle
+        sel = StreamSelection(rgb=True, depth=True, vel2d=True, vel3d=True, velocity_scale=1.5)
+        full = oracle.resolve(comp, pc, cam, sel)
+        owned = (full["index_plane"] >= lo) & (full["index_plane"] < hi)
+        planes = np.where(owned[..., None], full["data"], np.float32(0.0)).astype(np.float32)
+        pt = torch.from_numpy(np.ascontiguousarray(planes))
+        parallel.reduce_planes(pt, dst=0)
+        if rank == 0:
+            q.put((comp, pt.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_composite_equals_single_process():
+    pc, cam = _scene()
+    from paper_2407_19097_b200.msr import StreamSelection
+
+    sel = StreamSelection(rgb=True, depth=True, vel2d=True, vel3d=True, velocity_scale=1.5)
+    ref = oracle.rasterize(pc, cam, sel)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    comp, planes = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert np.array_equal(comp, ref["keybuf"])
+    # bit-exact including the sign of zero (int32 SUM of bit patterns)
+    assert np.array_equal(planes.view(np.int32), ref["data"].view(np.int32))
+
+
+def test_shard_ranges_cover_and_match_reference_chunking():
+    from paper_2407_19097_b200 import parallel
+
+    for n in (0, 1, 7, 1000, 350_000_000):
+        for w in (1, 2, 3, 4, 8):
+            rs = [parallel.shard_range(n, r, w) for r in range(w)]
+            assert rs[0][0] == 0 and rs[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+            ref = np.linspace(0, n, w + 1).astype(np.int64)
+            assert [r[0] for r in rs] == list(ref[:-1])
+
+
+def test_signed_domain_preserves_order():
+    from paper_2407_19097_b200 import parallel
+
+    rng = np.random.default_rng(0)
+    k = rng.integers(0, 2 ** 63, 10_000, dtype=np.uint64) * np.uint64(2) + rng.integers(0, 2, 10_000, dtype=np.uint64)
+    k = np.concatenate([k, [np.uint64(0), np.uint64(2 ** 64 - 1), np.uint64(2 ** 63)]])
+    s = parallel.to_signed(k)
+    assert np.array_equal(np.argsort(k, kind="stable"), np.argsort(s, kind="stable"))
+    assert np.array_equal(parallel.from_signed(s), k)
+    assert s[-2] == parallel.EMPTY_SIGNED
