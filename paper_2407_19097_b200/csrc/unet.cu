@@ -45,66 +45,93 @@ struct PyrOut {
   __nv_bfloat16* lvl[8];
 };
 
-__global__ void head_pyramid_kernel(const float* __restrict__ x, int H, int W, int cin, int cp,
-                                    const float* __restrict__ hw, const float* __restrict__ hb,
-                                    int use_head, int levels, PyrOut out) {
-  extern __shared__ float tile[];  // (T*T + T*T/4 + ...) x cin floats
+__global__ void __launch_bounds__(256)
+    head_pyramid_kernel(const float* __restrict__ x, int H, int W, int cin, int cp,
+                        const float* __restrict__ hw, const float* __restrict__ hb, int use_head,
+                        int levels, PyrOut out) {
+  extern __shared__ float tile[];  // level k-1 values of this CTA, (T*T) x cin floats, reused
   const int T = 1 << (levels - 1);
   const int tx = blockIdx.x, ty = blockIdx.y;
   const int t = threadIdx.x;
+  // level 0: one thread per pixel of the T x T tile (blockDim = T*T <= 256)
   const int ly = t / T, lx = t % T;
   const int y = ty * T + ly, xx = tx * T + lx;
-  // level 0
-  float v[16];
+  float v[16], hv[16];
   const float* px = x + ((size_t)y * W + xx) * cin;
-  for (int c = 0; c < cin; ++c) v[c] = px[c];
-  float* cur = tile;
-  __nv_bfloat16* o0 = out.lvl[0] + ((size_t)y * W + xx) * cp;
-  for (int j = 0; j < cp; j += 2) {
-    float r0 = 0.f, r1 = 0.f;
-    for (int h = 0; h < 2; ++h) {
-      const int jj = j + h;
-      float acc = 0.f;
-      if (jj < cin) {
-        if (use_head) {
-          acc = hb[jj];
-          for (int c = 0; c < cin; ++c) acc = fmaf(v[c], hw[c * cin + jj], acc);
-        } else {
-          acc = v[jj];
-        }
-        cur[t * cin + jj] = acc;
+#pragma unroll
+  for (int c = 0; c < 16; ++c) v[c] = c < cin ? px[c] : 0.f;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    float acc = 0.f;
+    if (j < cin) {
+      if (use_head) {
+        acc = hb[j];
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+          if (c < cin) acc = fmaf(v[c], hw[c * cin + j], acc);
+      } else {
+        acc = v[j];
       }
-      (h == 0 ? r0 : r1) = acc;
+      tile[t * cin + j] = acc;
     }
-    *reinterpret_cast<__nv_bfloat162*>(o0 + j) = __floats2bfloat162_rn(r0, r1);
+    hv[j] = acc;
+  }
+  // bf16 level 0, padded to cp channels, 16-byte stores
+  __nv_bfloat16* o0 = out.lvl[0] + ((size_t)y * W + xx) * cp;
+#pragma unroll
+  for (int c8 = 0; c8 < 16; c8 += 8) {
+    if (c8 >= cp) break;
+    uint4 pk;
+    uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+    for (int e = 0; e < 8; e += 2) {
+      const float a0 = (c8 + e < 16) ? hv[(c8 + e) & 15] : 0.f;
+      const float a1 = (c8 + e + 1 < 16) ? hv[(c8 + e + 1) & 15] : 0.f;
+      __nv_bfloat162 h2 = __floats2bfloat162_rn(a0, a1);
+      pw[e / 2] = *reinterpret_cast<uint32_t*>(&h2);
+    }
+    *reinterpret_cast<uint4*>(o0 + c8) = pk;
   }
   __syncthreads();
-  // levels 1..L-1
+  // levels 1..L-1: 2x2 averages in f32, in place in shared memory
   int side = T;
   for (int k = 1; k < levels; ++k) {
     const int ns = side >> 1;
-    float* nxt = cur + side * side * cin;
-    if (t < ns * ns) {
-      const int qy = t / ns, qx = t % ns;
+    float m[16];
+    const bool act = t < ns * ns;
+    const int qy = act ? t / ns : 0, qx = act ? t % ns : 0;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) m[c] = 0.f;
+    if (act) {
+      const float* a0 = tile + ((2 * qy) * side + 2 * qx) * cin;
+#pragma unroll
+      for (int c = 0; c < 16; ++c)
+        if (c < cin)
+          m[c] = ((a0[c] + a0[cin + c]) + (a0[side * cin + c] + a0[side * cin + cin + c])) * 0.25f;
+    }
+    __syncthreads();
+    if (act) {
+#pragma unroll
+      for (int c = 0; c < 16; ++c)
+        if (c < cin) tile[t * cin + c] = m[c];
       const int Wk = W >> k;
       __nv_bfloat16* ok = out.lvl[k] + ((size_t)(ty * ns + qy) * Wk + (tx * ns + qx)) * cp;
-      for (int c = 0; c < cp; c += 2) {
-        float r[2];
-        for (int h = 0; h < 2; ++h) {
-          const int cc = c + h;
-          float m = 0.f;
-          if (cc < cin) {
-            const float* a0 = cur + ((2 * qy) * side + 2 * qx) * cin + cc;
-            m = ((a0[0] + a0[cin]) + (a0[side * cin] + a0[side * cin + cin])) * 0.25f;
-            nxt[(qy * ns + qx) * cin + cc] = m;
-          }
-          r[h] = m;
+#pragma unroll
+      for (int c8 = 0; c8 < 16; c8 += 8) {
+        if (c8 >= cp) break;
+        uint4 pk;
+        uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+        for (int e = 0; e < 8; e += 2) {
+          const int c = c8 + e;
+          __nv_bfloat162 h2 = __floats2bfloat162_rn(c < cin ? m[c & 15] : 0.f,
+                                                    c + 1 < cin ? m[(c + 1) & 15] : 0.f);
+          pw[e / 2] = *reinterpret_cast<uint32_t*>(&h2);
         }
-        *reinterpret_cast<__nv_bfloat162*>(ok + c) = __floats2bfloat162_rn(r[0], r[1]);
+        *reinterpret_cast<uint4*>(ok + c8) = pk;
       }
     }
     __syncthreads();
-    cur = nxt;
     side = ns;
   }
 }
@@ -550,8 +577,7 @@ int nar_unet_forward(nar_unet* n, const float* in, int32_t H, int32_t W, float* 
     const int T = 1 << (L - 1);
     PyrOut po;
     for (int k = 0; k < L; ++k) po.lvl[k] = bf(p.off_pyr16[k]);
-    size_t sm = 0;
-    for (int k = 0, side = T; k < L; ++k, side >>= 1) sm += (size_t)side * side * cin * 4;
+    const size_t sm = (size_t)T * T * cin * 4;
     head_pyramid_kernel<<<dim3(W / T, H / T), T * T, sm, st>>>(
         in, H, W, cin, p.cinp, n->d_head_w, n->d_head_b, n->cfg.use_descriptor_head, L, po);
     if ((rc = check_launch("head_pyramid"))) return rc;

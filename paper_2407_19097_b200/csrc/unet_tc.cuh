@@ -61,8 +61,11 @@ struct ConvArgs {
   int head_n;
 };
 
-constexpr int kTcThreads = 416;  // 4 producer + 8 epilogue + 1 MMA warps
-constexpr int kMmaWarp = 12;
+constexpr int kProdWarps = 2;   // TMA issue + staging reshape
+constexpr int kProdThreads = kProdWarps * 32;
+constexpr int kEpiGroups = 4;   // epilogue warps per TMEM lane quarter
+constexpr int kMmaWarp = kProdWarps + 4 * kEpiGroups;
+constexpr int kTcThreads = (kMmaWarp + 1) * 32;  // 2 producer + 16 epilogue + 1 MMA warps
 constexpr int kHaloPx = 130;
 constexpr int kHaloRowBytes = kHaloPx * 16;  // one 8-channel slab row
 constexpr int kLowPx = 66;                   // low-res pixels behind a 130-px halo
@@ -83,7 +86,7 @@ __host__ __device__ constexpr int tc_stages(int N) {
              ? 4
              : (200 * 1024 - 2 * tc_stg_bytes(N)) / tc_stage_bytes(N);
 }
-constexpr int kTcParamFloats = 144 + 144 + 128 * 4 + 4;  // bias_f, bias_g, head_w, head_b
+constexpr int kTcParamFloats = 3 * 144 + 128 * 4 + 4;  // bias_f, bias_f*log2e, bias_g/2, head_w, head_b
 __host__ __device__ constexpr int tc_smem(int N) {
   return tc_stages(N) * tc_stage_bytes(N) + 2 * tc_stg_bytes(N) + 512 + kTcParamFloats * 4;
 }
@@ -214,17 +217,28 @@ __device__ __forceinline__ float tanh_approx(float x) {
   return y;
 }
 
-__device__ __forceinline__ float gate(float f, float g) {
-  const float e = f > 0.0f ? f : __expf(f) - 1.0f;        // elu (autodiff.py:186-194)
-  const float s = fmaf(0.5f, tanh_approx(0.5f * g), 0.5f); // sigmoid (autodiff.py:197-203)
-  return e * s;
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// elu(f + bf) * sigmoid(g + bg) on raw accumulators, with bfl = bf*log2(e) and
+// bgh = bg/2 precomputed: elu via ex2 (autodiff.py:186-194), sigmoid via
+// tanh (autodiff.py:197-203) -- 2 MUFU + 7 FMA-pipe ops per output.
+__device__ __forceinline__ float gate_b(float f, float g, float bf, float bfl, float bgh) {
+  const float fb = f + bf;
+  const float ex = ex2_approx(fmaf(f, 1.44269504088896341f, bfl));
+  const float e = fb > 0.0f ? fb : ex - 1.0f;
+  const float sg = fmaf(0.5f, tanh_approx(fmaf(0.5f, g, bgh)), 0.5f);
+  return e * sg;
 }
 
 // ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
 template <int N>
-__global__ void __launch_bounds__(kTcThreads, 1)
+__global__ void __maxnreg__(96)
     gated_conv_tc(const ConvArgs a, const __grid_constant__ CUtensorMap tma_a,
                   const __grid_constant__ CUtensorMap tma_b) {
   constexpr int R = tc_rows(N);
@@ -252,8 +266,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tbase_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   float* sbias_f = reinterpret_cast<float*>(stg_buf + 2 * STG_BYTES + 512);
-  float* sbias_g = sbias_f + 144;
-  float* shead_w = sbias_g + 144;
+  float* sbias_fl = sbias_f + 144;
+  float* sbias_gh = sbias_fl + 144;
+  float* shead_w = sbias_gh + 144;
   float* shead_b = shead_w + 512;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -270,15 +285,19 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 8);
+      mbar_init(&tempty[b], 4 * kEpiGroups);
     }
     fence_mbar_init();
     prefetch_tmap(&tma_a);
     if (nqb) prefetch_tmap(&tma_b);
   }
   for (int i = threadIdx.x; i < 144; i += kTcThreads) {
-    sbias_f[i] = i < a.cout ? a.bias_f[i] : 0.0f;
-    sbias_g[i] = i < a.cout ? a.bias_g[i] : 0.0f;
+    // zero beyond cout: padded accumulators are 0, so gate(0, 0 | 0) = elu(0) * 0.5 = 0
+    const float bf = i < a.cout ? a.bias_f[i] : 0.0f;
+    const float bg = i < a.cout ? a.bias_g[i] : 0.0f;
+    sbias_f[i] = bf;
+    sbias_fl[i] = bf * 1.44269504088896341f;
+    sbias_gh[i] = 0.5f * bg;
   }
   if (a.head_out)
     for (int i = threadIdx.x; i < a.cout * a.head_n; i += kTcThreads) shead_w[i] = a.head_w[i];
@@ -294,7 +313,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   tc_fence_after();
   const uint32_t tbase = *tbase_slot;
 
-  if (warp < 4) {
+  if (warp < kProdWarps) {
     // ------------------------------ producer ------------------------------
     // Stage `it` = (tile, chunk q).  Lane 0 of warp 0 TMA-loads the chunk's
     // halo box (whole 16-channel pixels, 32 B wide) into staging buffer it&1
@@ -336,28 +355,33 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
       mbar_wait(&empty[s], ph ^ 1u);
       mbar_wait(&stg[it & 1], (uint32_t)(it >> 1) & 1u);
-      constexpr int ITEMS = 2 * (R + 2) * kHaloPx;
       if (up2) {
+        // 2x2 replication: halo (row, j) <- low-res (ly, lx)
         const int ly0 = (y0 - 1) >> 1, lx0 = (x0 - 1) >> 1;
-        for (int i = t; i < ITEMS; i += 128) {
-          const int k8 = i & 1;
-          const int j = (i >> 1) % kHaloPx;
-          const int row = (i >> 1) / kHaloPx;
+#pragma unroll 1
+        for (int row = 0; row < R + 2; ++row) {
           const int ly = ((y0 - 1 + row) >> 1) - ly0;
-          const int lx = ((x0 - 1 + j) >> 1) - lx0;
-          const uint4 v = *reinterpret_cast<const uint4*>(buf + (ly * kLowPx + lx) * 32 + k8 * 16);
-          *reinterpret_cast<uint4*>(stA + k8 * SLAB + row * kHaloRowBytes + j * 16) = v;
+          const uint8_t* srow = buf + ly * (kLowPx * 32);
+          uint8_t* d0 = stA + row * kHaloRowBytes;
+          for (int j = t; j < kHaloPx; j += kProdThreads) {
+            const int lx = ((x0 - 1 + j) >> 1) - lx0;
+            const uint4 v0 = *reinterpret_cast<const uint4*>(srow + lx * 32);
+            const uint4 v1 = *reinterpret_cast<const uint4*>(srow + lx * 32 + 16);
+            *reinterpret_cast<uint4*>(d0 + j * 16) = v0;
+            *reinterpret_cast<uint4*>(d0 + SLAB + j * 16) = v1;
+          }
         }
       } else {
-        for (int i = t; i < ITEMS; i += 128) {
-          const int k8 = i & 1;
-          const int rj = i >> 1;  // row * 130 + j
-          const uint4 v = *reinterpret_cast<const uint4*>(buf + rj * 32 + k8 * 16);
-          *reinterpret_cast<uint4*>(stA + k8 * SLAB + rj * 16) = v;
+        // [row][px][32 B] -> two [row][px][16 B] slabs
+        for (int rj = t; rj < (R + 2) * kHaloPx; rj += kProdThreads) {
+          const uint4 v0 = *reinterpret_cast<const uint4*>(buf + rj * 32);
+          const uint4 v1 = *reinterpret_cast<const uint4*>(buf + rj * 32 + 16);
+          *reinterpret_cast<uint4*>(stA + rj * 16) = v0;
+          *reinterpret_cast<uint4*>(stA + SLAB + rj * 16) = v1;
         }
       }
       fence_proxy_async_smem();
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(kProdThreads) : "memory");
       if (t == 0) mbar_arrive(&full[s]);
     }
   } else if (warp == kMmaWarp) {
@@ -394,18 +418,18 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
   } else {
     // ------------------------------ epilogue -------------------------------
-    // 8 warps: warp w covers TMEM lanes 32*(w%4)..+31 (pixels) and the row
-    // groups g with g % 2 == (w-4)/4 (a group is one row, or two for pooling).
-    // Channels are processed 16 at a time (one x16 TMEM load per branch and
-    // row, one wait), biases held in registers across the rows.
+    // 16 warps: warp w covers TMEM lanes 32*(w%4)..+31 (pixels) and the row
+    // groups g with g % 4 == (w-4)/4 (a group is one row, or two for pooling).
+    // Channels are processed 8 at a time: one x8 TMEM load per branch and row,
+    // one wait; padded channels come out as exact zeros.
     const int quarter = warp & 3;
-    const int half = (warp - 4) >> 2;
+    const int grp = (warp - kProdWarps) >> 2;
     const int m = quarter * 32 + lane;
     const bool do_pool = a.pool_out != nullptr;  // requires R even (host-checked)
     const bool do_head = a.head_out != nullptr;
     const int rstep = do_pool ? 2 : 1;
-    constexpr int RPW = R > 1 ? R / 2 : 1;  // rows per warp, upper bound
-    const int nch = (a.cout_stride + 15) / 16;
+    constexpr int RPW = R >= kEpiGroups ? R / kEpiGroups : 1;  // rows per warp, upper bound
+    const int nc8 = a.cout_stride / 8;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     int tl = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tl) {
@@ -423,57 +447,54 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           for (int k = 0; k < 4; ++k) logit[i][k] = 0.0f;
       }
 #pragma unroll 1
-      for (int ch = 0; ch < nch; ++ch) {
-        const int c0 = ch * 16;
-        const bool two = c0 + 8 < COUTP;  // second 8-channel group has accumulators
-        float bfv[16], bgv[16];
+      for (int c8 = 0; c8 < nc8; ++c8) {
+        const int c0 = c8 * 8;
+        const bool have = c0 < COUTP;
+        float bfv[8], bflv[8], bghv[8];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
+        for (int e = 0; e < 8; ++e) {
           bfv[e] = sbias_f[c0 + e];
-          bgv[e] = sbias_g[c0 + e];
+          bflv[e] = sbias_fl[c0 + e];
+          bghv[e] = sbias_gh[c0 + e];
         }
         int slot = 0;
 #pragma unroll 1
-        for (int r = half * rstep; r < R; r += 2 * rstep, slot += rstep) {
-          float o[2][16];
+        for (int r = grp * rstep; r < R; r += kEpiGroups * rstep, slot += rstep) {
+          float o[2][8];
+          float f[2][8], g[2][8];
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             if (h == 1 && !do_pool) break;
-            float f[16], g[16];
-            const uint32_t col = tbase + (uint32_t)(b * R * N + (r + h) * N + c0) + lane_off;
-            if (two) {
-              tmem_ld16(col, f);
-              tmem_ld16(col + COUTP, g);
+            if (have) {
+              const uint32_t col = tbase + (uint32_t)(b * R * N + (r + h) * N + c0) + lane_off;
+              tmem_ld8(col, f[h]);
+              tmem_ld8(col + COUTP, g[h]);
             } else {
-              tmem_ld8(col, f);
-              tmem_ld8(col + COUTP, g);
 #pragma unroll
-              for (int e = 8; e < 16; ++e) f[e] = g[e] = 0.0f;
+              for (int e = 0; e < 8; ++e) f[h][e] = g[h][e] = 0.0f;
             }
-            tmem_wait_ld();
+          }
+          if (have) tmem_wait_ld();
 #pragma unroll
-            for (int e = 0; e < 16; ++e)
-              o[h][e] = (c0 + e < a.cout) ? gate(f[e] + bfv[e], g[e] + bgv[e]) : 0.0f;
+          for (int h = 0; h < 2; ++h) {
+            if (h == 1 && !do_pool) break;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) o[h][e] = gate_b(f[h][e], g[h][e], bfv[e], bflv[e], bghv[e]);
             const int y = y0 + r + h;
             const bool ok = y < a.H && xok;
             if (a.out != nullptr && ok) {
-              __nv_bfloat16* dst = a.out + ((size_t)y * a.W + x) * a.cout_stride + c0;
+              uint4 pk;
+              uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
 #pragma unroll
-              for (int g8 = 0; g8 < 2; ++g8) {
-                if (g8 == 1 && c0 + 8 >= a.cout_stride) break;
-                uint4 pk;
-                uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
-#pragma unroll
-                for (int e = 0; e < 8; e += 2) {
-                  __nv_bfloat162 hh = __floats2bfloat162_rn(o[h][g8 * 8 + e], o[h][g8 * 8 + e + 1]);
-                  pw[e / 2] = *reinterpret_cast<uint32_t*>(&hh);
-                }
-                *reinterpret_cast<uint4*>(dst + g8 * 8) = pk;
+              for (int e = 0; e < 8; e += 2) {
+                __nv_bfloat162 hh = __floats2bfloat162_rn(o[h][e], o[h][e + 1]);
+                pw[e / 2] = *reinterpret_cast<uint32_t*>(&hh);
               }
+              *reinterpret_cast<uint4*>(a.out + ((size_t)y * a.W + x) * a.cout_stride + c0) = pk;
             }
             if (do_head) {
 #pragma unroll
-              for (int e = 0; e < 16; ++e)
+              for (int e = 0; e < 8; ++e)
                 if (c0 + e < a.cout)
 #pragma unroll
                   for (int k = 0; k < 4; ++k)
@@ -484,29 +505,24 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           }
           if (do_pool) {
             // 2x2 average of the f32 outputs: rows r, r+1 here, columns m, m+1 via shuffle
-            float v[16];
+            float v[8];
 #pragma unroll
-            for (int e = 0; e < 16; ++e) {
+            for (int e = 0; e < 8; ++e) {
               v[e] = o[0][e] + o[1][e];
               v[e] += __shfl_xor_sync(0xffffffffu, v[e], 1);
             }
             const int y = y0 + r;
             if ((m & 1) == 0 && y < a.H && xok) {
-              __nv_bfloat16* dst = a.pool_out +
-                                   ((size_t)(y >> 1) * (a.W >> 1) + (x >> 1)) * a.cout_stride + c0;
+              uint4 pk;
+              uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
 #pragma unroll
-              for (int g8 = 0; g8 < 2; ++g8) {
-                if (g8 == 1 && c0 + 8 >= a.cout_stride) break;
-                uint4 pk;
-                uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
-#pragma unroll
-                for (int e = 0; e < 8; e += 2) {
-                  __nv_bfloat162 hh = __floats2bfloat162_rn(0.25f * v[g8 * 8 + e],
-                                                            0.25f * v[g8 * 8 + e + 1]);
-                  pw[e / 2] = *reinterpret_cast<uint32_t*>(&hh);
-                }
-                *reinterpret_cast<uint4*>(dst + g8 * 8) = pk;
+              for (int e = 0; e < 8; e += 2) {
+                __nv_bfloat162 hh = __floats2bfloat162_rn(0.25f * v[e], 0.25f * v[e + 1]);
+                pw[e / 2] = *reinterpret_cast<uint32_t*>(&hh);
               }
+              *reinterpret_cast<uint4*>(a.pool_out +
+                                        ((size_t)(y >> 1) * (a.W >> 1) + (x >> 1)) * a.cout_stride +
+                                        c0) = pk;
             }
           }
         }
@@ -514,7 +530,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       if (do_head) {
         int slot = 0;
 #pragma unroll 1
-        for (int r = half * rstep; r < R; r += 2 * rstep, slot += rstep) {
+        for (int r = grp * rstep; r < R; r += kEpiGroups * rstep, slot += rstep) {
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             if (h == 1 && !do_pool) break;

@@ -425,7 +425,9 @@ def rasterize(pc: PointCloud, cam: CameraPose, sel: StreamSelection, threads: in
     names = sel.needed_streams()
     # Attribute streams go up on a side stream while the points stream through
     # nar_render_host's chunk pipeline on the main stream.
-    side = torch.cuda.Stream(dev)
+    if getattr(r, "_side", None) is None:
+        r._side = torch.cuda.Stream(dev)
+    side = r._side
     side.wait_stream(main)
     with torch.cuda.stream(side):
         segs_streams = {n: torch.from_numpy(pc.stream(n).data).to(dev, non_blocking=True)
@@ -444,11 +446,15 @@ def rasterize(pc: PointCloud, cam: CameraPose, sel: StreamSelection, threads: in
     cloud = DeviceCloud([{"begin": 0, "count": pc.count, "positions": pos_dev,
                           "streams": segs_streams}], meta, dev)
     res = r.resolve(cloud, cam, sel, stream=main)
-    host = {}
+    # D2H into pinned staging buffers cached on the renderer (reused per call)
+    cache = getattr(r, "_host_out", None)
+    if cache is None or cache["data"].shape != res.data.shape:
+        cache = r._host_out = {k: torch.empty(getattr(res, k).shape, dtype=getattr(res, k).dtype,
+                                              pin_memory=True)
+                               for k in ("data", "coverage", "index_plane", "depth")}
+    host = cache
     for k in ("data", "coverage", "index_plane", "depth"):
-        t = getattr(res, k)
-        host[k] = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
-        host[k].copy_(t, non_blocking=True)
+        host[k].copy_(getattr(res, k), non_blocking=True)
     main.synchronize()  # also keeps the uploaded tensors alive until consumed
     names_out = sel.channel_names(pc)
     return FeatureImage(W, H, names_out, host["data"].numpy()[:H, :W].copy(),
