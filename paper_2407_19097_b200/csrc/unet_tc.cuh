@@ -79,7 +79,7 @@ __host__ __device__ constexpr int tc_a_bytes(int N) { return 2 * tc_slab(N); }
 __host__ __device__ constexpr int tc_b_bytes(int N) { return 9 * N * 32; }
 // staging: one TMA box of whole 16-channel chunks (32 B per pixel), either the
 // (R+2) x 130 halo or, for up2 sources, the low-res (LR x 66) halo
-__host__ __device__ constexpr int tc_stg_bytes(int N) { return tc_r128((tc_rows(N) + 2) * kHaloPx * 32); }
+__host__ __device__ constexpr int tc_stg_bytes(int N) { return tc_r128(tc_low_rows(N) * kLowPx * 32); }
 __host__ __device__ constexpr int tc_stage_bytes(int N) { return tc_a_bytes(N) + tc_b_bytes(N); }
 __host__ __device__ constexpr int tc_stages(int N) {
   return (200 * 1024 - 2 * tc_stg_bytes(N)) / tc_stage_bytes(N) > 4
@@ -250,8 +250,8 @@ __global__ void __maxnreg__(96)
   constexpr int STAGE = tc_stage_bytes(N);
   constexpr int SLAB = tc_slab(N);
   static_assert(A_BYTES % 128 == 0 && B_BYTES % 128 == 0 && STG_BYTES % 128 == 0, "align");
-  constexpr uint32_t STG_TX = (R + 2) * kHaloPx * 32;  // bytes of a direct halo box
-  constexpr uint32_t LOW_TX = LR * kLowPx * 32;        // bytes of an up2 low-res box
+  constexpr uint32_t A_TX = 2u * (R + 2) * kHaloPx * 16;  // bytes of the two direct slab boxes
+  constexpr uint32_t LOW_TX = LR * kLowPx * 32;          // bytes of an up2 low-res box
   constexpr int COUTP = N / 2;
   constexpr uint32_t IDESC = umma_idesc_bf16(128, N);
   static_assert(2 * R * N <= 512, "TMEM budget");
@@ -315,29 +315,33 @@ __global__ void __maxnreg__(96)
 
   if (warp < kProdWarps) {
     // ------------------------------ producer ------------------------------
-    // Stage `it` = (tile, chunk q).  Lane 0 of warp 0 TMA-loads the chunk's
-    // halo box (whole 16-channel pixels, 32 B wide) into staging buffer it&1
-    // one stage ahead, and streams the weights; the 128 producer threads then
-    // reshape staging -> the UMMA layout [k8][row][px][16 B] (replicating
-    // 2x2 for up2 sources) and release the stage to the MMA warp.
+    // Stage `it` = (tile, chunk q).  Direct chunks: lane 0 of warp 0 TMA-loads
+    // the two 8-channel slabs of the (R+2) x 130 halo straight into the UMMA
+    // layout [k8][row][px][16 B] and streams the weights.  up2 chunks: the
+    // low-res halo (whole 16-channel pixels) is TMA-loaded into a double-
+    // buffered staging area one up2 stage ahead, and the producer threads
+    // replicate it 2x2 into the halo layout.
     const int t = threadIdx.x;
     const int my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     const int n_it = my_tiles * nq;
-    auto issue_staging = [&](int it) {
-      const int tile = blockIdx.x + (it / nq) * gridDim.x, q = it % nq;
-      const int y0 = (tile / tiles_x) * R, x0 = (tile % tiles_x) * 128;
-      const bool in_a = q < nqa;
-      const int cbase = 16 * (in_a ? q : q - nqa);
-      uint8_t* buf = stg_buf + (it & 1) * STG_BYTES;
-      if (in_a && a.a_up2) {
-        mbar_expect_tx(&stg[it & 1], LOW_TX);
-        tma_load_3d(buf, &tma_a, cbase, (x0 - 1) >> 1, (y0 - 1) >> 1, &stg[it & 1]);
-      } else {
-        mbar_expect_tx(&stg[it & 1], STG_TX);
-        tma_load_3d(buf, in_a ? &tma_a : &tma_b, cbase, x0 - 1, y0 - 1, &stg[it & 1]);
-      }
+    auto is_up2 = [&](int j) { return a.a_up2 && (j % nq) < nqa; };
+    auto next_up2 = [&](int j) {
+      for (++j; j < n_it; ++j)
+        if (is_up2(j)) return j;
+      return n_it;
     };
-    if (t == 0 && n_it > 0) issue_staging(0);
+    auto issue_staging = [&](int j, int bsel) {
+      const int tile = blockIdx.x + (j / nq) * gridDim.x, q = j % nq;
+      const int y0 = (tile / tiles_x) * R, x0 = (tile % tiles_x) * 128;
+      mbar_expect_tx(&stg[bsel], LOW_TX);
+      tma_load_3d(stg_buf + bsel * STG_BYTES, &tma_a, 16 * q, (x0 - 1) >> 1, (y0 - 1) >> 1,
+                  &stg[bsel]);
+    };
+    int u = 0;  // up2 stages seen so far: staging buffer u & 1, parity (u >> 1) & 1
+    if (t == 0) {
+      const int j0 = next_up2(-1);
+      if (j0 < n_it) issue_staging(j0, 0);
+    }
     for (int it = 0; it < n_it; ++it) {
       const int tile = blockIdx.x + (it / nq) * gridDim.x, q = it % nq;
       const int y0 = (tile / tiles_x) * R, x0 = (tile % tiles_x) * 128;
@@ -345,17 +349,35 @@ __global__ void __maxnreg__(96)
       const uint32_t ph = (uint32_t)(it / S) & 1u;
       uint8_t* stA = smem + s * STAGE;
       uint8_t* stB = stA + A_BYTES;
-      const uint8_t* buf = stg_buf + (it & 1) * STG_BYTES;
-      const bool up2 = q < nqa && a.a_up2;
+      if (!is_up2(it)) {
+        // Every producer thread observes every phase of empty[s]: parity waits
+        // are only valid one phase ahead, so skipping a stage here would let a
+        // later wait succeed on a stale phase.
+        if (t != 0) mbar_wait(&empty[s], ph ^ 1u);
+        if (t == 0) {
+          const bool in_a = q < nqa;
+          const int cbase = 16 * (in_a ? q : q - nqa);
+          const CUtensorMap* map = in_a ? &tma_a : &tma_b;
+          mbar_wait(&empty[s], ph ^ 1u);
+          mbar_expect_tx(&full[s], A_TX + B_BYTES);
+          tma_load_3d(stA, map, cbase, x0 - 1, y0 - 1, &full[s]);
+          tma_load_3d(stA + SLAB, map, cbase + 8, x0 - 1, y0 - 1, &full[s]);
+          bulk_g2s(stB, a.wtc + (size_t)q * (B_BYTES / 2), B_BYTES, &full[s]);
+          mbar_arrive(&full[s]);
+        }
+        continue;
+      }
+      const uint8_t* buf = stg_buf + (u & 1) * STG_BYTES;
       if (t == 0) {
-        if (it + 1 < n_it) issue_staging(it + 1);  // overlaps this stage's reshape
+        const int j2 = next_up2(it);
+        if (j2 < n_it) issue_staging(j2, (u + 1) & 1);  // overlaps this stage's replication
         mbar_wait(&empty[s], ph ^ 1u);
         mbar_expect_tx(&full[s], B_BYTES);
         bulk_g2s(stB, a.wtc + (size_t)q * (B_BYTES / 2), B_BYTES, &full[s]);
       }
       mbar_wait(&empty[s], ph ^ 1u);
-      mbar_wait(&stg[it & 1], (uint32_t)(it >> 1) & 1u);
-      if (up2) {
+      mbar_wait(&stg[u & 1], (uint32_t)(u >> 1) & 1u);
+      {
         // 2x2 replication: halo (row, j) <- low-res (ly, lx)
         const int ly0 = (y0 - 1) >> 1, lx0 = (x0 - 1) >> 1;
 #pragma unroll 1
@@ -371,15 +393,8 @@ __global__ void __maxnreg__(96)
             *reinterpret_cast<uint4*>(d0 + SLAB + j * 16) = v1;
           }
         }
-      } else {
-        // [row][px][32 B] -> two [row][px][16 B] slabs
-        for (int rj = t; rj < (R + 2) * kHaloPx; rj += kProdThreads) {
-          const uint4 v0 = *reinterpret_cast<const uint4*>(buf + rj * 32);
-          const uint4 v1 = *reinterpret_cast<const uint4*>(buf + rj * 32 + 16);
-          *reinterpret_cast<uint4*>(stA + rj * 16) = v0;
-          *reinterpret_cast<uint4*>(stA + SLAB + rj * 16) = v1;
-        }
       }
+      ++u;
       fence_proxy_async_smem();
       asm volatile("bar.sync 1, %0;" ::"n"(kProdThreads) : "memory");
       if (t == 0) mbar_arrive(&full[s]);
@@ -575,13 +590,14 @@ static PFN_cuTensorMapEncodeTiled_v12000 tc_encode_fn() {
   return fn;
 }
 
-// NHWC bf16 tensor (h, w, cs) -> 3-D map over (channel, x, y), box {16, bw, bh}.
-static int tc_make_map(CUtensorMap* m, const void* base, int cs, int w, int h, int bw, int bh) {
+// NHWC bf16 tensor (h, w, cs) -> 3-D map over (channel, x, y), box {bc, bw, bh}.
+static int tc_make_map(CUtensorMap* m, const void* base, int cs, int w, int h, int bc, int bw,
+                       int bh) {
   auto fn = tc_encode_fn();
   if (!fn) return set_error(NAR_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[3] = {(cuuint64_t)cs, (cuuint64_t)w, (cuuint64_t)h};
   cuuint64_t strides[2] = {(cuuint64_t)cs * 2, (cuuint64_t)cs * 2 * (cuuint64_t)w};
-  cuuint32_t box[3] = {16, (cuuint32_t)bw, (cuuint32_t)bh};
+  cuuint32_t box[3] = {(cuuint32_t)bc, (cuuint32_t)bw, (cuuint32_t)bh};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -609,12 +625,12 @@ static int tc_launch_n(const ConvArgs& a, cudaStream_t st) {
   CUtensorMap ma, mb;
   int rc;
   if (a.a_up2)
-    rc = tc_make_map(&ma, a.src_a, a.ca_stride, a.W / 2, a.H / 2, kLowPx, tc_low_rows(N));
+    rc = tc_make_map(&ma, a.src_a, a.ca_stride, a.W / 2, a.H / 2, 16, kLowPx, tc_low_rows(N));
   else
-    rc = tc_make_map(&ma, a.src_a, a.ca_stride, a.W, a.H, kHaloPx, R + 2);
+    rc = tc_make_map(&ma, a.src_a, a.ca_stride, a.W, a.H, 8, kHaloPx, R + 2);
   if (rc) return rc;
   if (a.cb) {
-    rc = tc_make_map(&mb, a.src_b, a.cb_stride, a.W, a.H, kHaloPx, R + 2);
+    rc = tc_make_map(&mb, a.src_b, a.cb_stride, a.W, a.H, 8, kHaloPx, R + 2);
     if (rc) return rc;
   } else {
     mb = ma;

@@ -77,7 +77,9 @@ def test_tensor_core_matches_simt_at_1080p(cuda):
     params = init_params(cfg)
     g = torch.Generator(device=cuda).manual_seed(0)
     x = torch.rand((1088, 1920, 4), device=cuda, generator=g)
-    tc = UNet(cfg, params, device=cuda)(x)
+    net = UNet(cfg, params, device=cuda)
+    tc = net(x)
+    assert torch.equal(tc, net(x)), "tensor-core forward is not deterministic"
     os.environ["NAR_UNET_SIMT"] = "1"
     try:
         simt = UNet(cfg, params, device=cuda)(x)
