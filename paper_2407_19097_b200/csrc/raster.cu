@@ -116,8 +116,9 @@ __device__ __forceinline__ bool snap_certain(double t, int& i) {
   return ((uint32_t)q & 0xFFFFFFu) - 2u < 0xFFFFFDu;  // fraction in [2, 2^24 - 2] * 2^-24
 }
 
-__device__ __forceinline__ int project_fast(float x, float y, float z, const DevCam& k,
-                                            uint32_t& ix_out, uint32_t& iy_out, uint32_t& dbits) {
+__device__ __forceinline__ void project_fast(float x, float y, float z, const DevCam& k,
+                                             uint32_t& ix_out, uint32_t& iy_out, uint32_t& dbits,
+                                             bool& hit, bool& uncertain) {
   const double w0 = __dsub_rn((double)x, k.c[0]);
   const double w1 = __dsub_rn((double)y, k.c[1]);
   const double w2 = __dsub_rn((double)z, k.c[2]);
@@ -145,8 +146,8 @@ __device__ __forceinline__ int project_fast(float x, float y, float z, const Dev
   const bool inside = (uint32_t)ix < (uint32_t)k.w && (uint32_t)iy < (uint32_t)k.h;
   ix_out = (uint32_t)ix;
   iy_out = (uint32_t)iy;
-  // 0 = culled, 1 = certain hit, 2 = uncertain (in depth range, snap not certified)
-  return (int)in_depth * (certain ? (int)inside : 2);
+  hit = in_depth && certain && inside;  // certain hit
+  uncertain = in_depth && !certain;     // in depth range, snap not certified
 }
 
 template <bool kSigned>
@@ -301,12 +302,12 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
     const int s = k % kWarpStages;
     mbar_wait(&full[s], (uint32_t)(k / kWarpStages) & 1u);
     const float* chunk = ring + s * (kChunkPts * 3);
-    const uint64_t cbase = base_index + (uint64_t)cm.chunk(c) * kChunkPts;
+    const uint32_t cbase = (uint32_t)base_index + (uint32_t)cm.chunk(c) * (uint32_t)kChunkPts;
 
     // (1) projections: straight-line, interleavable across the 4 points
     float px[kPtsPerThread], py[kPtsPerThread], pz[kPtsPerThread];
     uint32_t ixs[kPtsPerThread], iys[kPtsPerThread], dbs[kPtsPerThread];
-    int sts[kPtsPerThread];
+    bool hits[kPtsPerThread], uncs[kPtsPerThread];
 #pragma unroll
     for (int j = 0; j < kPtsPerThread; ++j) {
       const int p = j * 32 + lane;
@@ -315,18 +316,18 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
       pz[j] = chunk[3 * p + 2];
     }
     __syncwarp();
-    if (lane == 0) {  // (3) slot s is consumed: refill it with chunk k + kWarpStages
+    {  // (3) slot s is consumed: refill it with chunk k + kWarpStages
       const int64_t cn = c + (int64_t)kWarpStages * c_stride;
-      if (cn < n_chunks) {
+      if (lane == 0 && cn < n_chunks) {
         fence_proxy_async_smem();
         mbar_expect_tx(&full[s], kChunkBytes);
-        bulk_g2s(ring + s * (kChunkPts * 3), pos + cm.chunk(cn) * (kChunkPts * 3), kChunkBytes,
-                 &full[s]);
+        bulk_g2s(ring + s * (kChunkPts * 3), pos + (size_t)cm.chunk(cn) * (kChunkPts * 3),
+                 kChunkBytes, &full[s]);
       }
     }
 #pragma unroll
     for (int j = 0; j < kPtsPerThread; ++j)
-      sts[j] = project_fast(px[j], py[j], pz[j], cam, ixs[j], iys[j], dbs[j]);
+      project_fast(px[j], py[j], pz[j], cam, ixs[j], iys[j], dbs[j], hits[j], uncs[j]);
 
     // (2) Hi-Z, optional warp pre-dedup of same-pixel hits, uncertain queue
     uint32_t pix[kPtsPerThread], idxs[kPtsPerThread];
@@ -335,29 +336,17 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
 #pragma unroll
     for (int j = 0; j < kPtsPerThread; ++j) {
       const int p = j * 32 + lane;
-      int st = sts[j];
       const uint32_t db = dbs[j];
-      if (use_hiz && st == 1) {
-        const uint32_t zb = (iys[j] >> hz.shift) * (uint32_t)hz.zw + (ixs[j] >> hz.shift);
-        st = (db >> 16) > zs[zb] ? 0 : 1;  // behind every pixel of its coarse block
+      bool hit = hits[j];
+      if (use_hiz) {  // behind every pixel of its coarse block? (index clamped: no branch)
+        const uint32_t zb = hit ? (iys[j] >> hz.shift) * (uint32_t)hz.zw + (ixs[j] >> hz.shift) : 0u;
+        hit = hit && (db >> 16) <= zs[zb];
       }
       pix[j] = iys[j] * (uint32_t)cam.w + ixs[j];
-      const uint32_t idx = (uint32_t)((cbase + (uint64_t)p) & 0xFFFFFFFFull);
+      const uint32_t idx = cbase + (uint32_t)p;
       key[j] = ((uint64_t)db << 32) | idx;
-      if (kDedup) {
-        // lanes hitting the same pixel: only the (depth, index)-minimum survives
-        const uint32_t active = __ballot_sync(0xffffffffu, st == 1);
-        if (st == 1) {
-          const uint32_t grp = __match_any_sync(active, pix[j]);
-          if (grp != (1u << lane)) {
-            const uint32_t dmin = __reduce_min_sync(grp, db);
-            const uint32_t imin = __reduce_min_sync(grp, db == dmin ? idx : 0xFFFFFFFFu);
-            if (db != dmin || idx != imin) st = 0;
-          }
-        }
-      }
-      if (st == 1) okmask |= 1u << j;
-      if (st == 2) umask |= 1u << j;
+      okmask |= (uint32_t)hit << j;
+      umask |= (uint32_t)uncs[j] << j;
       idxs[j] = idx;
     }
     if (__any_sync(0xffffffffu, umask != 0u)) {
