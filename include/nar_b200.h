@@ -108,6 +108,13 @@ int nar_render_host(uint64_t* keybuf_dev, const float* positions_host, int64_t n
                     uint64_t base_index, const nar_camera* cam, int32_t key_domain,
                     void* stream);
 
+/* ---- preprocessing: Morton order (geometry/morton.py:9-46) --------------------------
+ * keys_dev[i] = 63-bit z-order key of positions_dev[i] quantised to 21 bits per
+ * axis over the box [lo, hi] (f64, bit-identical to the reference); a stable
+ * sort by key gives the reference's morton_reorder permutation. */
+int nar_morton_keys(const float* positions_dev, int64_t n, const double* lo, const double* hi,
+                    uint64_t* keys_dev, void* stream);
+
 /* ---- resolve ---------------------------------------------------------------------- */
 /* One contiguous point buffer (a "data stream" of the multi-stream config):
  * global indices [begin, begin+count) live in rows [0, count) of these arrays. */

@@ -15,6 +15,10 @@ Contents (each cites the reference file:line it restates):
   * init_params / forward -- numpy f32 restatement of neural/model.py:65-204 and the
     forward ops of neural/autodiff.py:186-288 (im2col + BLAS conv).
 
+  * morton_keys / morton_order -- numpy restatement of geometry/morton.py:9-46
+    (21-bit f64 quantisation over the cloud AABB, magic-number bit spread,
+    stable argsort).
+
 Pinning: tests/test_oracle.py checks every function here against golden
 vectors produced by the real reference (tests/golden/make_golden.py, committed
 fixtures under tests/golden/), so parity is pinned, not assumed.
@@ -368,3 +372,38 @@ def psnr(a, b):
     if m == 0.0:
         return 100.0
     return min(10.0 * math.log10(1.0 / m), 100.0)
+
+
+# ---- Morton order (geometry/morton.py) ---------------------------------------------
+
+_SPREAD = [(32, 0x1F00000000FFFF), (16, 0x1F0000FF0000FF), (8, 0x100F00F00F00F00F),
+           (4, 0x10C30C30C30C30C3), (2, 0x1249249249249249)]
+
+
+def _spread21(q):
+    """morton.py:12-20: two zero bits between each of the low 21 bits."""
+    x = q.astype(np.uint64) & np.uint64(0x1FFFFF)
+    for sh, mask in _SPREAD:
+        x = (x | (x << np.uint64(sh))) & np.uint64(mask)
+    return x
+
+
+def morton_keys(positions, lo=None, hi=None):
+    """morton.py:23-37: keys over the cloud AABB (pointcloud.py:38-44 min/max)."""
+    p = np.asarray(positions, np.float32)
+    if lo is None:
+        lo, hi = p.min(axis=0).astype(np.float64), p.max(axis=0).astype(np.float64)
+    lo, hi = np.asarray(lo, np.float64), np.asarray(hi, np.float64)
+    ext = np.where(hi > lo, hi - lo, 1.0)
+    with np.errstate(invalid="ignore"):
+        q = np.floor((p.astype(np.float64) - lo) / ext * float(1 << 21)).astype(np.int64)
+    q = np.clip(q, 0, (1 << 21) - 1)
+    return _spread21(q[:, 0]) | (_spread21(q[:, 1]) << np.uint64(1)) | (
+        _spread21(q[:, 2]) << np.uint64(2))
+
+
+def morton_order(positions):
+    """morton.py:40-46: the stable permutation ``morton_reorder`` applies."""
+    if len(positions) == 0:
+        return np.zeros(0, np.int64)
+    return np.argsort(morton_keys(positions), kind="stable")

@@ -116,6 +116,7 @@ SIGNATURES = {
     "nar_render_host": (C.c_int, [_vp, _vp, _i64, _u64, C.POINTER(Camera), _i32, _vp]),
     "nar_hiz_scratch_bytes": (C.c_int, [_i32, _i32, C.POINTER(C.c_size_t)]),
     "nar_render_hiz": (C.c_int, [_vp, _vp, _vp, _i64, _u64, C.POINTER(Camera), _i32, _i32, _vp]),
+    "nar_morton_keys": (C.c_int, [_vp, _i64, _vp, _vp, _vp, _vp]),
     "nar_resolve": (
         C.c_int,
         [_vp, C.POINTER(Camera), _i32, C.POINTER(Selection), C.POINTER(Segment), _i32,

@@ -176,6 +176,80 @@ def main() -> None:
     for k, t in enumerate(pyr):
         net[f"pyramid/{k}"] = t.data
     np.savez_compressed(OUT / "unet.npz", **net)
+    # ---- preprocessing: Morton order, NARPC files, checkpoints ----
+    import io as _io
+    import os as _os
+
+    from nar.geometry import load_pointcloud, morton_keys, morton_reorder, save_pointcloud
+    from nar.neural.checkpoint import (load_checkpoint, quantize_checkpoint, save_checkpoint,
+                                       weight_payload_bytes)
+    from nar.neural.model import ModelState
+
+    pre = {}
+    clouds = {
+        "uniform": rng.uniform(-3, 5, (8000, 3)).astype(np.float32),
+        "flat": np.c_[rng.uniform(0, 1, (5000, 2)), np.full(5000, 0.25)].astype(np.float32),
+        "dups": np.repeat(rng.uniform(-1, 1, (700, 3)).astype(np.float32), 7, axis=0)[
+            rng.permutation(4900)],
+        "single": np.array([[1.5, -2.0, 0.125]], np.float32),
+    }
+    for name, pos in clouds.items():
+        pc = PointCloud(pos, [Stream("rgb", "u8", rng.integers(0, 256, (len(pos), 3),
+                                                                 dtype=np.uint8))])
+        keys = morton_keys(pc)
+        order = np.argsort(keys, kind="stable")
+        ro = morton_reorder(pc)
+        assert np.array_equal(ro.positions, pos[order])
+        pre[f"morton/{name}/positions"] = pos
+        pre[f"morton/{name}/keys"] = keys
+        pre[f"morton/{name}/order"] = order
+    n = 257
+    pc = PointCloud(rng.normal(0, 2, (n, 3)).astype(np.float32),
+                    [Stream("rgb", "u8", rng.integers(0, 256, (n, 3), dtype=np.uint8)),
+                     Stream("velocity", "f32", rng.normal(0, 1, (n, 3)).astype(np.float32)),
+                     Stream("temperature", "f32", rng.normal(0, 1, (n, 1)).astype(np.float32))])
+    tmp = Path(tempfile.mkdtemp())
+    save_pointcloud(pc, tmp / "a.narpc")
+    back = load_pointcloud(tmp / "a.narpc")
+    assert np.array_equal(back.positions, pc.positions)
+    pre["narpc/file"] = np.frombuffer((tmp / "a.narpc").read_bytes(), np.uint8)
+    pre["narpc/positions"] = pc.positions
+    for s_ in pc.streams:
+        pre[f"narpc/stream/{s_.name}"] = s_.data
+    save_pointcloud(PointCloud(np.zeros((0, 3), np.float32)), tmp / "e.narpc")
+    pre["narpc/empty_file"] = np.frombuffer((tmp / "e.narpc").read_bytes(), np.uint8)
+
+    cfg = UNetConfig(input_channels=4, channel_names=("r", "g", "b", "d"), base_channels=4, max_channels=32,
+                     init_seed=5)
+    st = ModelState.initialize(cfg)
+    st.step = 1234
+    st.params["enc0a.f_w"][0, 0, 0, :2] = [70000.0, -1e6]  # saturates in f16
+    for k in ("head.w", "head.b", "out.w", "out.b"):  # the rest stay zero (small file)
+        st.m[k] = rng.normal(0, 1e-3, st.m[k].shape).astype(np.float32)
+        st.v[k] = rng.uniform(0, 1e-6, st.v[k].shape).astype(np.float32)
+    save_checkpoint(st, tmp / "f32.narck")
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        sat = quantize_checkpoint(st, tmp / "f16.narck")
+    pre["ckpt/f32_file"] = np.frombuffer((tmp / "f32.narck").read_bytes(), np.uint8)
+    pre["ckpt/f16_file"] = np.frombuffer((tmp / "f16.narck").read_bytes(), np.uint8)
+    pre["ckpt/saturated"] = np.int64(sat)
+    pre["ckpt/payload_f32"] = np.int64(weight_payload_bytes(tmp / "f32.narck"))
+    pre["ckpt/payload_f16"] = np.int64(weight_payload_bytes(tmp / "f16.narck"))
+    q = load_checkpoint(tmp / "f16.narck", expected_config=cfg)
+    st.params["enc0a.f_w"][0, 0, 0, :2] = 0.0
+    q.params["enc0a.f_w"][0, 0, 0, :2] = 0.0
+    save_checkpoint(ModelState(cfg, q.params, step=7), tmp / "q.narck", precision="f16")
+    pre["ckpt/clean_f16_file"] = np.frombuffer((tmp / "q.narck").read_bytes(), np.uint8)
+    x = rng.uniform(0, 1, (1, 48, 80, 4)).astype(np.float32)
+    x[:, :, :20] = 0.0
+    pre["ckpt/x"] = x
+    pre["ckpt/y_f16"] = forward(Tensor(x), {k: Tensor(v) for k, v in q.params.items()},
+                                cfg).data
+    shutil.rmtree(tmp)
+    np.savez_compressed(OUT / "preprocess.npz", **pre)
+
     for f in sorted(OUT.glob("*.npz")):
         print(f.name, f.stat().st_size)
 
