@@ -106,14 +106,15 @@ __device__ __forceinline__ double rcp_approx_f64(double x) {
   return y;
 }
 
-__device__ __forceinline__ bool snap_certain(double t, int& i) {
-  // q = round(t * 2^24) from the low bits of t + 1.5*2^28 (exact for |t| < 2^27);
-  // floor(t) = q >> 24 unless t is within ~2^-23 of an integer, which the
-  // caller treats as uncertain.
-  const double s = __dadd_rn(t, 402653184.0);
-  const long long q = __double_as_longlong(s) - 0x41B8000000000000LL;
-  i = (int)(q >> 24);
-  return ((uint32_t)q & 0xFFFFFFu) - 2u < 0xFFFFFDu;  // fraction in [2, 2^24 - 2] * 2^-24
+__device__ __forceinline__ bool snap_certain(double t, uint32_t& i) {
+  // s = t + 1.5*2^20 puts t on a 2^-32 grid: for |t| < 2^19 the high word is
+  // 0x41380000 + floor(t) and the low word is frac(t) * 2^32.  Outside that
+  // range (and for inf / NaN) the high word leaves the window, so i lands far
+  // outside any image and the point is a certain miss.  A fraction within
+  // 2^-23 of an integer is reported uncertain (exact f64 path decides).
+  const double s = __dadd_rn(t, 1572864.0);
+  i = (uint32_t)__double2hiint(s) - 0x41380000u;
+  return (uint32_t)__double2loint(s) - 512u < 0xFFFFFC01u;
 }
 
 __device__ __forceinline__ void project_fast(float x, float y, float z, const DevCam& k,
@@ -136,16 +137,13 @@ __device__ __forceinline__ void project_fast(float x, float y, float z, const De
   const double fy = __fma_rn(w2, k.fr_[5], __fma_rn(w1, k.fr_[4], __dmul_rn(w0, k.fr_[3])));
   const double tx = __fma_rn(fx, r, k.cxh);
   const double ty = __fma_rn(fy, r, k.cyh);
-  // |t| < 2^16 on the high word (integer pipe; NaN fails)
-  const bool sane = (((uint32_t)__double2hiint(tx) & 0x7FFFFFFFu) < 0x40F00000u) &&
-                    (((uint32_t)__double2hiint(ty) & 0x7FFFFFFFu) < 0x40F00000u);
-  int ix, iy;
+  uint32_t ix, iy;
   const bool cx_ok = snap_certain(tx, ix);
   const bool cy_ok = snap_certain(ty, iy);
-  const bool certain = k.fast && sane && cx_ok && cy_ok;
-  const bool inside = (uint32_t)ix < (uint32_t)k.w && (uint32_t)iy < (uint32_t)k.h;
-  ix_out = (uint32_t)ix;
-  iy_out = (uint32_t)iy;
+  const bool certain = k.fast && cx_ok && cy_ok;
+  const bool inside = ix < (uint32_t)k.w && iy < (uint32_t)k.h;
+  ix_out = ix;
+  iy_out = iy;
   hit = in_depth && certain && inside;  // certain hit
   uncertain = in_depth && !certain;     // in depth range, snap not certified
 }
