@@ -71,6 +71,10 @@ int nar_device_count(int32_t* count);
 /* Host memory helpers (pinned allocations make H2D copies true async DMA). */
 int nar_host_alloc(void** ptr, size_t bytes);
 int nar_host_free(void* ptr);
+/* Device address of mapped pinned host memory (NAR_ERR_INVALID for pageable or
+ * device memory).  Kernels read through it over PCIe ("zero-copy"): the
+ * resolve gathers only the winners' attributes instead of uploading streams. */
+int nar_host_mapped_pointer(const void* host, void** dev);
 
 /* ---- host-parity twin of the reference FFI --------------------------------------
  * Same arguments and semantics as `_native.zbuffer_accumulate` (_native.pyx:32):

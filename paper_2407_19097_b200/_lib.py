@@ -107,6 +107,7 @@ SIGNATURES = {
     "nar_device_count": (C.c_int, [C.POINTER(C.c_int32)]),
     "nar_host_alloc": (C.c_int, [C.POINTER(C.c_void_p), C.c_size_t]),
     "nar_host_free": (C.c_int, [_vp]),
+    "nar_host_mapped_pointer": (C.c_int, [_vp, C.POINTER(C.c_void_p)]),
     "nar_zbuffer_accumulate": (
         C.c_int,
         [_vp, _vp, _i64, _u64, _vp, _vp, _d, _d, _d, _d, _d, _i32, _i32],
@@ -210,3 +211,11 @@ def stream_handle(stream) -> int:
     if stream is None:
         stream = torch.cuda.current_stream()
     return int(stream.cuda_stream)
+
+
+def mapped_pointer(host_ptr: int):
+    """Device address of mapped pinned host memory, or None (pageable memory)."""
+    out = C.c_void_p()
+    if load().nar_host_mapped_pointer(C.c_void_p(host_ptr), C.byref(out)) != 0:
+        return None
+    return out.value

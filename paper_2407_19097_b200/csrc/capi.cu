@@ -63,4 +63,17 @@ int nar_host_free(void* ptr) {
   return NAR_OK;
 }
 
+int nar_host_mapped_pointer(const void* host, void** dev) {
+  if (!host || !dev) return nar::set_error(NAR_ERR_INVALID, "NULL argument");
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, host) != cudaSuccess) {
+    cudaGetLastError();
+    return nar::set_error(NAR_ERR_INVALID, "pointer is not CUDA host memory");
+  }
+  if (a.type != cudaMemoryTypeHost || !a.devicePointer)
+    return nar::set_error(NAR_ERR_INVALID, "pointer is not mapped pinned host memory");
+  *dev = a.devicePointer;
+  return NAR_OK;
+}
+
 }  // extern "C"

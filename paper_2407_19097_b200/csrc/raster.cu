@@ -705,60 +705,82 @@ static int validate_camera(const nar_camera* cam) {
   return NAR_OK;
 }
 
+// Host-buffer render: points stream through two device staging buffers on a
+// copy stream while the previous chunk renders (copy/compute overlap).  The
+// staging buffers, copy stream, events and Hi-Z scratch persist across calls
+// (one set per process, grown on demand) so a frame-rate caller pays no
+// allocation; the `done` events carry over, so a call never overwrites a
+// buffer an earlier call's render is still reading.
+struct HostPath {
+  std::mutex mu;
+  float* buf[2] = {nullptr, nullptr};
+  int64_t cap = 0;  // points per buffer
+  uint16_t* zmax = nullptr;
+  cudaStream_t cp = nullptr;
+  cudaEvent_t copied[2] = {nullptr, nullptr}, done[2] = {nullptr, nullptr};
+};
+static HostPath g_host;
+
+static int host_path_reserve(HostPath& h, int64_t chunk) {
+  if (!h.cp) {
+    if (cudaStreamCreateWithFlags(&h.cp, cudaStreamNonBlocking) != cudaSuccess)
+      return set_error(NAR_ERR_CUDA, "stream creation failed");
+    for (int b = 0; b < 2; ++b) {
+      cudaEventCreateWithFlags(&h.copied[b], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&h.done[b], cudaEventDisableTiming);
+      cudaEventRecord(h.done[b], h.cp);
+    }
+    if (cudaMalloc(reinterpret_cast<void**>(&h.zmax), (size_t)kHizMaxEntries * 2) != cudaSuccess)
+      return set_error(NAR_ERR_NOMEM, "cudaMalloc of Hi-Z scratch failed");
+  }
+  if (chunk > h.cap) {
+    for (int b = 0; b < 2; ++b) {
+      cudaEventSynchronize(h.done[b]);
+      if (h.buf[b]) cudaFree(h.buf[b]);
+      h.buf[b] = nullptr;
+    }
+    h.cap = 0;
+    for (int b = 0; b < 2; ++b)
+      if (cudaMalloc(reinterpret_cast<void**>(&h.buf[b]), (size_t)chunk * 12) != cudaSuccess)
+        return set_error(NAR_ERR_NOMEM, "cudaMalloc of point staging failed");
+    h.cap = chunk;
+  }
+  return NAR_OK;
+}
+
 static int render_host_impl(uint64_t* keybuf_dev, const float* pos_host, int64_t n,
                             uint64_t base, const DevCam& cam, bool sgn, cudaStream_t st) {
   if (n <= 0) return NAR_OK;
   const int64_t kChunk = (int64_t)1 << 23;  // 8 Mi points = 96 MiB per buffer
   const int64_t chunk = n < kChunk ? ((n + kTilePts - 1) / kTilePts) * kTilePts : kChunk;
-  const int nbuf = n > chunk ? 2 : 1;
-  float* dbuf[2] = {nullptr, nullptr};
-  uint16_t* zmax = nullptr;
-  cudaStream_t cp = nullptr;
-  cudaEvent_t copied[2] = {nullptr, nullptr}, done[2] = {nullptr, nullptr};
-  int rc = NAR_OK;
-  for (int b = 0; b < nbuf; ++b) {
-    if (cudaMallocAsync(reinterpret_cast<void**>(&dbuf[b]), (size_t)chunk * 12, st) != cudaSuccess) {
-      rc = set_error(NAR_ERR_NOMEM, "cudaMallocAsync of point chunk failed");
+  HostPath& h = g_host;
+  std::lock_guard<std::mutex> lock(h.mu);
+  int rc = host_path_reserve(h, chunk);
+  if (rc) return rc;
+  // calls on different streams share the staging and Hi-Z scratch: order
+  // this call's work after the previous call's renders
+  cudaStreamWaitEvent(st, h.done[0], 0);
+  cudaStreamWaitEvent(st, h.done[1], 0);
+  // the copy stream starts after everything already queued on `st`
+  cudaEvent_t start = h.copied[0];
+  cudaEventRecord(start, st);
+  cudaStreamWaitEvent(h.cp, start, 0);
+  for (int64_t off = 0, k = 0; off < n && !rc; off += chunk, ++k) {
+    const int b = (int)(k & 1);
+    const int64_t cnt = (n - off) < chunk ? (n - off) : chunk;
+    cudaStreamWaitEvent(h.cp, h.done[b], 0);
+    if (cudaMemcpyAsync(h.buf[b], pos_host + 3 * off, (size_t)cnt * 12, cudaMemcpyHostToDevice,
+                        h.cp) != cudaSuccess) {
+      rc = set_error(NAR_ERR_CUDA, "H2D copy of points failed");
       break;
     }
+    cudaEventRecord(h.copied[b], h.cp);
+    cudaStreamWaitEvent(st, h.copied[b], 0);
+    // chunk k > 0 is tested against the coarse depth of chunks 0..k-1
+    rc = launch_render(keybuf_dev, h.buf[b], cnt, base + (uint64_t)off, cam, sgn, st,
+                       n > chunk ? h.zmax : nullptr, k > 0);
+    cudaEventRecord(h.done[b], st);
   }
-  if (!rc && n > chunk &&
-      cudaMallocAsync(reinterpret_cast<void**>(&zmax), (size_t)kHizMaxEntries * 2, st) != cudaSuccess)
-    rc = set_error(NAR_ERR_NOMEM, "cudaMallocAsync of Hi-Z scratch failed");
-  if (!rc && cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking) != cudaSuccess)
-    rc = set_error(NAR_ERR_CUDA, "stream creation failed");
-  for (int b = 0; b < 2 && !rc; ++b) {
-    cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming);
-  }
-  if (!rc) {
-    // the chunk buffers were allocated on `st`; make the copy stream wait
-    cudaEventRecord(done[0], st);
-    cudaStreamWaitEvent(cp, done[0], 0);
-    for (int64_t off = 0, k = 0; off < n && !rc; off += chunk, ++k) {
-      const int b = (int)(k % nbuf);
-      const int64_t cnt = (n - off) < chunk ? (n - off) : chunk;
-      if (k >= nbuf) cudaStreamWaitEvent(cp, done[b], 0);
-      if (cudaMemcpyAsync(dbuf[b], pos_host + 3 * off, (size_t)cnt * 12, cudaMemcpyHostToDevice,
-                          cp) != cudaSuccess) {
-        rc = set_error(NAR_ERR_CUDA, "H2D copy of points failed");
-        break;
-      }
-      cudaEventRecord(copied[b], cp);
-      cudaStreamWaitEvent(st, copied[b], 0);
-      // chunk k > 0 is tested against the coarse depth of chunks 0..k-1
-      rc = launch_render(keybuf_dev, dbuf[b], cnt, base + (uint64_t)off, cam, sgn, st, zmax, k > 0);
-      cudaEventRecord(done[b], st);
-    }
-  }
-  for (int b = 0; b < nbuf; ++b)
-    if (dbuf[b]) cudaFreeAsync(dbuf[b], st);
-  if (zmax) cudaFreeAsync(zmax, st);
-  for (int b = 0; b < 2; ++b) {
-    if (copied[b]) cudaEventDestroy(copied[b]);
-    if (done[b]) cudaEventDestroy(done[b]);
-  }
-  if (cp) cudaStreamDestroy(cp);
   if (!rc) rc = check_launch("render_host");
   return rc;
 }

@@ -391,6 +391,17 @@ class Renderer:
         return k
 
 
+class _Mapped:
+    """A host array's device address (mapped pinned memory), tensor-like enough
+    for the segment table."""
+
+    def __init__(self, ptr: int, shape):
+        self._ptr, self.shape = ptr, tuple(shape)
+
+    def data_ptr(self) -> int:
+        return self._ptr
+
+
 _renderers: dict = {}
 
 
@@ -409,8 +420,9 @@ def rasterize(pc: PointCloud, cam: CameraPose, sel: StreamSelection, threads: in
     """Render + resolve a host point cloud on the GPU (rasterizer.py:123-188).
 
     ``threads`` is accepted for signature compatibility and ignored.  Points
-    and the selected streams are copied host->device inside this call; pass a
-    ``PointCloud(..., pinned=True)`` for async DMA copies.
+    are copied host->device inside this call (async DMA when pinned); with a
+    ``PointCloud(..., pinned=True)`` the attribute streams are not copied at
+    all -- the resolve reads the winners' attributes in place.
     """
     import torch
 
@@ -423,24 +435,27 @@ def rasterize(pc: PointCloud, cam: CameraPose, sel: StreamSelection, threads: in
     main = torch.cuda.current_stream(dev)
     kc = cam.kernel_camera()
     names = sel.needed_streams()
-    # Attribute streams go up on a side stream while the points stream through
-    # nar_render_host's chunk pipeline on the main stream.
+    # Attribute streams in mapped pinned memory are not uploaded: the resolve
+    # gathers just the winners' attributes through their device address
+    # (zero-copy over PCIe).  Pageable streams go up on a side stream while the
+    # points stream through nar_render_host's chunk pipeline on the main stream.
     if getattr(r, "_side", None) is None:
         r._side = torch.cuda.Stream(dev)
     side = r._side
     side.wait_stream(main)
+    segs_streams, pos_dev = {}, None
     with torch.cuda.stream(side):
-        segs_streams = {n: torch.from_numpy(pc.stream(n).data).to(dev, non_blocking=True)
-                        for n in names}
-        pos_dev = (torch.from_numpy(pc.positions).to(dev, non_blocking=True)
-                   if sel.vel2d else None)
-    if pos_dev is None:
-        _lib.call("nar_render_host", r.keybuf.data_ptr(), pc.positions.ctypes.data, pc.count,
-                  C.c_uint64(0), C.byref(kc), r.domain, int(main.cuda_stream))
-    else:
-        main.wait_stream(side)
-        _lib.call("nar_render_hiz", r.keybuf.data_ptr(), r.hiz.data_ptr(), pos_dev.data_ptr(),
-                  pc.count, C.c_uint64(0), C.byref(kc), r.domain, 0, int(main.cuda_stream))
+        for n in names:
+            d = pc.stream(n).data
+            mp = _lib.mapped_pointer(d.ctypes.data) if d.size else None
+            segs_streams[n] = (_Mapped(mp, d.shape) if mp is not None else
+                               torch.from_numpy(d).to(dev, non_blocking=True))
+        if sel.vel2d:
+            mp = _lib.mapped_pointer(pc.positions.ctypes.data) if pc.count else None
+            pos_dev = (_Mapped(mp, pc.positions.shape) if mp is not None else
+                       torch.from_numpy(pc.positions).to(dev, non_blocking=True))
+    _lib.call("nar_render_host", r.keybuf.data_ptr(), pc.positions.ctypes.data, pc.count,
+              C.c_uint64(0), C.byref(kc), r.domain, int(main.cuda_stream))
     main.wait_stream(side)
     meta = {n: _StreamMeta(n, pc.stream(n).format, pc.stream(n).arity) for n in names}
     cloud = DeviceCloud([{"begin": 0, "count": pc.count, "positions": pos_dev,
@@ -457,6 +472,8 @@ def rasterize(pc: PointCloud, cam: CameraPose, sel: StreamSelection, threads: in
         host[k].copy_(getattr(res, k), non_blocking=True)
     main.synchronize()  # also keeps the uploaded tensors alive until consumed
     names_out = sel.channel_names(pc)
-    return FeatureImage(W, H, names_out, host["data"].numpy()[:H, :W].copy(),
-                        host["coverage"].numpy().copy(), host["index_plane"].numpy().copy(),
-                        host["depth"].numpy().copy())
+    # torch's CPU copy is multi-threaded (numpy's is not): ~60 MB at 1080p
+    own = {k: host[k].clone().numpy() for k in ("coverage", "index_plane", "depth")}
+    data = host["data"][:H, :W].clone().numpy()
+    return FeatureImage(W, H, names_out, data, own["coverage"], own["index_plane"],
+                        own["depth"])

@@ -58,6 +58,20 @@ def test_golden_random(cuda, golden, ci):
     check_feature_image(fi, g[p + "data"], g[p + "index_plane"], g[p + "depth"], g[p + "coverage"])
 
 
+@pytest.mark.parametrize("ci", [0, 3, 5])
+def test_golden_random_pinned_zero_copy(cuda, golden, ci):
+    """Pinned host clouds: attributes (and positions for vel2d) are read in
+    place by the resolve instead of uploaded -- same framebuffers."""
+    from paper_2407_19097_b200.geometry import PointCloud, Stream
+    from paper_2407_19097_b200.msr import rasterize
+
+    pc, cam, sel, g, p = random_case(golden, ci)
+    pp = PointCloud(pc.positions, [Stream(s.name, s.format, s.data) for s in pc.streams],
+                    pinned=True)
+    fi = rasterize(pp, cam, sel)
+    check_feature_image(fi, g[p + "data"], g[p + "index_plane"], g[p + "depth"], g[p + "coverage"])
+
+
 def test_nonfinite(cuda, golden):
     from paper_2407_19097_b200 import _kernels
     from paper_2407_19097_b200.geometry import Intrinsics
