@@ -444,34 +444,29 @@ def main_ours(args):
     # ---- full NAR frame on the same cloud: render + resolve + U-Net ----------
     pipeline = None
     if world == 1 and args.workload in ("c2", "c3") and not args.no_pipeline:
-        from paper_2407_19097_b200.neural import UNet, UNetConfig, init_params
+        from paper_2407_19097_b200.neural import UNetConfig, init_params
+        from paper_2407_19097_b200.pipeline import NeuralRenderer
 
-        cfg = UNetConfig(input_channels=len(names))
-        net = UNet(cfg, init_params(cfg), device=dev)
-        ph, pw = out["data"].shape[:2]
-        y = torch.empty((ph, pw, 3), dtype=torch.float32, device=dev)
+        # the paper's Table-4 split: MSR / transfer+proc / U-Net
+        cfg = UNetConfig(input_channels=len(names), channel_names=tuple(names))
+        nr = NeuralRenderer(W, H, cfg, init_params(cfg), sel=sel, device=dev)
         for _ in range(3):
-            frame()
-            net.forward_into(out["data"], y)
-        torch.cuda.synchronize()
+            nr.frame(cloud, cam, stream=main)
         kp = max(3, min(args.steps, 20))
-        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(kp)]
-        for k in range(kp):
-            ev[k][0].record(main)
-            frame()
-            ev[k][1].record(main)
-            net.forward_into(out["data"], y)
-            ev[k][2].record(main)
-        torch.cuda.synchronize()
-        fr = sorted(a.elapsed_time(c) for a, _, c in ev)
-        un = sorted(b.elapsed_time(c) for _, b, c in ev)
-        med = fr[len(fr) // 2]
+        ts = [nr.frame(cloud, cam, stream=main)[1] for _ in range(kp)]
+        med = lambda xs: sorted(xs)[len(xs) // 2]
+        tot = med([t.total_ms for t in ts])
+        un = med([t.unet_ms for t in ts])
+        ph, pw = nr._out["data"].shape[:2]
         pipeline = {"workload": f"{desc} + U-Net (random init, {len(names)} input channels) at {pw}x{ph}",
-                    "ms_per_frame_median": med, "fps": 1e3 / med,
-                    "unet_ms_median": un[len(un) // 2],
-                    "unet_tflops": (413.7e9 / 1e12 / (un[len(un) // 2] * 1e-3))
-                    if len(names) == 4 else None,
-                    "frames": kp}
+                    "ms_per_frame_median": tot, "fps": 1e3 / tot,
+                    "stage_ms_median": {"msr": med([t.msr_ms for t in ts]),
+                                        "transfer_proc": med([t.transfer_proc_ms for t in ts]),
+                                        "unet": un},
+                    "unet_ms_median": un,
+                    "unet_tflops": (413.7e9 / 1e12 / (un * 1e-3)) if len(names) == 4 else None,
+                    "frames": kp, "api": "paper_2407_19097_b200.pipeline.NeuralRenderer.frame"}
+        del nr
 
     cpu = None
     if not args.no_cpu and world == 1 and rank == 0:

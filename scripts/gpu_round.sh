@@ -1,0 +1,5 @@
+# default bench line + profiles evidence (launch list, full captures)
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+timeout 600 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; echo "bench rc=$?"
+timeout 300 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"
+bash scripts/gpu_profiles.sh

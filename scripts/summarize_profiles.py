@@ -65,11 +65,10 @@ def launches(tag):
               f"{rsum / 1e3:.1f} us = {100 * rsum / tot:.1f}% of the frame; their DRAM traffic "
               f"{rt_bytes / 1e9:.3f} GB per frame vs 4.200 GB algorithmic (350M x 12 B)."]
     # U-Net launches of one pipeline frame
-    unet = [k for k in seq if "gated_conv" in k["name"] or "head_pyramid" in k["name"]
-            or "pool_bf16" in k["name"]]
-    if unet:
-        per = 20
-        last = unet[-per:]
+    last_resolve = max(i for i, k in enumerate(seq) if "resolve_kernel" in k["name"])
+    last = [k for k in seq[last_resolve + 1:] if "gated_conv" in k["name"] or
+            "head_pyramid" in k["name"] or "pool_bf16" in k["name"] or "out_head" in k["name"]]
+    if last:
         ut = sum(k["gpu__time_duration.sum"] for k in last)
         lines += ["", "## U-Net forward (last pipeline frame)", "",
                   "| kernel | us | DRAM read MB | DRAM write MB |", "|---|---|---|---|"]
