@@ -40,6 +40,10 @@ struct DevCam {
   double cxh, cyh;       // cx + 0.5, cy + 0.5
   double fr_[6];         // f * R rows 0, 1
   int32_t fast;          // camera within the bound's domain
+  // f32 occlusion pre-test (see pretest): camera position as f32 hi + lo,
+  // rotation row 2, f * rows 0/1, principal point; `pre` = bounds hold
+  float chi[3], clo[3], r2f[3], fr0f[3], fr1f[3], cxf, cyf;
+  int32_t pre;
 };
 
 static DevCam make_devcam(const nar_camera& cam) {
@@ -62,6 +66,24 @@ static DevCam make_devcam(const nar_camera& cam) {
             cam.width <= 65536 && cam.height <= 65536)
                ? 1
                : 0;
+  for (int i = 0; i < 3; ++i) {
+    k.chi[i] = (float)cam.campos[i];
+    k.clo[i] = (float)(cam.campos[i] - (double)k.chi[i]);
+    k.r2f[i] = (float)cam.R[6 + i];
+    k.fr0f[i] = (float)(cam.f * cam.R[i]);
+    k.fr1f[i] = (float)(cam.f * cam.R[3 + i]);
+  }
+  k.cxf = (float)cam.cx;
+  k.cyf = (float)cam.cy;
+  // pretest error budget: |T'32 - T'| < 0.5 px and relative uz32 error
+  // < 2^-14 for every point whose pixel is within 1 of the image (|w|/uz <= K)
+  const double af = fabs(cam.f);
+  const double K = sqrt(1.0 + ((cam.width + 2.0) / af) * ((cam.width + 2.0) / af) +
+                        ((cam.height + 2.0) / af) * ((cam.height + 2.0) / af));
+  k.pre = (k.fast && af >= 1e-3 && cam.width / af < 1024.0 && cam.height / af < 1024.0 &&
+           K <= 16.0 && af * K < 65536.0 && fabs(cam.cx) < 131072.0 && fabs(cam.cy) < 131072.0)
+              ? 1
+              : 0;
   return k;
 }
 
@@ -148,6 +170,36 @@ __device__ __forceinline__ void project_fast(float x, float y, float z, const De
   uncertain = in_depth && !certain;     // in depth range, snap not certified
 }
 
+// f32 occlusion pre-test.  T'32 = (f R0 . w32) * rcp(uz32) + cx approximates
+// T - 0.5 within 0.5 px for every point whose pixel is within one pixel of the
+// image (DevCam::pre bounds), so round(T'32) is within +-1 of the exact pixel
+// floor(T); points further out stay outside.  `zd` is the Hi-Z dilated by one
+// pixel (max over the block's pixels and their 8-neighbourhood), so the block
+// of the clamped approximate pixel bounds the exact pixel's depth.  Returns
+// true when the point certainly cannot win (outside, or strictly behind).
+__device__ __forceinline__ bool pretest_reject(float x, float y, float z, const DevCam& k,
+                                               const uint16_t* zd, int shift, int zw) {
+  const float w0 = (x - k.chi[0]) - k.clo[0];
+  const float w1 = (y - k.chi[1]) - k.clo[1];
+  const float w2 = (z - k.chi[2]) - k.clo[2];
+  const float uz = fmaf(w2, k.r2f[2], fmaf(w1, k.r2f[1], w0 * k.r2f[0]));
+  float rz;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rz) : "f"(uz));
+  const float fx = fmaf(w2, k.fr0f[2], fmaf(w1, k.fr0f[1], w0 * k.fr0f[0]));
+  const float fy = fmaf(w2, k.fr1f[2], fmaf(w1, k.fr1f[1], w0 * k.fr1f[0]));
+  // round to nearest via 1.5*2^23; u = round(T'32) + 1 in [0, W+1] <=> candidate
+  const uint32_t ux = (uint32_t)__float_as_int(fmaf(fx, rz, k.cxf) + 12582912.0f) - 0x4B3FFFFFu;
+  const uint32_t uy = (uint32_t)__float_as_int(fmaf(fy, rz, k.cyf) + 12582912.0f) - 0x4B3FFFFFu;
+  const bool near_img = ux <= (uint32_t)k.w + 1u && uy <= (uint32_t)k.h + 1u;
+  const uint32_t cxp = min(max(ux, 1u), (uint32_t)k.w) - 1u;
+  const uint32_t cyp = min(max(uy, 1u), (uint32_t)k.h) - 1u;
+  const uint32_t zb = near_img ? (cyp >> shift) * (uint32_t)zw + (cxp >> shift) : 0u;
+  // (f32 bits of uz32 * (1 - 2^-14)) >> 16 > zd: strictly behind (negative / NaN uz32
+  // compare high and are rejected unless the block is still empty)
+  const bool behind = (__float_as_uint(uz * 0.99993896484375f) >> 16) > (uint32_t)zd[zb];
+  return !near_img || behind;
+}
+
 template <bool kSigned>
 __device__ __forceinline__ void fold_key(uint64_t* keybuf, uint32_t pix, uint64_t key) {
   if (kSigned) {
@@ -194,20 +246,24 @@ constexpr int kQueueBytes = kRenderWarps * 32 * 16;
 constexpr int kHizMaxEntries = 32768;                        // 64 KB coarse depth (u16)
 constexpr int kRenderSmem =
     kRingBytes + kQueueBytes + kHizMaxEntries * 2 + kRenderWarps * kWarpStages * 8 + 128;
-constexpr int kTilePts = kChunkPts;  // granularity of the TMA path (tail -> simple kernel)
+constexpr int kUnitPts = 2 * kChunkPts;  // schedule granularity (tail -> simple kernel)
+constexpr int kUnitBytes = kUnitPts * 12;
+constexpr int kTilePts = kUnitPts;
 
-// Chunk schedule of one launch: linear chunk slots j in [j0, j1) map to
-// chunks of the cloud by mode 0: j; 1 (Hi-Z seed pass): j*S; 2 (the rest):
-// j + j/(S-1) + 1, i.e. every chunk that is not a multiple of S.
+// Unit schedule of one launch: slots j in [j0, j1) map to 128-point units of
+// the cloud by mode 0: j; 1 (Hi-Z seed pass): j*S; 2 (the rest):
+// j + j/(S-1) + 1, i.e. every unit that is not a multiple of S.  The exact
+// kernel walks 64-point halves of the units (chunk c = slot c/2, half c%2).
 constexpr int kHizSeedStride = 16;  // S
 struct ChunkMap {
-  int64_t j0, j1;  // chunk slots (< 2^32: point indices are 32-bit)
+  int64_t j0, j1;  // unit slots (< 2^25: point indices are 32-bit)
   int32_t mode;
-  __device__ __forceinline__ int64_t chunk(int64_t j) const {
-    const uint32_t u = (uint32_t)j;
-    return mode == 0 ? j
-                     : (mode == 1 ? (int64_t)u * kHizSeedStride
-                                  : (int64_t)u + u / (kHizSeedStride - 1) + 1);
+  __device__ __forceinline__ uint32_t unit(uint32_t j) const {
+    return mode == 0 ? j : (mode == 1 ? j * kHizSeedStride : j + j / (kHizSeedStride - 1) + 1);
+  }
+  // first point of 64-point chunk c (c counts halves of slots)
+  __device__ __forceinline__ uint32_t off64(uint32_t c) const {
+    return unit(c >> 1) * kUnitPts + (c & 1u) * kChunkPts;
   }
 };
 
@@ -246,7 +302,7 @@ __device__ __forceinline__ void flush_queue(const QEntry* q, int n, int lane, ui
 // (4) fold the PREVIOUS chunk's survivors, whose keybuf reads were issued one
 //     step ago, so the random-L2 read latency overlaps a chunk of math;
 // (5) issue this chunk's keybuf reads.
-template <bool kSigned, bool kDedup>
+template <bool kSigned>
 __global__ void __launch_bounds__(kRenderThreads, 1)
     render_tma_kernel(uint64_t* __restrict__ keybuf, const float* __restrict__ pos,
                       const ChunkMap cm, uint64_t base_index, const DevCam cam, const HizArgs hz) {
@@ -258,9 +314,9 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytes + kQueueBytes +
                                                kHizMaxEntries * 2) + warp * kWarpStages;
 
-  const int64_t c_first = cm.j0 + (int64_t)blockIdx.x * kRenderWarps + warp;
+  const int64_t c_first = 2 * cm.j0 + (int64_t)blockIdx.x * kRenderWarps + warp;
   const int64_t c_stride = (int64_t)gridDim.x * kRenderWarps;
-  const int64_t n_chunks = cm.j1;
+  const int64_t n_chunks = 2 * cm.j1;
   if (lane == 0) {
     for (int s = 0; s < kWarpStages; ++s) mbar_init(&full[s], 1);
     fence_mbar_init();
@@ -268,7 +324,7 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
       const int64_t c = c_first + (int64_t)s * c_stride;
       if (c < n_chunks) {
         mbar_expect_tx(&full[s], kChunkBytes);
-        bulk_g2s(ring + s * (kChunkPts * 3), pos + cm.chunk(c) * (kChunkPts * 3), kChunkBytes,
+        bulk_g2s(ring + s * (kChunkPts * 3), pos + (size_t)cm.off64((uint32_t)c) * 3, kChunkBytes,
                  &full[s]);
       }
     }
@@ -300,7 +356,7 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
     const int s = k % kWarpStages;
     mbar_wait(&full[s], (uint32_t)(k / kWarpStages) & 1u);
     const float* chunk = ring + s * (kChunkPts * 3);
-    const uint32_t cbase = (uint32_t)base_index + (uint32_t)cm.chunk(c) * (uint32_t)kChunkPts;
+    const uint32_t cbase = (uint32_t)base_index + cm.off64((uint32_t)c);
 
     // (1) projections: straight-line, interleavable across the 4 points
     float px[kPtsPerThread], py[kPtsPerThread], pz[kPtsPerThread];
@@ -319,7 +375,7 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
       if (lane == 0 && cn < n_chunks) {
         fence_proxy_async_smem();
         mbar_expect_tx(&full[s], kChunkBytes);
-        bulk_g2s(ring + s * (kChunkPts * 3), pos + (size_t)cm.chunk(cn) * (kChunkPts * 3),
+        bulk_g2s(ring + s * (kChunkPts * 3), pos + (size_t)cm.off64((uint32_t)cn) * 3,
                  kChunkBytes, &full[s]);
       }
     }
@@ -382,8 +438,138 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
   flush_queue<kSigned>(wq, qn, lane, keybuf, cam);
 }
 
-// Coarse max depth of the current keybuf: 2^shift threads per coarse block,
-// one pixel row each (independent loads), max-reduced with warp shuffles.
+// Hi-Z passes: the f32 pre-test rejects most points in ~35 instructions; the
+// rest (candidates) are compacted into a per-warp shared-memory queue and run
+// through the exact path 32 at a time with every lane busy:
+// (1) pre-test both points of the lane; ballot-compact candidates (xyz, index)
+//     onto the queue; hand the ring slot back to TMA;
+// (2) while >= 32 are queued, pop 32: certified projection (uncertain ones
+//     take the exact f64 path inline -- they are ~1e-6 of points), early-z
+//     read of the keybuf and atomicMin if smaller.
+// Each warp step takes one 128-point unit (4 points per lane) in one ring
+// stage; candidates are drained after each half, so the queue never holds
+// more than 31 + 64.
+constexpr int kPreStages = 3;
+constexpr int kPreRingBytes = kRenderWarps * kPreStages * kUnitBytes;
+constexpr int kCandCap = 32 + kChunkPts;  // queue entries per warp
+constexpr int kCandBytes = kRenderWarps * kCandCap * 16;
+constexpr int kPreSmem =
+    kPreRingBytes + kCandBytes + kHizMaxEntries * 2 + kRenderWarps * kPreStages * 8 + 128;
+static_assert(kPreSmem <= 227 * 1024, "pre-test kernel smem");
+
+template <bool kSigned>
+__device__ __forceinline__ void exact_candidate(const QEntry e, uint64_t* keybuf,
+                                                const DevCam& cam) {
+  uint32_t ix, iy, db;
+  bool hit, unc;
+  project_fast(e.x, e.y, e.z, cam, ix, iy, db, hit, unc);
+  if (hit) {
+    fold_key<kSigned>(keybuf, iy * (uint32_t)cam.w + ix, ((uint64_t)db << 32) | e.idx);
+  } else if (unc) {
+    uint32_t pix;
+    if (project_point(e.x, e.y, e.z, cam, pix, db))
+      fold_key<kSigned>(keybuf, pix, ((uint64_t)db << 32) | e.idx);
+  }
+}
+
+template <bool kSigned>
+__global__ void __launch_bounds__(kRenderThreads, 1)
+    render_pre_kernel(uint64_t* __restrict__ keybuf, const float* __restrict__ pos,
+                      const ChunkMap cm, uint64_t base_index, const DevCam cam, const HizArgs hz) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float* ring = reinterpret_cast<float*>(smem) + warp * (kPreStages * kUnitPts * 3);
+  QEntry* wq = reinterpret_cast<QEntry*>(smem + kPreRingBytes) + warp * kCandCap;
+  uint16_t* zs = reinterpret_cast<uint16_t*>(smem + kPreRingBytes + kCandBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kPreRingBytes + kCandBytes +
+                                               kHizMaxEntries * 2) + warp * kPreStages;
+
+  const uint32_t j_first = (uint32_t)cm.j0 + blockIdx.x * kRenderWarps + warp;
+  const uint32_t j_stride = gridDim.x * kRenderWarps;
+  const uint32_t j_end = (uint32_t)cm.j1;
+  if (lane == 0) {
+    for (int s = 0; s < kPreStages; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+    for (int s = 0; s < kPreStages; ++s) {
+      const uint32_t j = j_first + s * j_stride;
+      if (j < j_end) {
+        mbar_expect_tx(&full[s], kUnitBytes);
+        bulk_g2s(ring + s * (kUnitPts * 3), pos + (size_t)cm.unit(j) * (kUnitPts * 3),
+                 kUnitBytes, &full[s]);
+      }
+    }
+  }
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(hz.zmax);
+    uint4* dst = reinterpret_cast<uint4*>(zs);
+    for (int i = tid; i < (hz.entries + 7) / 8; i += kRenderThreads) dst[i] = __ldcg(src + i);
+    __syncthreads();
+  }
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  int qn = 0;  // warp-uniform queue fill
+  int k = 0;
+  for (uint32_t j = j_first; j < j_end; j += j_stride, ++k) {
+    const int s = k % kPreStages;
+    mbar_wait(&full[s], (uint32_t)(k / kPreStages) & 1u);
+    const float* unit = ring + s * (kUnitPts * 3);
+    const uint32_t cb = (uint32_t)base_index + cm.unit(j) * kUnitPts;
+    float px[4], py[4], pz[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int p = q * 32 + lane;
+      px[q] = unit[3 * p];
+      py[q] = unit[3 * p + 1];
+      pz[q] = unit[3 * p + 2];
+    }
+    __syncwarp();
+    {  // stage s is consumed: refill it with unit k + kPreStages
+      const uint32_t jn = j + kPreStages * j_stride;
+      if (lane == 0 && jn < j_end) {
+        fence_proxy_async_smem();
+        mbar_expect_tx(&full[s], kUnitBytes);
+        bulk_g2s(ring + s * (kUnitPts * 3), pos + (size_t)cm.unit(jn) * (kUnitPts * 3),
+                 kUnitBytes, &full[s]);
+      }
+    }
+    bool cand[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      cand[q] = !pretest_reject(px[q], py[q], pz[q], cam, zs, hz.shift, hz.zw);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+      for (int q = 2 * h; q < 2 * h + 2; ++q) {
+        const uint32_t b = __ballot_sync(0xffffffffu, cand[q]);
+        if (cand[q])
+          wq[qn + __popc(b & lt_mask)] =
+              QEntry{px[q], py[q], pz[q], cb + (uint32_t)(q * 32 + lane)};
+        qn += __popc(b);
+      }
+      if (qn >= 32) {  // warp-uniform; at most 31 + 64 queued
+        __syncwarp();
+        const QEntry e = wq[qn - 32 + lane];
+        __syncwarp();
+        qn -= 32;
+        exact_candidate<kSigned>(e, keybuf, cam);
+        if (qn >= 32) {
+          __syncwarp();
+          const QEntry e2 = wq[qn - 32 + lane];
+          __syncwarp();
+          qn -= 32;
+          exact_candidate<kSigned>(e2, keybuf, cam);
+        }
+      }
+    }
+  }
+  __syncwarp();
+  if (lane < qn) exact_candidate<kSigned>(wq[lane], keybuf, cam);
+}
+
+// Coarse max depth of the current keybuf, dilated by one pixel: zq[b] covers
+// the block's pixels and their 8-neighbourhood (the window the f32 pre-test
+// needs; for the exact test it is merely looser).  2^shift threads per block,
+// one pixel row each plus the rows above / below for the edge threads,
+// max-reduced with warp shuffles.
 template <bool kSigned>
 __global__ void __launch_bounds__(256)
     hiz_kernel(const uint64_t* __restrict__ keybuf, int W, int H, int shift, int zw, int zh,
@@ -395,18 +581,22 @@ __global__ void __launch_bounds__(256)
   uint32_t m = 0;
   if (valid) {
     const int bx = b % zw, by = b / zw;
-    const int y = (by << shift) + row, x0 = bx << shift;
-    if (y < H) {
-      const unsigned long long* p = reinterpret_cast<const unsigned long long*>(keybuf) +
-                                    (size_t)y * W + x0;
-      const int n = min(side, W - x0);
-#pragma unroll 8
-      for (int i = 0; i < n; ++i) {
-        uint64_t k = __ldcg(p + i);
+    const int x0 = max((bx << shift) - 1, 0), x1 = min((bx << shift) + side + 1, W);
+    auto scan = [&](int y) {
+      if (y < 0 || y >= H) return;
+      const unsigned long long* p =
+          reinterpret_cast<const unsigned long long*>(keybuf) + (size_t)y * W;
+#pragma unroll 4
+      for (int x = x0; x < x1; ++x) {
+        uint64_t k = __ldcg(p + x);
         if (kSigned) k ^= NAR_SIGN_FLIP;
         m = max(m, (uint32_t)(k >> 32));
       }
-    }
+    };
+    const int y = (by << shift) + row;
+    scan(y);
+    if (row == 0) scan(y - 1);
+    if (row == side - 1) scan(y + 1);
   }
   for (int o = 1; o < side; o <<= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
   if (valid && row == 0) {
@@ -600,7 +790,7 @@ __global__ void __launch_bounds__(256)
 static int g_num_sms = 0;
 static int g_render_blocks_per_sm = 0;
 static std::once_flag g_init_once;
-static bool g_dedup = false;  // warp pre-dedup of same-pixel hits (NAR_RENDER_DEDUP=1 enables)
+static bool g_no_pre = false;  // NAR_RENDER_NO_PRETEST=1: exact-path-only Hi-Z passes
 
 static int device_init() {
   int err = 0;
@@ -608,16 +798,16 @@ static int device_init() {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) { err = 1; return; }
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(render_tma_kernel<false, false>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, kRenderSmem);
-    cudaFuncSetAttribute(render_tma_kernel<true, false>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, kRenderSmem);
-    cudaFuncSetAttribute(render_tma_kernel<false, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, kRenderSmem);
-    cudaFuncSetAttribute(render_tma_kernel<true, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, kRenderSmem);
-    const char* dd = getenv("NAR_RENDER_DEDUP");
-    g_dedup = dd && dd[0] == '1';
+    cudaFuncSetAttribute(render_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kRenderSmem);
+    cudaFuncSetAttribute(render_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kRenderSmem);
+    cudaFuncSetAttribute(render_pre_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kPreSmem);
+    cudaFuncSetAttribute(render_pre_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kPreSmem);
+    const char* np = getenv("NAR_RENDER_NO_PRETEST");
+    g_no_pre = np && np[0] == '1';
     g_render_blocks_per_sm = 1;
   });
   if (err || g_num_sms == 0) return set_error(NAR_ERR_CUDA, "no CUDA device");
@@ -649,8 +839,9 @@ static int launch_render(uint64_t* keybuf, const float* pos, int64_t n, uint64_t
     const int64_t n_tiles = n / kTilePts;
     if (n_tiles > 0) {
       const int64_t sms = g_num_sms;
-      auto kern = sgn ? (g_dedup ? render_tma_kernel<true, true> : render_tma_kernel<true, false>)
-                      : (g_dedup ? render_tma_kernel<false, true> : render_tma_kernel<false, false>);
+      auto kern = sgn ? render_tma_kernel<true> : render_tma_kernel<false>;
+      auto kpre = sgn ? render_pre_kernel<true> : render_pre_kernel<false>;
+      const bool pre = cam.pre && !g_no_pre;
       auto run = [&](ChunkMap cm, bool with_hiz) {
         HizArgs hz{nullptr, shift, zw, zw * zh};
         if (with_hiz) {
@@ -660,13 +851,23 @@ static int launch_render(uint64_t* keybuf, const float* pos, int64_t n, uint64_t
         const int64_t nj = cm.j1 - cm.j0;
         const int64_t need = (nj + kRenderWarps - 1) / kRenderWarps;
         const int grid = (int)(need < sms ? need : sms);
-        if (grid > 0) kern<<<grid, kRenderThreads, kRenderSmem, st>>>(keybuf, pos, cm, base, cam, hz);
+        if (grid <= 0) return;
+        if (with_hiz && pre)
+          kpre<<<grid, kRenderThreads, kPreSmem, st>>>(keybuf, pos, cm, base, cam, hz);
+        else
+          kern<<<grid, kRenderThreads, kRenderSmem, st>>>(keybuf, pos, cm, base, cam, hz);
       };
       // Hi-Z schedule: a seed pass over every S-th chunk (spread over the whole
       // cloud, so the coarse depth covers the screen even for spatially sorted
       // input), then the remaining chunks in passes, each after a refresh.
       const int64_t S = kHizSeedStride;
-      const int64_t min_pass = sms * kRenderWarps * 32;  // ~32 steps per warp per pass
+      // ~16 units per warp per pass; NAR_RENDER_PASS_UNITS overrides (tests force
+      // the multi-pass schedule on small clouds with it)
+      int64_t min_pass = sms * kRenderWarps * 16;
+      if (const char* e = getenv("NAR_RENDER_PASS_UNITS")) {
+        const long long v = atoll(e);
+        if (v > 0) min_pass = v;
+      }
       if (zmax && n_tiles >= S * min_pass / 4) {
         const int64_t n_seed = (n_tiles + S - 1) / S;
         run(ChunkMap{0, n_seed, 1}, refresh_first);

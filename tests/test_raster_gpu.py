@@ -269,3 +269,41 @@ def test_pixel_snap_boundaries(cuda):
     args = (cam.orientation, cam.position, f, cx, cy, intr.near, intr.far, W, H)
     ref = oracle.zbuffer_render(pos, *args, threads=4)
     assert np.array_equal(_kernels.zbuffer_render(pos, *args), ref)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_hiz_pretest_multipass_vs_oracle(cuda, seed, monkeypatch):
+    """The Hi-Z schedule (seed pass, then passes through the f32 pre-test with
+    the dilated coarse depth) forced onto small clouds: random scales, far
+    offsets from the origin, cameras inside the cloud, wide/narrow FOV,
+    duplicates -- keybuf bit-identical to the oracle."""
+    import os
+
+    from paper_2407_19097_b200.geometry import Intrinsics, look_at
+    from paper_2407_19097_b200.msr import DeviceCloud, Renderer
+
+    monkeypatch.setenv("NAR_RENDER_PASS_UNITS", "48")
+    rng = np.random.default_rng(7000 + seed)
+    n = int(10 ** rng.uniform(5.3, 6.3))
+    W, H = int(rng.integers(16, 640)), int(rng.integers(16, 480))
+    scale = 10.0 ** rng.uniform(-2, 3)
+    offset = rng.normal(size=3) * scale * (10.0 ** rng.uniform(0, 3) if seed % 3 == 0 else 0.0)
+    pos = rng.uniform(-1, 1, (n, 3)) * scale
+    if seed % 4 == 1:  # clustered surfaces: many near-equal depths
+        pos[:, 2] = np.round(pos[:, 2] / scale * 8) / 8 * scale
+    pos = (pos + offset).astype(np.float32)
+    k = n // 10
+    pos[rng.integers(0, n, k)] = pos[rng.integers(0, n, k)]
+    eye = rng.normal(size=3)
+    eye = eye / np.linalg.norm(eye) * scale * rng.uniform(0.3 if seed % 2 else 1.5, 4.0) + offset
+    cam = look_at(eye, rng.uniform(-0.2, 0.2, 3) * scale + offset,
+                  Intrinsics(fov_y_deg=rng.uniform(15, 130), width=W, height=H,
+                             near=float(scale * rng.uniform(1e-4, 0.3))))
+    import torch
+
+    r = Renderer(W, H, device=cuda)
+    r.render(DeviceCloud.from_tensors(torch.from_numpy(pos).to(cuda)), cam)
+    i = cam.intrinsics
+    ref = oracle.zbuffer_render(pos, cam.orientation, cam.position, i.focal_px, i.cx, i.cy,
+                                i.near, i.far, W, H, threads=os.cpu_count() or 4)
+    assert np.array_equal(r.keys(), ref)
