@@ -42,7 +42,10 @@ struct DevCam {
   int32_t fast;          // camera within the bound's domain
   // f32 occlusion pre-test (see pretest): camera position as f32 hi + lo,
   // rotation row 2, f * rows 0/1, principal point; `pre` = bounds hold
-  float chi[3], clo[3], r2f[3], fr0f[3], fr1f[3], cxf, cyf;
+  float chi[3];          // camera position rounded to f32
+  float r2f[3], uz0;     // uz = R2 . (p - chi) + uz0      (uz0 = -R2 . (c - chi))
+  float fxr[3], fx0;     // T' uz = (f R0 + cx R2) . (p - chi) + fx0
+  float fyr[3], fy0;
   int32_t pre;
 };
 
@@ -66,22 +69,29 @@ static DevCam make_devcam(const nar_camera& cam) {
             cam.width <= 65536 && cam.height <= 65536)
                ? 1
                : 0;
+  double uz0 = 0.0, fx0 = 0.0, fy0 = 0.0;
   for (int i = 0; i < 3; ++i) {
     k.chi[i] = (float)cam.campos[i];
-    k.clo[i] = (float)(cam.campos[i] - (double)k.chi[i]);
+    const double lo = cam.campos[i] - (double)k.chi[i];
+    const double fxr = cam.f * cam.R[i] + cam.cx * cam.R[6 + i];
+    const double fyr = cam.f * cam.R[3 + i] + cam.cy * cam.R[6 + i];
     k.r2f[i] = (float)cam.R[6 + i];
-    k.fr0f[i] = (float)(cam.f * cam.R[i]);
-    k.fr1f[i] = (float)(cam.f * cam.R[3 + i]);
+    k.fxr[i] = (float)fxr;
+    k.fyr[i] = (float)fyr;
+    uz0 -= cam.R[6 + i] * lo;
+    fx0 -= fxr * lo;
+    fy0 -= fyr * lo;
   }
-  k.cxf = (float)cam.cx;
-  k.cyf = (float)cam.cy;
+  k.uz0 = (float)uz0;
+  k.fx0 = (float)fx0;
+  k.fy0 = (float)fy0;
   // pretest error budget: |T'32 - T'| < 0.5 px and relative uz32 error
   // < 2^-14 for every point whose pixel is within 1 of the image (|w|/uz <= K)
   const double af = fabs(cam.f);
   const double K = sqrt(1.0 + ((cam.width + 2.0) / af) * ((cam.width + 2.0) / af) +
                         ((cam.height + 2.0) / af) * ((cam.height + 2.0) / af));
   k.pre = (k.fast && af >= 1e-3 && cam.width / af < 1024.0 && cam.height / af < 1024.0 &&
-           K <= 16.0 && af * K < 65536.0 && fabs(cam.cx) < 131072.0 && fabs(cam.cy) < 131072.0)
+           K <= 16.0 && (af + fabs(cam.cx) + fabs(cam.cy)) * K < 65536.0)
               ? 1
               : 0;
   return k;
@@ -170,30 +180,27 @@ __device__ __forceinline__ void project_fast(float x, float y, float z, const De
   uncertain = in_depth && !certain;     // in depth range, snap not certified
 }
 
-// f32 occlusion pre-test.  T'32 = (f R0 . w32) * rcp(uz32) + cx approximates
-// T - 0.5 within 0.5 px for every point whose pixel is within one pixel of the
-// image (DevCam::pre bounds), so round(T'32) is within +-1 of the exact pixel
-// floor(T); points further out stay outside.  `zd` is the Hi-Z dilated by one
-// pixel (max over the block's pixels and their 8-neighbourhood), so the block
-// of the clamped approximate pixel bounds the exact pixel's depth.  Returns
-// true when the point certainly cannot win (outside, or strictly behind).
+// f32 occlusion pre-test.  T' = T - 0.5 = (f R0 + cx R2).w / (R2.w) (the
+// principal point folded into the rows, so no separate add), evaluated in f32
+// as T'32 = fx32 * rcp(uz32) + 1.5*2^23: the low word of that sum is
+// round(T'32), which is within +-1 of the exact pixel floor(T) for every point
+// whose pixel is within one pixel of the image (|T'32 - T'| < 0.5 under the
+// DevCam::pre bounds); points further out stay outside.  u = round(T'32) + 1
+// indexes the Hi-Z on a grid shifted by one pixel whose blocks are dilated by
+// one pixel (hiz_kernel), so the block of u bounds the depth of the exact
+// pixel without clamping.  Returns true when the point certainly cannot win.
 __device__ __forceinline__ bool pretest_reject(float x, float y, float z, const DevCam& k,
                                                const uint16_t* zd, int shift, int zw) {
-  const float w0 = (x - k.chi[0]) - k.clo[0];
-  const float w1 = (y - k.chi[1]) - k.clo[1];
-  const float w2 = (z - k.chi[2]) - k.clo[2];
-  const float uz = fmaf(w2, k.r2f[2], fmaf(w1, k.r2f[1], w0 * k.r2f[0]));
+  const float w0 = x - k.chi[0], w1 = y - k.chi[1], w2 = z - k.chi[2];
+  const float uz = fmaf(w2, k.r2f[2], fmaf(w1, k.r2f[1], fmaf(w0, k.r2f[0], k.uz0)));
+  const float fx = fmaf(w2, k.fxr[2], fmaf(w1, k.fxr[1], fmaf(w0, k.fxr[0], k.fx0)));
+  const float fy = fmaf(w2, k.fyr[2], fmaf(w1, k.fyr[1], fmaf(w0, k.fyr[0], k.fy0)));
   float rz;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rz) : "f"(uz));
-  const float fx = fmaf(w2, k.fr0f[2], fmaf(w1, k.fr0f[1], w0 * k.fr0f[0]));
-  const float fy = fmaf(w2, k.fr1f[2], fmaf(w1, k.fr1f[1], w0 * k.fr1f[0]));
-  // round to nearest via 1.5*2^23; u = round(T'32) + 1 in [0, W+1] <=> candidate
-  const uint32_t ux = (uint32_t)__float_as_int(fmaf(fx, rz, k.cxf) + 12582912.0f) - 0x4B3FFFFFu;
-  const uint32_t uy = (uint32_t)__float_as_int(fmaf(fy, rz, k.cyf) + 12582912.0f) - 0x4B3FFFFFu;
-  const bool near_img = ux <= (uint32_t)k.w + 1u && uy <= (uint32_t)k.h + 1u;
-  const uint32_t cxp = min(max(ux, 1u), (uint32_t)k.w) - 1u;
-  const uint32_t cyp = min(max(uy, 1u), (uint32_t)k.h) - 1u;
-  const uint32_t zb = near_img ? (cyp >> shift) * (uint32_t)zw + (cxp >> shift) : 0u;
+  const uint32_t u = (uint32_t)__float_as_int(fmaf(fx, rz, 12582912.0f)) - 0x4B3FFFFFu;
+  const uint32_t v = (uint32_t)__float_as_int(fmaf(fy, rz, 12582912.0f)) - 0x4B3FFFFFu;
+  const bool near_img = u <= (uint32_t)k.w + 1u && v <= (uint32_t)k.h + 1u;
+  const uint32_t zb = near_img ? (v >> shift) * (uint32_t)zw + (u >> shift) : 0u;
   // (f32 bits of uz32 * (1 - 2^-14)) >> 16 > zd: strictly behind (negative / NaN uz32
   // compare high and are rejected unless the block is still empty)
   const bool behind = (__float_as_uint(uz * 0.99993896484375f) >> 16) > (uint32_t)zd[zb];
@@ -243,7 +250,7 @@ constexpr int kChunkBytes = kChunkPts * 12;
 constexpr int kWarpStages = 6;
 constexpr int kRingBytes = kRenderWarps * kWarpStages * kChunkBytes;
 constexpr int kQueueBytes = kRenderWarps * 32 * 16;
-constexpr int kHizMaxEntries = 32768;                        // 64 KB coarse depth (u16)
+constexpr int kHizMaxEntries = 34816;                        // 68 KB coarse depth (u16)
 constexpr int kRenderSmem =
     kRingBytes + kQueueBytes + kHizMaxEntries * 2 + kRenderWarps * kWarpStages * 8 + 128;
 constexpr int kUnitPts = 2 * kChunkPts;  // schedule granularity (tail -> simple kernel)
@@ -393,7 +400,8 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
       const uint32_t db = dbs[j];
       bool hit = hits[j];
       if (use_hiz) {  // behind every pixel of its coarse block? (index clamped: no branch)
-        const uint32_t zb = hit ? (iys[j] >> hz.shift) * (uint32_t)hz.zw + (ixs[j] >> hz.shift) : 0u;
+        const uint32_t zb =
+            hit ? ((iys[j] + 1u) >> hz.shift) * (uint32_t)hz.zw + ((ixs[j] + 1u) >> hz.shift) : 0u;
         hit = hit && (db >> 16) <= zs[zb];
       }
       pix[j] = iys[j] * (uint32_t)cam.w + ixs[j];
@@ -513,14 +521,12 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
     mbar_wait(&full[s], (uint32_t)(k / kPreStages) & 1u);
     const float* unit = ring + s * (kUnitPts * 3);
     const uint32_t cb = (uint32_t)base_index + cm.unit(j) * kUnitPts;
-    float px[4], py[4], pz[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int p = q * 32 + lane;
-      px[q] = unit[3 * p];
-      py[q] = unit[3 * p + 1];
-      pz[q] = unit[3 * p + 2];
-    }
+    // lane l takes points 4l .. 4l+3: three conflict-free 16-byte loads
+    const float4* u4 = reinterpret_cast<const float4*>(unit) + 3 * lane;
+    const float4 a0 = u4[0], a1 = u4[1], a2 = u4[2];
+    const float px[4] = {a0.x, a0.w, a1.z, a2.y};
+    const float py[4] = {a0.y, a1.x, a1.w, a2.z};
+    const float pz[4] = {a0.z, a1.y, a2.x, a2.w};
     __syncwarp();
     {  // stage s is consumed: refill it with unit k + kPreStages
       const uint32_t jn = j + kPreStages * j_stride;
@@ -542,7 +548,7 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
         const uint32_t b = __ballot_sync(0xffffffffu, cand[q]);
         if (cand[q])
           wq[qn + __popc(b & lt_mask)] =
-              QEntry{px[q], py[q], pz[q], cb + (uint32_t)(q * 32 + lane)};
+              QEntry{px[q], py[q], pz[q], cb + (uint32_t)(4 * lane + q)};
         qn += __popc(b);
       }
       if (qn >= 32) {  // warp-uniform; at most 31 + 64 queued
@@ -565,11 +571,12 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
   if (lane < qn) exact_candidate<kSigned>(wq[lane], keybuf, cam);
 }
 
-// Coarse max depth of the current keybuf, dilated by one pixel: zq[b] covers
-// the block's pixels and their 8-neighbourhood (the window the f32 pre-test
-// needs; for the exact test it is merely looser).  2^shift threads per block,
-// one pixel row each plus the rows above / below for the edge threads,
-// max-reduced with warp shuffles.
+// Coarse max depth of the current keybuf on the shifted, dilated grid: block
+// (bu, bv) holds ceil(max depth bits / 2^16) over pixels x in
+// [bu*S - 2, bu*S + S - 1] (and y alike), i.e. the pixels whose u = x + 1 falls
+// in the block plus a one-pixel border -- the window the f32 pre-test needs.
+// S = 2^shift threads per block, one row each (threads 0, 1 take the two extra
+// rows), max-reduced with warp shuffles.
 template <bool kSigned>
 __global__ void __launch_bounds__(256)
     hiz_kernel(const uint64_t* __restrict__ keybuf, int W, int H, int shift, int zw, int zh,
@@ -581,7 +588,7 @@ __global__ void __launch_bounds__(256)
   uint32_t m = 0;
   if (valid) {
     const int bx = b % zw, by = b / zw;
-    const int x0 = max((bx << shift) - 1, 0), x1 = min((bx << shift) + side + 1, W);
+    const int x0 = max((bx << shift) - 2, 0), x1 = min((bx << shift) + side, W);
     auto scan = [&](int y) {
       if (y < 0 || y >= H) return;
       const unsigned long long* p =
@@ -593,10 +600,9 @@ __global__ void __launch_bounds__(256)
         m = max(m, (uint32_t)(k >> 32));
       }
     };
-    const int y = (by << shift) + row;
+    const int y = (by << shift) - 2 + row;
     scan(y);
-    if (row == 0) scan(y - 1);
-    if (row == side - 1) scan(y + 1);
+    if (row < 2) scan(y + side);
   }
   for (int o = 1; o < side; o <<= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
   if (valid && row == 0) {
@@ -608,8 +614,8 @@ __global__ void __launch_bounds__(256)
 static void hiz_geometry(int W, int H, int& shift, int& zw, int& zh) {
   shift = 3;  // <= 5 (one warp per coarse block row set) for any image < 2^32 pixels
   for (;;) {
-    zw = (W + (1 << shift) - 1) >> shift;
-    zh = (H + (1 << shift) - 1) >> shift;
+    zw = ((W + 1) >> shift) + 1;  // u = x + 1 in [0, W]... the shifted grid
+    zh = ((H + 1) >> shift) + 1;
     if ((int64_t)zw * zh <= kHizMaxEntries) return;
     ++shift;
   }

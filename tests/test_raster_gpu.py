@@ -307,3 +307,26 @@ def test_hiz_pretest_multipass_vs_oracle(cuda, seed, monkeypatch):
     ref = oracle.zbuffer_render(pos, cam.orientation, cam.position, i.focal_px, i.cx, i.cy,
                                 i.near, i.far, W, H, threads=os.cpu_count() or 4)
     assert np.array_equal(r.keys(), ref)
+
+
+def test_host_path_chunked_hiz(cuda):
+    """nar_render_host over 20M host points (three 8 Mi-point staging chunks;
+    chunks 2 and 3 are tested against the Hi-Z of the earlier ones) gives the
+    same keybuf as the plain single-pass device render."""
+    import torch
+
+    from paper_2407_19097_b200 import _kernels
+    from paper_2407_19097_b200.geometry import Intrinsics, look_at
+    from paper_2407_19097_b200.msr import DeviceCloud, Renderer
+
+    n = 20_000_000
+    rng = np.random.default_rng(12)
+    pos = rng.uniform(-1, 1, (n, 3)).astype(np.float32)
+    cam = look_at((0.3, -2.0, 0.9), (0, 0, 0), Intrinsics(width=1280, height=720))
+    i = cam.intrinsics
+    kb = _kernels.zbuffer_render(pos, cam.orientation, cam.position, i.focal_px, i.cx, i.cy,
+                                 i.near, i.far, 1280, 720)
+    plain = Renderer(1280, 720, device=cuda)
+    plain.use_hiz = False
+    plain.render(DeviceCloud.from_tensors(torch.from_numpy(pos).to(cuda)), cam)
+    assert np.array_equal(kb, plain.keys())
