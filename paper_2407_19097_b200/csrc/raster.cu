@@ -189,21 +189,53 @@ __device__ __forceinline__ void project_fast(float x, float y, float z, const De
 // indexes the Hi-Z on a grid shifted by one pixel whose blocks are dilated by
 // one pixel (hiz_kernel), so the block of u bounds the depth of the exact
 // pixel without clamping.  Returns true when the point certainly cannot win.
-__device__ __forceinline__ bool pretest_reject(float x, float y, float z, const DevCam& k,
-                                               const uint16_t* zd, int shift, int zw) {
-  const float w0 = x - k.chi[0], w1 = y - k.chi[1], w2 = z - k.chi[2];
+// Packed f32x2 helpers (FADD2 / FFMA2: two lanes of f32 per instruction; a
+// pair built from one value twice becomes a scalar-broadcast operand).
+__device__ __forceinline__ uint64_t pk2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void upk2(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t sub2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+
+// (w0, w1) = (x, y) - chi[0..1] as one FADD2 (x, y adjacent in the lane's
+// registers); returns the reject decision for one point.
+__device__ __forceinline__ bool pretest_reject_w(float w0, float w1, float w2, const DevCam& k,
+                                                 uint32_t zaddr, uint32_t kraw, int shift,
+                                                 int zw) {
   const float uz = fmaf(w2, k.r2f[2], fmaf(w1, k.r2f[1], fmaf(w0, k.r2f[0], k.uz0)));
-  const float fx = fmaf(w2, k.fxr[2], fmaf(w1, k.fxr[1], fmaf(w0, k.fxr[0], k.fx0)));
-  const float fy = fmaf(w2, k.fyr[2], fmaf(w1, k.fyr[1], fmaf(w0, k.fyr[0], k.fy0)));
+  // (T' uz for x, for y) with the rows paired: three FFMA2
+  const uint64_t fxy =
+      fma2(pk2(w2, w2), pk2(k.fxr[2], k.fyr[2]),
+           fma2(pk2(w1, w1), pk2(k.fxr[1], k.fyr[1]),
+                fma2(pk2(w0, w0), pk2(k.fxr[0], k.fyr[0]), pk2(k.fx0, k.fy0))));
   float rz;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rz) : "f"(uz));
-  const uint32_t u = (uint32_t)__float_as_int(fmaf(fx, rz, 12582912.0f)) - 0x4B3FFFFFu;
-  const uint32_t v = (uint32_t)__float_as_int(fmaf(fy, rz, 12582912.0f)) - 0x4B3FFFFFu;
-  const bool near_img = u <= (uint32_t)k.w + 1u && v <= (uint32_t)k.h + 1u;
-  const uint32_t zb = near_img ? (v >> shift) * (uint32_t)zw + (u >> shift) : 0u;
+  // bits of T' + 1.5*2^23 + 1 = 0x4B400000 + u with u = round(T') + 1; the
+  // constant part of the block index is folded into the caller's `zd` base
+  float sx, sy;
+  upk2(fma2(fxy, pk2(rz, rz), pk2(12582913.0f, 12582913.0f)), sx, sy);
+  const uint32_t bu = (uint32_t)__float_as_int(sx), bv = (uint32_t)__float_as_int(sy);
+  const bool near_img = bu - 0x4B400000u <= (uint32_t)k.w + 1u && bv - 0x4B400000u <= (uint32_t)k.h + 1u;
+  // shared address of the block: zaddr = &zs[0] - 2 * kraw, kraw = raw index of u = v = 0
+  const uint32_t raw = (bv >> shift) * (uint32_t)zw + (bu >> shift);
+  uint16_t zq;
+  asm("ld.shared.u16 %0, [%1];" : "=h"(zq) : "r"(zaddr + 2u * (near_img ? raw : kraw)));
   // (f32 bits of uz32 * (1 - 2^-14)) >> 16 > zd: strictly behind (negative / NaN uz32
   // compare high and are rejected unless the block is still empty)
-  const bool behind = (__float_as_uint(uz * 0.99993896484375f) >> 16) > (uint32_t)zd[zb];
+  const bool behind = (__float_as_uint(uz * 0.99993896484375f) >> 16) > (uint32_t)zq;
   return !near_img || behind;
 }
 
@@ -514,6 +546,11 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
     __syncthreads();
   }
   const uint32_t lt_mask = (1u << lane) - 1u;
+  // zs shifted back by the block index of u = 0, v = 0 (see pretest_reject_w);
+  // only dereferenced for in-range u, v
+  const uint32_t kb = 0x4B400000u >> hz.shift;
+  const uint32_t kraw = kb * (uint32_t)hz.zw + kb;
+  const uint32_t zaddr = smem_u32(zs) - 2u * kraw;
   int qn = 0;  // warp-uniform queue fill
   int k = 0;
   for (uint32_t j = j_first; j < j_end; j += j_stride, ++k) {
@@ -537,10 +574,24 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
                  kUnitBytes, &full[s]);
       }
     }
+    // w = p - chi: the (x, y) or (y, z) halves of each point that sit in one
+    // aligned register pair go through FADD2
+    float w[4][3];
+    {
+      const uint64_t c01 = pk2(cam.chi[0], cam.chi[1]), c12 = pk2(cam.chi[1], cam.chi[2]);
+      upk2(sub2(pk2(a0.x, a0.y), c01), w[0][0], w[0][1]);
+      w[0][2] = a0.z - cam.chi[2];
+      w[1][0] = a0.w - cam.chi[0];
+      upk2(sub2(pk2(a1.x, a1.y), c12), w[1][1], w[1][2]);
+      upk2(sub2(pk2(a1.z, a1.w), c01), w[2][0], w[2][1]);
+      w[2][2] = a2.x - cam.chi[2];
+      w[3][0] = a2.y - cam.chi[0];
+      upk2(sub2(pk2(a2.z, a2.w), c12), w[3][1], w[3][2]);
+    }
     bool cand[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q)
-      cand[q] = !pretest_reject(px[q], py[q], pz[q], cam, zs, hz.shift, hz.zw);
+      cand[q] = !pretest_reject_w(w[q][0], w[q][1], w[q][2], cam, zaddr, kraw, hz.shift, hz.zw);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
 #pragma unroll
