@@ -640,10 +640,30 @@ __global__ void __launch_bounds__(256)
   if (valid) {
     const int bx = b % zw, by = b / zw;
     const int x0 = max((bx << shift) - 2, 0), x1 = min((bx << shift) + side, W);
+    // rows are 16-byte aligned when W is even: pairs of keys per load, all
+    // issued before the max (x0 is even)
+    const bool vec = ((W & 1) == 0) && side == 8;
     auto scan = [&](int y) {
       if (y < 0 || y >= H) return;
       const unsigned long long* p =
           reinterpret_cast<const unsigned long long*>(keybuf) + (size_t)y * W;
+      if (vec) {
+        ulonglong2 v[5];
+#pragma unroll
+        for (int i = 0; i < 5; ++i)
+          v[i] = x0 + 2 * i + 1 < x1 ? __ldcg(reinterpret_cast<const ulonglong2*>(p + x0) + i)
+                                     : make_ulonglong2(0ull, 0ull);
+#pragma unroll
+        for (int i = 0; i < 5; ++i) {
+          uint64_t a = v[i].x, b = v[i].y;
+          if (kSigned) {
+            a = x0 + 2 * i + 1 < x1 ? a ^ NAR_SIGN_FLIP : 0ull;
+            b = x0 + 2 * i + 1 < x1 ? b ^ NAR_SIGN_FLIP : 0ull;
+          }
+          m = max(m, max((uint32_t)(a >> 32), (uint32_t)(b >> 32)));
+        }
+        return;
+      }
 #pragma unroll 4
       for (int x = x0; x < x1; ++x) {
         uint64_t k = __ldcg(p + x);
@@ -930,9 +950,27 @@ static int launch_render(uint64_t* keybuf, const float* pos, int64_t n, uint64_t
         run(ChunkMap{0, n_seed, 1}, refresh_first);
         const int64_t n_rest = n_tiles - n_seed;
         int64_t passes = n_rest / min_pass;
-        passes = passes < 1 ? 1 : (passes > 6 ? 6 : passes);
-        for (int64_t p = 0; p < passes; ++p)
-          run(ChunkMap{n_rest * p / passes, n_rest * (p + 1) / passes, 2}, true);
+        int64_t max_passes = 4;
+        if (const char* e = getenv("NAR_RENDER_MAX_PASSES")) {
+          const long long v = atoll(e);
+          if (v > 0) max_passes = v;
+        }
+        passes = passes < 1 ? 1 : (passes > max_passes ? max_passes : passes);
+        // pass sizes grow 1, 2, 4, then stay at 4 (x the first): the early,
+        // loosely culled passes are short and refresh the coarse depth sooner
+        int geo = 1;
+        if (const char* e = getenv("NAR_RENDER_GEO")) geo = atoi(e);
+        int64_t wsum = 0, wt[64];
+        for (int64_t p = 0; p < passes && p < 64; ++p) {
+          wt[p] = geo ? ((int64_t)1 << (p < 2 ? p : 2)) : 1;
+          wsum += wt[p];
+        }
+        int64_t acc = 0;
+        for (int64_t p = 0; p < passes && p < 64; ++p) {
+          const int64_t a = n_rest * acc / wsum;
+          acc += wt[p];
+          run(ChunkMap{a, n_rest * acc / wsum, 2}, true);
+        }
       } else {
         run(ChunkMap{0, n_tiles, 0}, zmax && refresh_first);
       }
