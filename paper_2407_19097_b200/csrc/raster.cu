@@ -745,7 +745,11 @@ __device__ __forceinline__ float stream_value(const void* base, int32_t fmt, int
   return __ldg(static_cast<const float*>(base) + row * arity + col);
 }
 
-template <bool kSigned>
+// kRgbd: the selection is exactly rgb (u8, arity >= 3) + depth -- one float4
+// store per pixel.  Otherwise channels are stored straight to global memory as
+// they are produced (no per-thread channel array: dynamic indexing would put
+// it in local memory).
+template <bool kSigned, bool kRgbd>
 __global__ void __launch_bounds__(256)
     resolve_kernel(uint64_t* __restrict__ keybuf, const ResolveParams P) {
   const int32_t W = P.cam.w, H = P.cam.h;
@@ -754,111 +758,108 @@ __global__ void __launch_bounds__(256)
   if (gid >= npix_out) return;
   const int32_t y = (int32_t)(gid / P.data_w);
   const int32_t x = (int32_t)(gid - (int64_t)y * P.data_w);
-  float ch[NAR_MAX_CHANNELS];
-#pragma unroll
-  for (int c = 0; c < NAR_MAX_CHANNELS; ++c) ch[c] = 0.0f;
-
-  if (y < H && x < W) {
-    const int64_t pix = (int64_t)y * W + x;
-    uint64_t key = keybuf[pix];
-    if (kSigned) key ^= NAR_SIGN_FLIP;
-    if (P.clear) keybuf[pix] = kSigned ? (NAR_EMPTY_KEY ^ NAR_SIGN_FLIP) : NAR_EMPTY_KEY;
-    const bool covered = key != NAR_EMPTY_KEY;
-    const int64_t idx = covered ? (int64_t)(key & 0xFFFFFFFFull) : -1;
-    const float dep = covered ? __uint_as_float((uint32_t)(key >> 32)) : 0.0f;
-    if (P.coverage) P.coverage[pix] = covered ? 1 : 0;
-    if (P.index_plane) P.index_plane[pix] = idx;
-    if (P.depth) P.depth[pix] = dep;
-
-    int s = -1;
-    if (covered) {
-      for (int k = 0; k < P.nseg; ++k)
-        if (idx >= P.seg[k].begin && idx < P.seg[k].begin + P.seg[k].count) s = k;
+  float* dst = P.data ? P.data + gid * P.C : nullptr;
+  if (!(y < H && x < W)) {  // padding of the CNN input: zeros
+    if (dst) {
+      if (kRgbd) *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+      else for (int c = 0; c < P.C; ++c) dst[c] = 0.0f;
     }
-    const bool owner = s >= 0;
-    const nar_selection& sel = P.sel;
-    int col = 0;
-    if (owner) {
-      const nar_segment& sg = P.seg[s];
-      const int64_t row = idx - sg.begin;
-      if (sel.rgb) {
+    return;
+  }
+  const int64_t pix = (int64_t)y * W + x;
+  uint64_t key = keybuf[pix];
+  if (kSigned) key ^= NAR_SIGN_FLIP;
+  if (P.clear) keybuf[pix] = kSigned ? (NAR_EMPTY_KEY ^ NAR_SIGN_FLIP) : NAR_EMPTY_KEY;
+  const bool covered = key != NAR_EMPTY_KEY;
+  const int64_t idx = covered ? (int64_t)(key & 0xFFFFFFFFull) : -1;
+  const float dep = covered ? __uint_as_float((uint32_t)(key >> 32)) : 0.0f;
+  if (P.coverage) P.coverage[pix] = covered ? 1 : 0;
+  if (P.index_plane) P.index_plane[pix] = idx;
+  if (P.depth) P.depth[pix] = dep;
+
+  int s = -1;
+  if (covered) {
+    for (int k = 0; k < P.nseg; ++k)
+      if (idx >= P.seg[k].begin && idx < P.seg[k].begin + P.seg[k].count) s = k;
+  }
+  const nar_selection& sel = P.sel;
+  if (kRgbd) {
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (s >= 0) {
+      const uint8_t* c = static_cast<const uint8_t*>(P.seg[s].rgb) +
+                         (idx - P.seg[s].begin) * sel.rgb_arity;
+      v.x = __fdiv_rn((float)__ldg(c), 255.0f);
+      v.y = __fdiv_rn((float)__ldg(c + 1), 255.0f);
+      v.z = __fdiv_rn((float)__ldg(c + 2), 255.0f);
+      v.w = fminf(fmaxf(__fdiv_rn(P.near_f, dep), 0.0f), 1.0f);
+    }
+    if (dst) *reinterpret_cast<float4*>(dst) = v;
+    return;
+  }
+  if (!dst) return;
+  if (s < 0) {  // empty, or (owner_only) won by another rank's points
+    for (int c = 0; c < P.C; ++c) dst[c] = 0.0f;
+    return;
+  }
+  const nar_segment& sg = P.seg[s];
+  const int64_t row = idx - sg.begin;
+  int col = 0;
+  if (sel.rgb) {
 #pragma unroll
-        for (int c = 0; c < 3; ++c)
-          ch[c] = stream_value(sg.rgb, sel.rgb_format, sel.rgb_arity, row,
-                               sel.rgb_arity == 1 ? 0 : c);
-        col += 3;
-      }
-      if (sel.depth) {
-        // rasterizer.py:156-157 f32(near) / depth, clipped to [0, 1]
-        float d = __fdiv_rn(P.near_f, dep);
-        d = fminf(fmaxf(d, 0.0f), 1.0f);
-        ch[col++] = d;
-      }
-      if (sel.vel2d || sel.vel3d) {
-        double v[3];
+    for (int c = 0; c < 3; ++c)
+      dst[col++] = stream_value(sg.rgb, sel.rgb_format, sel.rgb_arity, row,
+                                sel.rgb_arity == 1 ? 0 : c);
+  }
+  if (sel.depth) {
+    // rasterizer.py:156-157 f32(near) / depth, clipped to [0, 1]
+    dst[col++] = fminf(fmaxf(__fdiv_rn(P.near_f, dep), 0.0f), 1.0f);
+  }
+  if (sel.vel2d || sel.vel3d) {
+    double v[3];
 #pragma unroll
-        for (int c = 0; c < 3; ++c)
-          v[c] = (double)stream_value(sg.velocity, sel.vel_format, sel.vel_arity, row, c);
-        const double scale = sel.velocity_scale;
-        if (sel.vel2d) {
-          // velocity.py:26-48 + camera.py:154-166, f64 (BLAS order: <= 1 f32 ulp)
-          const DevCam& k = P.cam;
-          const double w0 = (double)__ldg(sg.positions + 3 * row) - k.c[0];
-          const double w1 = (double)__ldg(sg.positions + 3 * row + 1) - k.c[1];
-          const double w2 = (double)__ldg(sg.positions + 3 * row + 2) - k.c[2];
-          const double ux = w0 * k.r[0] + w1 * k.r[1] + w2 * k.r[2];
-          const double uy = w0 * k.r[3] + w1 * k.r[4] + w2 * k.r[5];
-          const double uz = w0 * k.r[6] + w1 * k.r[7] + w2 * k.r[8];
-          const double sc = k.f / (uz * uz);
-          double vp0 = 0.0, vp1 = 0.0;
+    for (int c = 0; c < 3; ++c)
+      v[c] = (double)stream_value(sg.velocity, sel.vel_format, sel.vel_arity, row, c);
+    const double scale = sel.velocity_scale;
+    if (sel.vel2d) {
+      // velocity.py:26-48 + camera.py:154-166, f64 (BLAS order: <= 1 f32 ulp)
+      const DevCam& k = P.cam;
+      const double w0 = (double)__ldg(sg.positions + 3 * row) - k.c[0];
+      const double w1 = (double)__ldg(sg.positions + 3 * row + 1) - k.c[1];
+      const double w2 = (double)__ldg(sg.positions + 3 * row + 2) - k.c[2];
+      const double ux = w0 * k.r[0] + w1 * k.r[1] + w2 * k.r[2];
+      const double uy = w0 * k.r[3] + w1 * k.r[4] + w2 * k.r[5];
+      const double uz = w0 * k.r[6] + w1 * k.r[7] + w2 * k.r[8];
+      const double sc = k.f / (uz * uz);
+      double vp0 = 0.0, vp1 = 0.0;
 #pragma unroll
-          for (int j = 0; j < 3; ++j) {
-            const double j0 = (uz * k.r[j] - ux * k.r[6 + j]) * sc;
-            const double j1 = (uz * k.r[3 + j] - uy * k.r[6 + j]) * sc;
-            vp0 += j0 * v[j];
-            vp1 += j1 * v[j];
-          }
-          const double mag = hypot(vp0, vp1);
-          const double theta = mag < 1e-9 ? 0.0 : atan2(-vp1, vp0);
-          ch[col++] = (float)(vp0 / scale);
-          ch[col++] = (float)(vp1 / scale);
-          ch[col++] = (float)theta;
-          ch[col++] = (float)(mag / scale);
-        }
-        if (sel.vel3d) {
-          // velocity.py:17-23
-          const double nrm = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
-          ch[col++] = (float)(v[0] / scale);
-          ch[col++] = (float)(v[1] / scale);
-          ch[col++] = (float)(v[2] / scale);
-          ch[col++] = (float)(nrm / scale);
-        }
+      for (int j = 0; j < 3; ++j) {
+        const double j0 = (uz * k.r[j] - ux * k.r[6 + j]) * sc;
+        const double j1 = (uz * k.r[3 + j] - uy * k.r[6 + j]) * sc;
+        vp0 += j0 * v[j];
+        vp1 += j1 * v[j];
       }
-      for (int q = 0; q < sel.n_scalars; ++q) {
-        const int32_t ar = sel.scalar_arity[q];
-        for (int c = 0; c < ar && col < NAR_MAX_CHANNELS; ++c)
-          ch[col++] = stream_value(sg.scalars[q], sel.scalar_format[q], ar, row, c);
-      }
-      if (sel.coverage_channel && col < NAR_MAX_CHANNELS) ch[col++] = 1.0f;
-    } else if (covered && !P.owner_only) {
-      // winner outside every segment: only possible for inconsistent inputs;
-      // keep zeros (the host validated the index ranges).
+      const double mag = hypot(vp0, vp1);
+      const double theta = mag < 1e-9 ? 0.0 : atan2(-vp1, vp0);
+      dst[col++] = (float)(vp0 / scale);
+      dst[col++] = (float)(vp1 / scale);
+      dst[col++] = (float)theta;
+      dst[col++] = (float)(mag / scale);
+    }
+    if (sel.vel3d) {
+      // velocity.py:17-23
+      const double nrm = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+      dst[col++] = (float)(v[0] / scale);
+      dst[col++] = (float)(v[1] / scale);
+      dst[col++] = (float)(v[2] / scale);
+      dst[col++] = (float)(nrm / scale);
     }
   }
-  if (P.data) {
-    float* dst = P.data + gid * P.C;
-    // channel count is small (<= 16); vectorise when 4-aligned
-    if ((P.C & 3) == 0) {
-      float4* d4 = reinterpret_cast<float4*>(dst);
-#pragma unroll
-      for (int c = 0; c < NAR_MAX_CHANNELS / 4; ++c)
-        if (4 * c < P.C) d4[c] = make_float4(ch[4 * c], ch[4 * c + 1], ch[4 * c + 2], ch[4 * c + 3]);
-    } else {
-#pragma unroll
-      for (int c = 0; c < NAR_MAX_CHANNELS; ++c)
-        if (c < P.C) dst[c] = ch[c];
-    }
+  for (int q = 0; q < sel.n_scalars; ++q) {
+    const int32_t ar = sel.scalar_arity[q];
+    for (int c = 0; c < ar && col < P.C; ++c)
+      dst[col++] = stream_value(sg.scalars[q], sel.scalar_format[q], ar, row, c);
   }
+  if (sel.coverage_channel && col < P.C) dst[col++] = 1.0f;
 }
 
 // ----------------------------------------------------------------------------
@@ -1239,10 +1240,12 @@ int nar_resolve(uint64_t* keybuf_dev, const nar_camera* cam, int32_t key_domain,
   P.clear = out->clear_keybuf;
   const int64_t n_out = (int64_t)P.data_h * P.data_w;
   const int64_t blocks = (n_out + 255) / 256;
-  if (key_domain == NAR_KEYS_SIGNED)
-    resolve_kernel<true><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(keybuf_dev, P);
-  else
-    resolve_kernel<false><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(keybuf_dev, P);
+  const bool rgbd = C == 4 && sel->rgb && sel->depth && sel->rgb_format == NAR_FMT_U8 &&
+                    sel->rgb_arity >= 3 && (reinterpret_cast<uintptr_t>(out->data) & 15) == 0;
+  auto kern = key_domain == NAR_KEYS_SIGNED
+                  ? (rgbd ? resolve_kernel<true, true> : resolve_kernel<true, false>)
+                  : (rgbd ? resolve_kernel<false, true> : resolve_kernel<false, false>);
+  kern<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(keybuf_dev, P);
   return check_launch("resolve");
 }
 
