@@ -45,7 +45,10 @@ struct PyrOut {
   __nv_bfloat16* lvl[8];
 };
 
-__global__ void __launch_bounds__(256)
+// CIN: compile-time upper bound of cin (4, 8 or 16) so the per-pixel channel
+// arrays stay in registers at high occupancy.
+template <int CIN>
+__global__ void __launch_bounds__(256, 4)
     head_pyramid_kernel(const float* __restrict__ x, int H, int W, int cin, int cp,
                         const float* __restrict__ hw, const float* __restrict__ hb, int use_head,
                         int levels, PyrOut out) {
@@ -56,19 +59,24 @@ __global__ void __launch_bounds__(256)
   // level 0: one thread per pixel of the T x T tile (blockDim = T*T <= 256)
   const int ly = t / T, lx = t % T;
   const int y = ty * T + ly, xx = tx * T + lx;
-  float v[16], hv[16];
+  float v[CIN], hv[CIN];
   const float* px = x + ((size_t)y * W + xx) * cin;
+  if (CIN == 4 && cin == 4) {
+    const float4 q = __ldg(reinterpret_cast<const float4*>(px));
+    v[0] = q.x; v[1] = q.y; v[2 % CIN] = q.z; v[3 % CIN] = q.w;
+  } else {
 #pragma unroll
-  for (int c = 0; c < 16; ++c) v[c] = c < cin ? px[c] : 0.f;
+    for (int c = 0; c < CIN; ++c) v[c] = c < cin ? __ldg(px + c) : 0.f;
+  }
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
+  for (int j = 0; j < CIN; ++j) {
     float acc = 0.f;
     if (j < cin) {
       if (use_head) {
-        acc = hb[j];
+        acc = __ldg(hb + j);
 #pragma unroll
-        for (int c = 0; c < 16; ++c)
-          if (c < cin) acc = fmaf(v[c], hw[c * cin + j], acc);
+        for (int c = 0; c < CIN; ++c)
+          if (c < cin) acc = fmaf(v[c], __ldg(hw + c * cin + j), acc);
       } else {
         acc = v[j];
       }
@@ -82,37 +90,38 @@ __global__ void __launch_bounds__(256)
   for (int c8 = 0; c8 < 16; c8 += 8) {
     if (c8 >= cp) break;
     uint4 pk;
-    uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
 #pragma unroll
     for (int e = 0; e < 8; e += 2) {
-      const float a0 = (c8 + e < 16) ? hv[(c8 + e) & 15] : 0.f;
-      const float a1 = (c8 + e + 1 < 16) ? hv[(c8 + e + 1) & 15] : 0.f;
+      const float a0 = (c8 + e < CIN) ? hv[(c8 + e) % CIN] : 0.f;
+      const float a1 = (c8 + e + 1 < CIN) ? hv[(c8 + e + 1) % CIN] : 0.f;
       __nv_bfloat162 h2 = __floats2bfloat162_rn(a0, a1);
-      pw[e / 2] = *reinterpret_cast<uint32_t*>(&h2);
+      (&pk.x)[e / 2] = *reinterpret_cast<uint32_t*>(&h2);
     }
     *reinterpret_cast<uint4*>(o0 + c8) = pk;
   }
   __syncthreads();
   // levels 1..L-1: 2x2 averages in f32, in place in shared memory
   int side = T;
-  for (int k = 1; k < levels; ++k) {
+#pragma unroll
+  for (int k = 1; k < 5; ++k) {  // unrolled: out.lvl[k] stays a parameter (no local copy)
+    if (k >= levels) break;
     const int ns = side >> 1;
-    float m[16];
+    float m[CIN];
     const bool act = t < ns * ns;
     const int qy = act ? t / ns : 0, qx = act ? t % ns : 0;
 #pragma unroll
-    for (int c = 0; c < 16; ++c) m[c] = 0.f;
+    for (int c = 0; c < CIN; ++c) m[c] = 0.f;
     if (act) {
       const float* a0 = tile + ((2 * qy) * side + 2 * qx) * cin;
 #pragma unroll
-      for (int c = 0; c < 16; ++c)
+      for (int c = 0; c < CIN; ++c)
         if (c < cin)
           m[c] = ((a0[c] + a0[cin + c]) + (a0[side * cin + c] + a0[side * cin + cin + c])) * 0.25f;
     }
     __syncthreads();
     if (act) {
 #pragma unroll
-      for (int c = 0; c < 16; ++c)
+      for (int c = 0; c < CIN; ++c)
         if (c < cin) tile[t * cin + c] = m[c];
       const int Wk = W >> k;
       __nv_bfloat16* ok = out.lvl[k] + ((size_t)(ty * ns + qy) * Wk + (tx * ns + qx)) * cp;
@@ -120,13 +129,12 @@ __global__ void __launch_bounds__(256)
       for (int c8 = 0; c8 < 16; c8 += 8) {
         if (c8 >= cp) break;
         uint4 pk;
-        uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
 #pragma unroll
         for (int e = 0; e < 8; e += 2) {
           const int c = c8 + e;
-          __nv_bfloat162 h2 = __floats2bfloat162_rn(c < cin ? m[c & 15] : 0.f,
-                                                    c + 1 < cin ? m[(c + 1) & 15] : 0.f);
-          pw[e / 2] = *reinterpret_cast<uint32_t*>(&h2);
+          __nv_bfloat162 h2 = __floats2bfloat162_rn(c < CIN && c < cin ? m[c % CIN] : 0.f,
+                                                    c + 1 < CIN && c + 1 < cin ? m[(c + 1) % CIN] : 0.f);
+          (&pk.x)[e / 2] = *reinterpret_cast<uint32_t*>(&h2);
         }
         *reinterpret_cast<uint4*>(ok + c8) = pk;
       }
@@ -578,8 +586,13 @@ int nar_unet_forward(nar_unet* n, const float* in, int32_t H, int32_t W, float* 
     PyrOut po;
     for (int k = 0; k < L; ++k) po.lvl[k] = bf(p.off_pyr16[k]);
     const size_t sm = (size_t)T * T * cin * 4;
-    head_pyramid_kernel<<<dim3(W / T, H / T), T * T, sm, st>>>(
-        in, H, W, cin, p.cinp, n->d_head_w, n->d_head_b, n->cfg.use_descriptor_head, L, po);
+    if (T * T > 256) return set_error(NAR_ERR_CONFIG, "at most 5 pyramid levels supported");
+    auto kern = cin <= 4 ? head_pyramid_kernel<4>
+                         : (cin <= 8 ? head_pyramid_kernel<8> : head_pyramid_kernel<16>);
+    const bool aligned = (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+    if (cin == 4 && !aligned) kern = head_pyramid_kernel<8>;  // no float4 loads
+    kern<<<dim3(W / T, H / T), T * T, sm, st>>>(in, H, W, cin, p.cinp, n->d_head_w,
+                                               n->d_head_b, n->cfg.use_descriptor_head, L, po);
     if ((rc = check_launch("head_pyramid"))) return rc;
   }
 

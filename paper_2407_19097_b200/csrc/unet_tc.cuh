@@ -237,7 +237,7 @@ __device__ __forceinline__ float gate_b(float f, float g, float bf, float bfl, f
 // ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
-template <int N>
+template <int N, bool kHead>
 __global__ void __maxnreg__(96)
     gated_conv_tc(const ConvArgs a, const __grid_constant__ CUtensorMap tma_a,
                   const __grid_constant__ CUtensorMap tma_b) {
@@ -440,8 +440,9 @@ __global__ void __maxnreg__(96)
     const int quarter = warp & 3;
     const int grp = (warp - kProdWarps) >> 2;
     const int m = quarter * 32 + lane;
-    const bool do_pool = a.pool_out != nullptr;  // requires R even (host-checked)
-    const bool do_head = a.head_out != nullptr;
+    // kHead (the last layer): fused 1x1 out head, never pooled (host-checked)
+    const bool do_pool = !kHead && a.pool_out != nullptr;  // requires R even (host-checked)
+    constexpr bool do_head = kHead;
     const int rstep = do_pool ? 2 : 1;
     constexpr int RPW = R >= kEpiGroups ? R / kEpiGroups : 1;  // rows per warp, upper bound
     const int nc8 = a.cout_stride / 8;
@@ -454,7 +455,7 @@ __global__ void __maxnreg__(96)
       tc_fence_after();
       const int x = x0 + m;
       const bool xok = x < a.W;
-      float logit[RPW][4];
+      float logit[kHead ? RPW : 1][4];
       if (do_head) {
 #pragma unroll
         for (int i = 0; i < RPW; ++i)
@@ -472,9 +473,13 @@ __global__ void __maxnreg__(96)
           bflv[e] = sbias_fl[c0 + e];
           bghv[e] = sbias_gh[c0 + e];
         }
-        int slot = 0;
-#pragma unroll 1
-        for (int r = grp * rstep; r < R; r += kEpiGroups * rstep, slot += rstep) {
+        // rows of this warp: r = grp*rstep + i*4*rstep; unrolled so `slot`
+        // (the logit row) is a compile-time index (registers, not local memory)
+#pragma unroll
+        for (int i = 0; i < RPW; ++i) {
+          const int r = grp * rstep + i * kEpiGroups * rstep;
+          const int slot = i * rstep;
+          if (r >= R || slot >= RPW) break;
           float o[2][8];
           float f[2][8], g[2][8];
 #pragma unroll
@@ -514,8 +519,8 @@ __global__ void __maxnreg__(96)
 #pragma unroll
                   for (int k = 0; k < 4; ++k)
                     if (k < a.head_n)
-                      logit[slot + h][k] =
-                          fmaf(o[h][e], shead_w[(c0 + e) * a.head_n + k], logit[slot + h][k]);
+                      logit[kHead ? i : 0][k] =
+                          fmaf(o[h][e], shead_w[(c0 + e) * a.head_n + k], logit[kHead ? i : 0][k]);
             }
           }
           if (do_pool) {
@@ -543,9 +548,11 @@ __global__ void __maxnreg__(96)
         }
       }
       if (do_head) {
-        int slot = 0;
-#pragma unroll 1
-        for (int r = grp * rstep; r < R; r += kEpiGroups * rstep, slot += rstep) {
+#pragma unroll
+        for (int i = 0; i < RPW; ++i) {
+          const int r = grp * rstep + i * kEpiGroups * rstep;
+          const int slot = i * rstep;
+          if (r >= R || slot >= RPW) break;
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             if (h == 1 && !do_pool) break;
@@ -554,7 +561,9 @@ __global__ void __maxnreg__(96)
               float* dst = a.head_out + ((size_t)y * a.W + x) * a.head_n;
 #pragma unroll
               for (int k = 0; k < 4; ++k)
-                if (k < a.head_n) dst[k] = 1.0f / (1.0f + __expf(-(logit[slot + h][k] + shead_b[k])));
+                if (k < a.head_n)
+                  dst[k] = fmaf(0.5f, tanh_approx(0.5f * (logit[kHead ? i : 0][k] + shead_b[k])),
+                                0.5f);  // sigmoid
             }
           }
         }
@@ -606,12 +615,12 @@ static int tc_make_map(CUtensorMap* m, const void* base, int cs, int w, int h, i
   return NAR_OK;
 }
 
-template <int N>
-static int tc_launch_n(const ConvArgs& a, cudaStream_t st) {
+template <int N, bool kHead>
+static int tc_launch_nh(const ConvArgs& a, cudaStream_t st) {
   static bool attr_done = false;
   if (!attr_done) {
     const cudaError_t e = cudaFuncSetAttribute(
-        gated_conv_tc<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem(N));
+        gated_conv_tc<N, kHead>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem(N));
     if (e != cudaSuccess) {
       char msg[160];
       snprintf(msg, sizeof(msg), "cannot set conv smem size %d: %s", tc_smem(N),
@@ -640,8 +649,19 @@ static int tc_launch_n(const ConvArgs& a, cudaStream_t st) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int tiles = ((a.W + 127) / 128) * ((a.H + R - 1) / R);
   const int grid = tiles < sms ? tiles : sms;
-  gated_conv_tc<N><<<grid, kTcThreads, tc_smem(N), st>>>(a, ma, mb);
+  gated_conv_tc<N, kHead><<<grid, kTcThreads, tc_smem(N), st>>>(a, ma, mb);
   return check_launch("gated_conv_tc");
+}
+
+template <int N>
+static int tc_launch_n(const ConvArgs& a, cudaStream_t st) {
+  if (!a.head_out) return tc_launch_nh<N, false>(a, st);
+  if constexpr (N <= 64) {
+    if (a.pool_out) return set_error(NAR_ERR_CONFIG, "fused out head cannot be pooled");
+    return tc_launch_nh<N, true>(a, st);
+  } else {
+    return set_error(NAR_ERR_CONFIG, "fused out head needs a layer of <= 32 channels");
+  }
 }
 
 inline int tc_rows_for(int cout) { return tc_rows(2 * ((cout + 7) / 8 * 8)); }
