@@ -251,6 +251,14 @@ __device__ __forceinline__ void fold_key(uint64_t* keybuf, uint32_t pix, uint64_
   }
 }
 
+template <bool kSigned>
+__device__ __forceinline__ void red_key(uint64_t* keybuf, uint32_t pix, uint64_t key) {
+  if (kSigned)
+    atomicMin(reinterpret_cast<long long*>(keybuf) + pix, (long long)(key ^ NAR_SIGN_FLIP));
+  else
+    atomicMin(reinterpret_cast<unsigned long long*>(keybuf) + pix, (unsigned long long)key);
+}
+
 // Atomic half of fold_key, given a previously loaded current value.
 template <bool kSigned>
 __device__ __forceinline__ void fold_loaded(uint64_t* keybuf, uint32_t pix, uint64_t key,
@@ -341,7 +349,7 @@ __device__ __forceinline__ void flush_queue(const QEntry* q, int n, int lane, ui
 // (4) fold the PREVIOUS chunk's survivors, whose keybuf reads were issued one
 //     step ago, so the random-L2 read latency overlaps a chunk of math;
 // (5) issue this chunk's keybuf reads.
-template <bool kSigned>
+template <bool kSigned, bool kRed>
 __global__ void __launch_bounds__(kRenderThreads, 1)
     render_tma_kernel(uint64_t* __restrict__ keybuf, const float* __restrict__ pos,
                       const ChunkMap cm, uint64_t base_index, const DevCam cam, const HizArgs hz) {
@@ -459,6 +467,12 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
         }
       }
     }
+    if (kRed) {  // seed pass: the keybuf is still mostly empty, early-z would not filter
+#pragma unroll
+      for (int j = 0; j < kPtsPerThread; ++j)
+        if ((okmask >> j) & 1u) red_key<kSigned>(keybuf, pix[j], key[j]);
+      continue;
+    }
     // (4) + (5)
 #pragma unroll
     for (int j = 0; j < kPtsPerThread; ++j)
@@ -497,6 +511,11 @@ constexpr int kPreSmem =
     kPreRingBytes + kCandBytes + kHizMaxEntries * 2 + kRenderWarps * kPreStages * 8 + 128;
 static_assert(kPreSmem <= 227 * 1024, "pre-test kernel smem");
 
+// Exact path for one queued candidate.  Certain hits go straight to a
+// fire-and-forget atomicMin (RED): the candidates already passed the Hi-Z
+// test, so an early-z read of the keybuf would mostly confirm them and only
+// stall the warp for the L2 round trip.  Uncertain snaps (~1e-6 of points)
+// take the exact f64 path.
 template <bool kSigned>
 __device__ __forceinline__ void exact_candidate(const QEntry e, uint64_t* keybuf,
                                                 const DevCam& cam) {
@@ -504,11 +523,11 @@ __device__ __forceinline__ void exact_candidate(const QEntry e, uint64_t* keybuf
   bool hit, unc;
   project_fast(e.x, e.y, e.z, cam, ix, iy, db, hit, unc);
   if (hit) {
-    fold_key<kSigned>(keybuf, iy * (uint32_t)cam.w + ix, ((uint64_t)db << 32) | e.idx);
+    red_key<kSigned>(keybuf, iy * (uint32_t)cam.w + ix, ((uint64_t)db << 32) | e.idx);
   } else if (unc) {
     uint32_t pix;
     if (project_point(e.x, e.y, e.z, cam, pix, db))
-      fold_key<kSigned>(keybuf, pix, ((uint64_t)db << 32) | e.idx);
+      red_key<kSigned>(keybuf, pix, ((uint64_t)db << 32) | e.idx);
   }
 }
 
@@ -866,7 +885,6 @@ __global__ void __launch_bounds__(256)
 // host side
 // ----------------------------------------------------------------------------
 static int g_num_sms = 0;
-static int g_render_blocks_per_sm = 0;
 static std::once_flag g_init_once;
 static bool g_no_pre = false;  // NAR_RENDER_NO_PRETEST=1: exact-path-only Hi-Z passes
 
@@ -876,17 +894,20 @@ static int device_init() {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) { err = 1; return; }
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(render_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kRenderSmem);
-    cudaFuncSetAttribute(render_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kRenderSmem);
+    cudaFuncSetAttribute(render_tma_kernel<false, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, kRenderSmem);
+    cudaFuncSetAttribute(render_tma_kernel<true, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, kRenderSmem);
+    cudaFuncSetAttribute(render_tma_kernel<false, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, kRenderSmem);
+    cudaFuncSetAttribute(render_tma_kernel<true, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, kRenderSmem);
     cudaFuncSetAttribute(render_pre_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kPreSmem);
     cudaFuncSetAttribute(render_pre_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kPreSmem);
     const char* np = getenv("NAR_RENDER_NO_PRETEST");
     g_no_pre = np && np[0] == '1';
-    g_render_blocks_per_sm = 1;
   });
   if (err || g_num_sms == 0) return set_error(NAR_ERR_CUDA, "no CUDA device");
   return NAR_OK;
@@ -917,7 +938,8 @@ static int launch_render(uint64_t* keybuf, const float* pos, int64_t n, uint64_t
     const int64_t n_tiles = n / kTilePts;
     if (n_tiles > 0) {
       const int64_t sms = g_num_sms;
-      auto kern = sgn ? render_tma_kernel<true> : render_tma_kernel<false>;
+      auto kern = sgn ? render_tma_kernel<true, false> : render_tma_kernel<false, false>;
+      auto kseed = sgn ? render_tma_kernel<true, true> : render_tma_kernel<false, true>;
       auto kpre = sgn ? render_pre_kernel<true> : render_pre_kernel<false>;
       const bool pre = cam.pre && !g_no_pre;
       auto run = [&](ChunkMap cm, bool with_hiz) {
@@ -932,6 +954,8 @@ static int launch_render(uint64_t* keybuf, const float* pos, int64_t n, uint64_t
         if (grid <= 0) return;
         if (with_hiz && pre)
           kpre<<<grid, kRenderThreads, kPreSmem, st>>>(keybuf, pos, cm, base, cam, hz);
+        else if (cm.mode == 1 && !with_hiz)
+          kseed<<<grid, kRenderThreads, kRenderSmem, st>>>(keybuf, pos, cm, base, cam, hz);
         else
           kern<<<grid, kRenderThreads, kRenderSmem, st>>>(keybuf, pos, cm, base, cam, hz);
       };
