@@ -301,7 +301,7 @@ constexpr int kTilePts = kUnitPts;
 // the cloud by mode 0: j; 1 (Hi-Z seed pass): j*S; 2 (the rest):
 // j + j/(S-1) + 1, i.e. every unit that is not a multiple of S.  The exact
 // kernel walks 64-point halves of the units (chunk c = slot c/2, half c%2).
-constexpr int kHizSeedStride = 16;  // S
+constexpr int kHizSeedStride = 24;  // S
 struct ChunkMap {
   int64_t j0, j1;  // unit slots (< 2^25: point indices are 32-bit)
   int32_t mode;
