@@ -405,7 +405,12 @@ static int run_conv(nar_unet* n, Layer& l, const __nv_bfloat16* src_a, int ca_st
     a.head_w = n->d_out_w;
     a.head_b = n->d_out_b;
     a.head_n = n->cfg.output_channels;
-    if (a.head_n > 4) {  // beyond the fused epilogue's register budget
+    for (int c = 0; c < 32; ++c)
+      for (int k = 0; k < 4; ++k)
+        a.head_wv[c * 4 + k] =
+            (c < l.cout && k < a.head_n) ? n->out_w[(size_t)c * a.head_n + k] : 0.0f;
+    for (int k = 0; k < 4; ++k) a.head_bv[k] = k < a.head_n ? n->out_b[k] : 0.0f;
+    if (a.head_n > 4 || l.cout > 32) {  // beyond the fused epilogue's budget
       a.head_out = nullptr;
       if (!a.out) a.out = scratch;
     }

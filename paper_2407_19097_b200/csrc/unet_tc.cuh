@@ -59,6 +59,10 @@ struct ConvArgs {
   const float* head_b;
   float* head_out;             // (H, W, head_n) f32
   int head_n;
+  // the same head weights by value (kernel-parameter constant bank): [c][4] and [4],
+  // zero padded, so the fused head's FMAs take constant operands (cout <= 32)
+  float head_wv[32 * 4];
+  float head_bv[4];
 };
 
 constexpr int kProdWarps = 2;   // TMA issue + staging reshape
@@ -462,8 +466,12 @@ __global__ void __maxnreg__(96)
 #pragma unroll
           for (int k = 0; k < 4; ++k) logit[i][k] = 0.0f;
       }
-#pragma unroll 1
-      for (int c8 = 0; c8 < nc8; ++c8) {
+      // kHead: channel chunks unrolled (<= 4) so head weights index the
+      // parameter bank with compile-time offsets
+      constexpr int NC8_HEAD = 2 * ((COUTP + 15) / 16);
+#pragma unroll
+      for (int c8 = 0; c8 < (kHead ? NC8_HEAD : 1 << 20); ++c8) {
+        if (c8 >= nc8) break;
         const int c0 = c8 * 8;
         const bool have = c0 < COUTP;
         float bfv[8], bflv[8], bghv[8];
@@ -520,7 +528,7 @@ __global__ void __maxnreg__(96)
                   for (int k = 0; k < 4; ++k)
                     if (k < a.head_n)
                       logit[kHead ? i : 0][k] =
-                          fmaf(o[h][e], shead_w[(c0 + e) * a.head_n + k], logit[kHead ? i : 0][k]);
+                          fmaf(o[h][e], a.head_wv[((c0 + e) & 31) * 4 + k], logit[kHead ? i : 0][k]);
             }
           }
           if (do_pool) {
@@ -562,7 +570,7 @@ __global__ void __maxnreg__(96)
 #pragma unroll
               for (int k = 0; k < 4; ++k)
                 if (k < a.head_n)
-                  dst[k] = fmaf(0.5f, tanh_approx(0.5f * (logit[kHead ? i : 0][k] + shead_b[k])),
+                  dst[k] = fmaf(0.5f, tanh_approx(0.5f * (logit[kHead ? i : 0][k] + a.head_bv[k])),
                                 0.5f);  // sigmoid
             }
           }
