@@ -115,3 +115,41 @@ def test_signed_domain_preserves_order():
     assert np.array_equal(np.argsort(k, kind="stable"), np.argsort(s, kind="stable"))
     assert np.array_equal(parallel.from_signed(s), k)
     assert s[-2] == parallel.EMPTY_SIGNED
+
+
+def _nccl_worker(port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        from paper_2407_19097_b200.msr import DeviceCloud, Renderer
+        from paper_2407_19097_b200.parallel import ShardedRenderer
+        from paper_2407_19097_b200.msr import StreamSelection
+
+        torch.cuda.set_device(0)
+        pc, cam = _scene()
+        i = cam.intrinsics
+        cloud = DeviceCloud.from_host(pc)
+        sel = StreamSelection(rgb=True, depth=True, vel2d=True, vel3d=True, velocity_scale=1.5)
+        sr = ShardedRenderer(i.width, i.height)
+        img = sr.frame(cloud, cam, sel)
+        ref = Renderer(i.width, i.height).rasterize(cloud, cam, sel)
+        q.put((img.data.cpu().numpy(), ref.data.cpu().numpy(),
+               img.index_plane.cpu().numpy(), ref.index_plane.cpu().numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_nccl_single_rank_sharded_frame(cuda):
+    """The NCCL path on the GPU (signed key domain render, int64 MIN all-reduce,
+    owner-only resolve, int32 SUM reduce) with one rank equals the plain frame."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_worker, args=(_free_port(), q))
+    p.start()
+    got, ref, gi, ri = q.get(timeout=300)
+    p.join(timeout=60)
+    assert p.exitcode == 0
+    assert np.array_equal(gi, ri)
+    assert np.array_equal(got.view(np.int32), ref.view(np.int32))
