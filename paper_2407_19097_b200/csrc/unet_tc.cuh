@@ -91,15 +91,25 @@ __host__ __device__ constexpr int tc_stages(int N) {
              : (200 * 1024 - 2 * tc_stg_bytes(N)) / tc_stage_bytes(N);
 }
 constexpr int kTcParamFloats = 3 * 144 + 128 * 4 + 4;  // bias_f, bias_f*log2e, bias_g/2, head_w, head_b
+// Narrow layers (N <= 48) use "sliding" MMAs: one MMA per (halo row, kx) with
+// the three ky weight blocks stacked along N (N' = 3N) accumulates into three
+// consecutive output rows at once -- (R+2)*3 MMAs per chunk instead of 9*R,
+// which matters because an M=128, K=16 MMA costs ~55 cycles for any N <= 64.
+// Accumulators are zeroed first by one MMA with zero operands (kTcZeroBytes).
+__host__ __device__ constexpr bool tc_slide(int N) { return N <= 48; }
+constexpr int kTcZeroBytes = 256 * 32;  // B: 256 rows x K16 bf16 (A uses its first 4 KB)
 __host__ __device__ constexpr int tc_smem(int N) {
-  return tc_stages(N) * tc_stage_bytes(N) + 2 * tc_stg_bytes(N) + 512 + kTcParamFloats * 4;
+  return tc_stages(N) * tc_stage_bytes(N) + 2 * tc_stg_bytes(N) + 512 + kTcParamFloats * 4 +
+         (tc_slide(N) ? kTcZeroBytes : 0);
 }
 
 // Host: pack HWIO f32 weights into bf16 [chunk q][tap][k8][n][8] where
 // n < Coutp indexes f outputs and n >= Coutp g outputs (zero padded).
+// Sliding layers (tc_slide(N)): [chunk q][kx][k8][n' = (2 - ky) * N + n][8].
 inline void tc_pack_weights(const std::vector<float>& wf, const std::vector<float>& wg, int ca,
                             int cb, int cout, std::vector<uint16_t>& packed) {
   const int coutp = (cout + 7) / 8 * 8, N = 2 * coutp;
+  const bool slide = tc_slide(N);
   const int nqa = (ca + 15) / 16, nqb = (cb + 15) / 16, nq = nqa + nqb, cin = ca + cb;
   packed.assign((size_t)nq * 9 * 2 * N * 8, 0);
   auto bf16 = [](float v) -> uint16_t {
@@ -122,7 +132,13 @@ inline void tc_pack_weights(const std::vector<float>& wf, const std::vector<floa
             const int j = is_g ? n - coutp : n;
             if (j >= cout) continue;
             const float v = (is_g ? wg : wf)[((size_t)tap * cin + ci) * cout + j];
-            packed[((((size_t)q * 9 + tap) * 2 + k8) * N + n) * 8 + e] = bf16(v);
+            if (slide) {
+              const int ky = tap / 3, kx = tap % 3;
+              const size_t np = (size_t)(2 - ky) * N + n;
+              packed[((((size_t)q * 3 + kx) * 2 + k8) * (3 * N) + np) * 8 + e] = bf16(v);
+            } else {
+              packed[((((size_t)q * 9 + tap) * 2 + k8) * N + n) * 8 + e] = bf16(v);
+            }
           }
 }
 
@@ -274,6 +290,8 @@ __global__ void __maxnreg__(96)
   float* sbias_gh = sbias_fl + 144;
   float* shead_w = sbias_gh + 144;
   float* shead_b = shead_w + 512;
+  constexpr bool SLIDE = tc_slide(N);
+  uint8_t* szero = reinterpret_cast<uint8_t*>(sbias_f + kTcParamFloats);  // SLIDE only
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles_x = (a.W + 127) / 128;
@@ -302,6 +320,11 @@ __global__ void __maxnreg__(96)
     sbias_f[i] = bf;
     sbias_fl[i] = bf * 1.44269504088896341f;
     sbias_gh[i] = 0.5f * bg;
+  }
+  if (SLIDE) {
+    for (int i = threadIdx.x; i < kTcZeroBytes / 16; i += kTcThreads)
+      reinterpret_cast<uint4*>(szero)[i] = make_uint4(0u, 0u, 0u, 0u);
+    fence_proxy_async_smem();  // generic-proxy zeros, read by the tensor core
   }
   if (a.head_out)
     for (int i = threadIdx.x; i < a.cout * a.head_n; i += kTcThreads) shead_w[i] = a.head_w[i];
@@ -418,15 +441,37 @@ __global__ void __maxnreg__(96)
         if (lane == 0) {
           const uint32_t sa = smem_u32(smem + s * STAGE);
           const uint32_t sb = sa + A_BYTES;
+          if constexpr (SLIDE) {
+            if (q == 0) {  // zero this tile's R*N accumulator columns
+              const uint32_t z = smem_u32(szero);
+              umma_bf16(dcol, umma_desc(z, 2048, 128), umma_desc(z, R * N * 16, 128),
+                        umma_idesc_bf16(128, R * N), 0u);
+            }
 #pragma unroll 1
-          for (int tap = 0; tap < 9; ++tap) {
-            const int ky = tap / 3, kx = tap % 3;
-            const uint64_t bdesc = umma_desc(sb + tap * (N * 32), N * 16, 128);
+            for (int kx = 0; kx < 3; ++kx) {
+              const uint32_t bk = sb + kx * (3 * N * 32);  // [k8][3N][8]: LBO = 3N*16
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-              const uint64_t adesc =
-                  umma_desc(sa + (r + ky) * kHaloRowBytes + kx * 16, SLAB, 128);
-              umma_bf16(dcol + r * N, adesc, bdesc, IDESC, (q > 0 || tap > 0) ? 1u : 0u);
+              for (int h = 0; h < R + 2; ++h) {
+                // output rows r = h - ky for ky in [kymin, kymax]; blocks ordered ky = 2, 1, 0
+                const int kymax = h < 2 ? h : 2;
+                const int kymin = h - (R - 1) > 0 ? h - (R - 1) : 0;
+                const int nb = kymax - kymin + 1;
+                const uint64_t bdesc = umma_desc(bk + (2 - kymax) * N * 16, 3 * N * 16, 128);
+                const uint64_t adesc = umma_desc(sa + h * kHaloRowBytes + kx * 16, SLAB, 128);
+                umma_bf16(dcol + (h - kymax) * N, adesc, bdesc, umma_idesc_bf16(128, nb * N), 1u);
+              }
+            }
+          } else {
+#pragma unroll 1
+            for (int tap = 0; tap < 9; ++tap) {
+              const int ky = tap / 3, kx = tap % 3;
+              const uint64_t bdesc = umma_desc(sb + tap * (N * 32), N * 16, 128);
+#pragma unroll
+              for (int r = 0; r < R; ++r) {
+                const uint64_t adesc =
+                    umma_desc(sa + (r + ky) * kHaloRowBytes + kx * 16, SLAB, 128);
+                umma_bf16(dcol + r * N, adesc, bdesc, IDESC, (q > 0 || tap > 0) ? 1u : 0u);
+              }
             }
           }
           umma_commit(&empty[s]);
