@@ -96,7 +96,7 @@ constexpr int kTcParamFloats = 3 * 144 + 128 * 4 + 4;  // bias_f, bias_f*log2e, 
 // consecutive output rows at once -- (R+2)*3 MMAs per chunk instead of 9*R,
 // which matters because an M=128, K=16 MMA costs ~55 cycles for any N <= 64.
 // Accumulators are zeroed first by one MMA with zero operands (kTcZeroBytes).
-__host__ __device__ constexpr bool tc_slide(int N) { return N <= 48; }
+__host__ __device__ constexpr bool tc_slide(int N) { return N <= 64; }
 constexpr int kTcZeroBytes = 256 * 32;  // B: 256 rows x K16 bf16 (A uses its first 4 KB)
 __host__ __device__ constexpr int tc_smem(int N) {
   return tc_stages(N) * tc_stage_bytes(N) + 2 * tc_stg_bytes(N) + 512 + kTcParamFloats * 4 +
