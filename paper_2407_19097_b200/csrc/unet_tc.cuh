@@ -406,18 +406,41 @@ __global__ void __maxnreg__(96)
       mbar_wait(&stg[u & 1], (uint32_t)(u >> 1) & 1u);
       {
         // 2x2 replication: halo (row, j) <- low-res (ly, lx)
+        // fully unrolled: all loads of a row pair in flight before the stores
         const int ly0 = (y0 - 1) >> 1, lx0 = (x0 - 1) >> 1;
-#pragma unroll 1
-        for (int row = 0; row < R + 2; ++row) {
-          const int ly = ((y0 - 1 + row) >> 1) - ly0;
-          const uint8_t* srow = buf + ly * (kLowPx * 32);
-          uint8_t* d0 = stA + row * kHaloRowBytes;
-          for (int j = t; j < kHaloPx; j += kProdThreads) {
-            const int lx = ((x0 - 1 + j) >> 1) - lx0;
-            const uint4 v0 = *reinterpret_cast<const uint4*>(srow + lx * 32);
-            const uint4 v1 = *reinterpret_cast<const uint4*>(srow + lx * 32 + 16);
-            *reinterpret_cast<uint4*>(d0 + j * 16) = v0;
-            *reinterpret_cast<uint4*>(d0 + SLAB + j * 16) = v1;
+        constexpr int JIT = (kHaloPx + kProdThreads - 1) / kProdThreads;
+        int lxs[JIT];
+#pragma unroll
+        for (int i = 0; i < JIT; ++i) {
+          const int j = t + i * kProdThreads;
+          lxs[i] = ((x0 - 1 + (j < kHaloPx ? j : 0)) >> 1) - lx0;
+        }
+#pragma unroll
+        for (int row = 0; row < R + 2; row += 2) {
+          uint4 v[2][JIT][2];
+#pragma unroll
+          for (int rr = 0; rr < 2; ++rr) {
+            const int ly = ((y0 - 1 + row + rr) >> 1) - ly0;
+            const uint8_t* srow = buf + ly * (kLowPx * 32);
+#pragma unroll
+            for (int i = 0; i < JIT; ++i) {
+              if (row + rr < R + 2 && t + i * kProdThreads < kHaloPx) {
+                v[rr][i][0] = *reinterpret_cast<const uint4*>(srow + lxs[i] * 32);
+                v[rr][i][1] = *reinterpret_cast<const uint4*>(srow + lxs[i] * 32 + 16);
+              }
+            }
+          }
+#pragma unroll
+          for (int rr = 0; rr < 2; ++rr) {
+            uint8_t* d0 = stA + (row + rr) * kHaloRowBytes;
+#pragma unroll
+            for (int i = 0; i < JIT; ++i) {
+              const int j = t + i * kProdThreads;
+              if (row + rr < R + 2 && j < kHaloPx) {
+                *reinterpret_cast<uint4*>(d0 + j * 16) = v[rr][i][0];
+                *reinterpret_cast<uint4*>(d0 + SLAB + j * 16) = v[rr][i][1];
+              }
+            }
           }
         }
       }
