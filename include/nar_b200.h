@@ -68,6 +68,8 @@ typedef struct nar_camera {
 const char* nar_version(void);
 const char* nar_last_error(void);
 int nar_device_count(int32_t* count);
+/* Number of kernels this library has launched so far (process-wide). */
+uint64_t nar_launch_count(void);
 /* Host memory helpers (pinned allocations make H2D copies true async DMA). */
 int nar_host_alloc(void** ptr, size_t bytes);
 int nar_host_free(void* ptr);

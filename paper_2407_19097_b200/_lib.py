@@ -107,6 +107,7 @@ SIGNATURES = {
     "nar_device_count": (C.c_int, [C.POINTER(C.c_int32)]),
     "nar_host_alloc": (C.c_int, [C.POINTER(C.c_void_p), C.c_size_t]),
     "nar_host_free": (C.c_int, [_vp]),
+    "nar_launch_count": (C.c_uint64, []),
     "nar_host_mapped_pointer": (C.c_int, [_vp, C.POINTER(C.c_void_p)]),
     "nar_zbuffer_accumulate": (
         C.c_int,
@@ -219,3 +220,9 @@ def mapped_pointer(host_ptr: int):
     if load().nar_host_mapped_pointer(C.c_void_p(host_ptr), C.byref(out)) != 0:
         return None
     return out.value
+
+
+def launch_count() -> int:
+    """Kernels launched by libnar_b200 so far (bench.py's gpu_launches)."""
+    return int(load().nar_launch_count())
+

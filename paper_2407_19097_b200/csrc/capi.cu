@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdio.h>
 
+#include <atomic>
 #include <string>
 
 #include "common.cuh"
@@ -24,6 +25,10 @@ int check_launch(const char* what) {
   std::string m = std::string(what) + ": " + cudaGetErrorString(e);
   return set_error(NAR_ERR_CUDA, m.c_str());
 }
+
+static std::atomic<uint64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+uint64_t launch_total() { return g_launches.load(std::memory_order_relaxed); }
 
 }  // namespace nar
 
@@ -62,6 +67,8 @@ int nar_host_free(void* ptr) {
   }
   return NAR_OK;
 }
+
+uint64_t nar_launch_count(void) { return nar::launch_total(); }
 
 int nar_host_mapped_pointer(const void* host, void** dev) {
   if (!host || !dev) return nar::set_error(NAR_ERR_INVALID, "NULL argument");

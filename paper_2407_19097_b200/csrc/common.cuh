@@ -12,6 +12,9 @@ namespace nar {
 int set_error(int code, const char* msg);
 // Converts a pending launch error into a status.
 int check_launch(const char* what);
+// every kernel launch of the library is counted (nar_launch_count)
+void count_launch();
+uint64_t launch_total();
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

@@ -60,6 +60,7 @@ extern "C" int nar_morton_keys(const float* positions_dev, int64_t n, const doub
   }
   int64_t blocks = (n + 255) / 256;
   if (blocks > 148 * 32) blocks = 148 * 32;
+  nar::count_launch();
   nar::morton_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(positions_dev, n, b,
                                                                         keys_dev);
   return nar::check_launch("morton_keys");

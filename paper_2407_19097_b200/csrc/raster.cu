@@ -929,10 +929,13 @@ static int launch_render(uint64_t* keybuf, const float* pos, int64_t n, uint64_t
   auto refresh = [&]() {
     const int64_t nt = ((int64_t)zw * zh) << shift;
     const unsigned g = (unsigned)((nt + 255) / 256);
-    if (sgn)
+    if (sgn) {
+      nar::count_launch();
       hiz_kernel<true><<<g, 256, 0, st>>>(keybuf, cam.w, cam.h, shift, zw, zh, zmax);
-    else
+    } else {
+      nar::count_launch();
       hiz_kernel<false><<<g, 256, 0, st>>>(keybuf, cam.w, cam.h, shift, zw, zh, zmax);
+    }
   };
   if ((reinterpret_cast<uintptr_t>(pos) & 15) == 0) {
     const int64_t n_tiles = n / kTilePts;
@@ -952,12 +955,16 @@ static int launch_render(uint64_t* keybuf, const float* pos, int64_t n, uint64_t
         const int64_t need = (nj + kRenderWarps - 1) / kRenderWarps;
         const int grid = (int)(need < sms ? need : sms);
         if (grid <= 0) return;
-        if (with_hiz && pre)
+        if (with_hiz && pre) {
+          nar::count_launch();
           kpre<<<grid, kRenderThreads, kPreSmem, st>>>(keybuf, pos, cm, base, cam, hz);
-        else if (cm.mode == 1 && !with_hiz)
+        } else if (cm.mode == 1 && !with_hiz) {
+          nar::count_launch();
           kseed<<<grid, kRenderThreads, kRenderSmem, st>>>(keybuf, pos, cm, base, cam, hz);
-        else
+        } else {
+          nar::count_launch();
           kern<<<grid, kRenderThreads, kRenderSmem, st>>>(keybuf, pos, cm, base, cam, hz);
+        }
       };
       // Hi-Z schedule: a seed pass over every S-th chunk (spread over the whole
       // cloud, so the coarse depth covers the screen even for spatially sorted
@@ -1007,12 +1014,15 @@ static int launch_render(uint64_t* keybuf, const float* pos, int64_t n, uint64_t
     int64_t blocks = (rest + 255) / 256;
     const int64_t cap = (int64_t)(g_num_sms > 0 ? g_num_sms : 148) * 8;
     if (blocks > cap) blocks = cap;
-    if (sgn)
+    if (sgn) {
+      nar::count_launch();
       render_simple_kernel<true><<<(int)blocks, 256, 0, st>>>(keybuf, pos + 3 * done, rest,
                                                              base + (uint64_t)done, cam);
-    else
+    } else {
+      nar::count_launch();
       render_simple_kernel<false><<<(int)blocks, 256, 0, st>>>(keybuf, pos + 3 * done, rest,
                                                               base + (uint64_t)done, cam);
+    }
   }
   return check_launch("render");
 }
@@ -1120,6 +1130,7 @@ int nar_keybuf_fill(uint64_t* keybuf_dev, int64_t npix, uint64_t value, void* st
   int64_t blocks = (npix / 2 + 255) / 256;
   if (blocks < 1) blocks = 1;
   if (blocks > (int64_t)g_num_sms * 16) blocks = (int64_t)g_num_sms * 16;
+  nar::count_launch();
   fill_u64_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(keybuf_dev, npix, value);
   return check_launch("keybuf_fill");
 }
@@ -1269,6 +1280,7 @@ int nar_resolve(uint64_t* keybuf_dev, const nar_camera* cam, int32_t key_domain,
   auto kern = key_domain == NAR_KEYS_SIGNED
                   ? (rgbd ? resolve_kernel<true, true> : resolve_kernel<true, false>)
                   : (rgbd ? resolve_kernel<false, true> : resolve_kernel<false, false>);
+  nar::count_launch();
   kern<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(keybuf_dev, P);
   return check_launch("resolve");
 }

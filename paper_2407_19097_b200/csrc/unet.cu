@@ -383,16 +383,19 @@ static int run_conv(nar_unet* n, Layer& l, const __nv_bfloat16* src_a, int ca_st
   const int cst = a.cout_stride;
   auto pool_kernel = [&](const __nv_bfloat16* src) {
     const int64_t t = (int64_t)(H / 2) * (W / 2) * (cst / 8);
+    nar::count_launch();
     pool_bf16_kernel<<<(unsigned)((t + 255) / 256), 256, 0, st>>>(src, H, W, cst, pool_out);
   };
   auto head_kernel = [&](const __nv_bfloat16* src) {
     const int64_t np = (int64_t)H * W;
+    nar::count_launch();
     out_head_kernel<<<(unsigned)((np + 127) / 128), 128, 0, st>>>(
         src, np, l.cout, cst, n->d_out_w, n->d_out_b, n->cfg.output_channels, head_out);
   };
   if (n->simt) {
     if (!a.out) a.out = scratch;
     const int64_t tot = (int64_t)H * W * l.cout;
+    nar::count_launch();
     gated_conv_simt<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(a);
     if (pool_out) pool_kernel(a.out);
     if (head_out) head_kernel(a.out);
@@ -596,6 +599,7 @@ int nar_unet_forward(nar_unet* n, const float* in, int32_t H, int32_t W, float* 
                          : (cin <= 8 ? head_pyramid_kernel<8> : head_pyramid_kernel<16>);
     const bool aligned = (reinterpret_cast<uintptr_t>(in) & 15) == 0;
     if (cin == 4 && !aligned) kern = head_pyramid_kernel<8>;  // no float4 loads
+    nar::count_launch();
     kern<<<dim3(W / T, H / T), T * T, sm, st>>>(in, H, W, cin, p.cinp, n->d_head_w,
                                                n->d_head_b, n->cfg.use_descriptor_head, L, po);
     if ((rc = check_launch("head_pyramid"))) return rc;

@@ -725,6 +725,7 @@ static int tc_launch_nh(const ConvArgs& a, cudaStream_t st) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int tiles = ((a.W + 127) / 128) * ((a.H + R - 1) / R);
   const int grid = tiles < sms ? tiles : sms;
+  nar::count_launch();
   gated_conv_tc<N, kHead><<<grid, kTcThreads, tc_smem(N), st>>>(a, ma, mb);
   return check_launch("gated_conv_tc");
 }

@@ -120,5 +120,5 @@ if __name__ == "__main__":
     tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
     PROF.mkdir(exist_ok=True)
     launches(tag)
-    full(tag, "render", "render_tma_kernel, one Hi-Z pass of the C2 frame (~55M points)")
+    full(tag, "render", "render_pre_kernel, the last (largest) pre-test pass of a C2 frame")
     full(tag, "conv", "gated_conv_tc<32> (enc0b, level 0, 1920x1088x16 -> 16)")
