@@ -61,7 +61,7 @@ def launches(tag):
             rt_bytes += (k.get("dram__bytes_read.sum") or 0) + (k.get("dram__bytes_write.sum") or 0)
         lines.append(f"| {i} | {short(k['name'])} | {t:.1f} | {100 * k['gpu__time_duration.sum'] / tot:.1f}% | {rd:.1f} | {wr:.1f} |")
     rsum = sum(k["gpu__time_duration.sum"] for k in frame if "render" in k["name"] or "hiz" in k["name"])
-    lines += ["", f"Frame total {tot / 1e3:.1f} us; render kernels (render_tma + hiz refresh) "
+    lines += ["", f"Frame total {tot / 1e3:.1f} us; render kernels (seed, pre-test passes, Hi-Z refreshes) "
               f"{rsum / 1e3:.1f} us = {100 * rsum / tot:.1f}% of the frame; their DRAM traffic "
               f"{rt_bytes / 1e9:.3f} GB per frame vs 4.200 GB algorithmic (350M x 12 B)."]
     # U-Net launches of one pipeline frame
