@@ -6,6 +6,10 @@
   with the reference's error behaviour (FormatError / CorruptError /
   CapacityError).  ``device=`` uploads the payload straight into a resident
   ``DeviceCloud`` (the positions block is already the kernel's f32 AoS layout).
+* ``save_features`` / ``load_features``: the feature-dump container of
+  pkg/src/nar/msr/feature_io.py:12-43 (u32 W, u32 H, u16 C, channel names,
+  then channel-major f32 planes); ``save_features`` also takes a device
+  G-buffer (the padded CNN input) and writes its image extent.
 * ``morton_reorder``: pkg/src/nar/geometry/morton.py:9-46 on the GPU -- keys by
   the ``nar_morton_keys`` kernel (f64 quantisation, bit-identical), then a
   stable sort; indices change exactly as the reference's ``pc.take(order)``.
@@ -154,3 +158,54 @@ def morton_reorder(cloud):
     pos_d = torch.from_numpy(np.ascontiguousarray(cloud.positions)).cuda()
     order = torch.sort(morton_keys_device(pos_d), stable=True).indices.cpu().numpy()
     return cloud.take(order)
+
+
+# ---- feature dumps (msr/feature_io.py) ---------------------------------------------
+
+def save_features(names, data, path, height: int | None = None, width: int | None = None) -> None:
+    """Write (H, W, C) f32 planes channel-major (feature_io.py:12-23).  ``data`` may
+    be a numpy array or a device tensor (e.g. a DeviceFeatureImage's padded
+    ``data``); ``height``/``width`` crop it to the image extent."""
+    if hasattr(data, "detach"):
+        data = data.detach()
+        if height is not None:
+            data = data[:height, :width]
+        planes = data.permute(2, 0, 1).contiguous().cpu().numpy()
+    else:
+        data = np.asarray(data)
+        if height is not None:
+            data = data[:height, :width]
+        planes = np.ascontiguousarray(np.moveaxis(data, 2, 0))
+    c, h, w = planes.shape
+    names = tuple(names)
+    if c != len(names):
+        raise ValueError(f"{len(names)} channel names for {c} planes")
+    head = [struct.pack("<IIH", w, h, c)]
+    for n in names:
+        nb = n.encode("utf-8")
+        head.append(struct.pack("<B", len(nb)) + nb)
+    with open(path, "wb") as f:
+        f.write(b"".join(head))
+        f.write(np.ascontiguousarray(planes, "<f4").tobytes())
+
+
+def load_features(path):
+    """(names, (H, W, C) f32) from a feature dump; CorruptError on a short header
+    or a payload of the wrong size (feature_io.py:26-43)."""
+    raw = memoryview(open(path, "rb").read())
+    if len(raw) < 10:
+        raise CorruptError("feature dump too short for header")
+    w, h, c = struct.unpack_from("<IIH", raw, 0)
+    off, names = 10, []
+    for _ in range(c):
+        if off >= len(raw):
+            raise CorruptError("feature dump truncated in the channel names")
+        n = raw[off]
+        names.append(bytes(raw[off + 1:off + 1 + n]).decode("utf-8"))
+        off += 1 + n
+    want = w * h * c * 4
+    if len(raw) - off != want:
+        raise CorruptError(f"feature dump payload is {len(raw) - off} bytes, wanted {want}")
+    planes = np.frombuffer(raw, "<f4", count=w * h * c, offset=off).reshape(c, h, w)
+    return tuple(names), np.ascontiguousarray(np.moveaxis(planes, 0, 2))
+

@@ -247,6 +247,12 @@ def main() -> None:
     pre["ckpt/x"] = x
     pre["ckpt/y_f16"] = forward(Tensor(x), {k: Tensor(v) for k, v in q.params.items()},
                                 cfg).data
+    from nar.msr.feature_io import save_features
+
+    feat = rng.normal(0, 1, (13, 21, 5)).astype(np.float32)
+    save_features(("r", "g", "b", "d", "coverage"), feat, tmp / "f.feat")
+    pre["feat/data"] = feat
+    pre["feat/file"] = np.frombuffer((tmp / "f.feat").read_bytes(), np.uint8)
     shutil.rmtree(tmp)
     np.savez_compressed(OUT / "preprocess.npz", **pre)
 

@@ -166,3 +166,20 @@ def test_selection_from_channels():
                 StreamSelection(rgb=True, depth=True, vel2d=True, coverage_channel=True),
                 StreamSelection(depth=True, vel3d=True)):
         assert selection_from_channels(sel.channel_names()) == sel
+
+
+# ---- feature dumps ---------------------------------------------------------------------
+
+def test_feature_dump_roundtrip_and_errors(pre, tmp_path):
+    names = ("r", "g", "b", "d", "coverage")
+    got_names, data = pp.load_features(_write(tmp_path, "f.feat", pre["feat/file"]))
+    assert got_names == names and np.array_equal(data, pre["feat/data"])
+    pp.save_features(names, pre["feat/data"], tmp_path / "g.feat")
+    assert (tmp_path / "g.feat").read_bytes() == bytes(pre["feat/file"])
+    raw = bytes(pre["feat/file"])
+    with pytest.raises(CorruptError):
+        pp.load_features(_write(tmp_path, "s", raw[:8]))
+    with pytest.raises(CorruptError):
+        pp.load_features(_write(tmp_path, "t", raw[:-4]))
+    with pytest.raises(ValueError):
+        pp.save_features(names[:4], pre["feat/data"], tmp_path / "x.feat")

@@ -147,3 +147,17 @@ def test_render_neural_and_bench(cuda, pre, tmp_path):
     assert np.max(np.abs(rgb - ref)) <= MAX_ABS
     med = bench(pc, cam, p, frames=5, warmup=2)
     assert med["fps"] > 0 and med["total_ms"] > 0
+
+
+def test_feature_dump_from_device(cuda, pre, tmp_path):
+    import torch
+
+    from paper_2407_19097_b200.preprocess import load_features, save_features
+
+    data = pre["feat/data"]
+    padded = torch.zeros((16, 32, 5), device=cuda)
+    padded[:13, :21] = torch.from_numpy(data).to(cuda)
+    save_features(("r", "g", "b", "d", "coverage"), padded, tmp_path / "d.feat", 13, 21)
+    assert (tmp_path / "d.feat").read_bytes() == bytes(pre["feat/file"])
+    names, back = load_features(tmp_path / "d.feat")
+    assert np.array_equal(back, data)
