@@ -1,7 +1,8 @@
 """Benchmark of the NAR hot path on B200 (BASELINE.json metric).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--workload c2|c1|c3|c4] [--no-e2e] [--no-cpu]
+                  [--workload c2|c1|c3|c4] [--no-e2e] [--no-cpu] [--no-pipeline]
+                  [--no-morton]
 
 One step = one frame of the hot path over the workload's synthetic cloud,
 resident in HBM: render (project + early-z into the u64 keybuf) + resolve to
@@ -14,8 +15,10 @@ the G-buffer to rank 0.
 Keys in the JSON line: value = whole-job points/s (Gpts/s); e2e = the same
 metric through the reference-facing API (``rasterize`` on a pinned host
 PointCloud, H2D of the points and D2H of the FeatureImage inside the timed
-region); roofline = the render kernel against measured HBM bandwidth at
-12 algorithmic bytes per point; cpu_baseline = the reference's own Cython
+region); roofline = the render passes against measured HBM bandwidth at
+12 algorithmic bytes per point; pipeline = the full NAR frame (render,
+resolve, U-Net) with the paper's stage split; morton_order = the same frame
+on the Morton-reordered cloud; cpu_baseline = the reference's own Cython
 render kernel (oracle/_ref) with its chunked thread-pool dispatch plus the
 reference resolve, on the host cores, over a bounded sample.
 """
@@ -243,10 +246,17 @@ def run_cpu_baseline(W, H, n_sample, passes=3):
     for _ in range(passes):
         reference_frame(pos, rgb, cam, threads)
     dt = (time.perf_counter() - t0) / passes
+    # single-thread figure on a tenth of the sample (T=1 and T=cores)
+    n1 = n_sample // 10
+    t0 = time.perf_counter()
+    reference_frame(pos[:n1], rgb[:n1], cam, 1)
+    dt1 = time.perf_counter() - t0
     return {"value": n_sample / dt / 1e9, "unit": "Gpts/s", "cores": threads,
             "kind": "reference" if impl == "reference" else "port",
             "sample": f"{n_sample} uniform points at {W}x{H}, RGB+D render+resolve, "
-                      f"mean of {passes} frames ({dt:.2f} s/frame)"}
+                      f"mean of {passes} frames ({dt:.2f} s/frame)",
+            "value_1_thread": n1 / dt1 / 1e9,
+            "sample_1_thread": f"{n1} points, 1 frame ({dt1:.2f} s)"}
 
 
 def main_reference(args):
@@ -469,6 +479,39 @@ def main_ours(args):
                     "frames": kp, "api": "paper_2407_19097_b200.pipeline.NeuralRenderer.frame"}
         del nr
 
+    # ---- the same frame on the Morton-ordered cloud ------------
+    morton = None
+    if world == 1 and len(cloud.segments) == 1 and not args.no_morton:
+        from paper_2407_19097_b200.preprocess import morton_reorder
+
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ea.record(main)
+        mcloud = morton_reorder(cloud)
+        eb.record(main)
+        torch.cuda.synchronize()
+        reorder_ms = ea.elapsed_time(eb)
+        km = max(3, min(args.steps, 20))
+        for _ in range(3):
+            r.render(mcloud, cam)
+            r.resolve(mcloud, cam, sel, out=out)
+        evm = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+                torch.cuda.Event(enable_timing=True)) for _ in range(km)]
+        for a_, b_, c_ in evm:
+            a_.record(main)
+            r.render(mcloud, cam)
+            b_.record(main)
+            r.resolve(mcloud, cam, sel, out=out)
+            c_.record(main)
+        torch.cuda.synchronize()
+        fm = sum(a_.elapsed_time(c_) for a_, _, c_ in evm) / km
+        rm = sum(a_.elapsed_time(b_) for a_, b_, _ in evm) / km
+        morton = {"ms_per_step": fm, "value": cloud.count / (fm * 1e-3) / 1e9, "unit": "Gpts/s",
+                  "render_ms": rm, "reorder_ms_once": reorder_ms, "steps": km,
+                  "note": "same cloud after paper_2407_19097_b200.preprocess.morton_reorder "
+                          "(GPU keys + stable sort, not in the timed region)"}
+        del mcloud
+        torch.cuda.empty_cache()
+
     cpu = None
     if not args.no_cpu and world == 1 and rank == 0:
         cpu = run_cpu_baseline(W, H, min(n_pts, 35_000_000))
@@ -497,12 +540,14 @@ def main_ours(args):
             "render_ms": render_avg,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
                          "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+                         "frac_nominal_8tbs": achieved / 8000.0,
                          "traffic": traffic, "peak_kind": peak_kind,
                          "kernel": "render passes (render_pre_kernel + seed render_tma_kernel + hiz_kernel)",
                          "bytes_per_point": BYTES_PER_POINT},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "pipeline": pipeline,
+            "morton_order": morton,
             "gpu_launches": n_launches,
             "clocks": clocks,
         }
@@ -520,6 +565,7 @@ def main():
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--points", type=int, default=0, help="override points per GPU")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-morton", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-pipeline", action="store_true")
     args = ap.parse_args()
