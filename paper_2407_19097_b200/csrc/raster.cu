@@ -305,8 +305,13 @@ constexpr int kHizSeedStride = 24;  // S
 struct ChunkMap {
   int64_t j0, j1;  // unit slots (< 2^25: point indices are 32-bit)
   int32_t mode;
+  // interleaving: slot j -> j' = period*(j >> lshift) + r0 + (j & (2^lshift - 1)), i.e.
+  // the residues [r0, r0 + 2^lshift) mod `period` of the mode's sequence, so a
+  // pass samples the whole cloud (spatially uniform also for sorted clouds)
+  uint32_t period, r0, lshift;
   __device__ __forceinline__ uint32_t unit(uint32_t j) const {
-    return mode == 0 ? j : (mode == 1 ? j * kHizSeedStride : j + j / (kHizSeedStride - 1) + 1);
+    const uint32_t jj = period * (j >> lshift) + r0 + (j & ((1u << lshift) - 1u));
+    return mode == 0 ? jj : (mode == 1 ? jj * kHizSeedStride : jj + jj / (kHizSeedStride - 1) + 1);
   }
   // first point of 64-point chunk c (c counts halves of slots)
   __device__ __forceinline__ uint32_t off64(uint32_t c) const {
@@ -979,7 +984,7 @@ static int launch_render(uint64_t* keybuf, const float* pos, int64_t n, uint64_t
       }
       if (zmax && n_tiles >= S * min_pass / 4) {
         const int64_t n_seed = (n_tiles + S - 1) / S;
-        run(ChunkMap{0, n_seed, 1}, refresh_first);
+        run(ChunkMap{0, n_seed, 1, 1, 0, 0}, refresh_first);
         const int64_t n_rest = n_tiles - n_seed;
         int64_t passes = n_rest / min_pass;
         int64_t max_passes = 4;
@@ -997,14 +1002,23 @@ static int launch_render(uint64_t* keybuf, const float* pos, int64_t n, uint64_t
           wt[p] = geo ? ((int64_t)1 << (p < 2 ? p : 2)) : 1;
           wsum += wt[p];
         }
+        // pass p takes the residues [acc, acc + wt[p]) mod wsum of the remaining units,
+        // in blocks of kB consecutive units (contiguous DRAM runs of kB * 1.5 KB)
+        const int64_t kB = 8;
+        const int64_t period = wsum * kB;
         int64_t acc = 0;
         for (int64_t p = 0; p < passes && p < 64; ++p) {
-          const int64_t a = n_rest * acc / wsum;
-          acc += wt[p];
-          run(ChunkMap{a, n_rest * acc / wsum, 2}, true);
+          uint32_t ls = 3;  // log2(kB)
+          while ((int64_t)1 << (ls + 1) <= wt[p] * kB) ++ls;
+          const int64_t len = (int64_t)1 << ls;  // weights are powers of two
+          const int64_t rem = n_rest % period;
+          const int64_t part = rem - acc < 0 ? 0 : (rem - acc > len ? len : rem - acc);
+          const int64_t slots = (n_rest / period) * len + part;
+          run(ChunkMap{0, slots, 2, (uint32_t)period, (uint32_t)acc, ls}, true);
+          acc += len;
         }
       } else {
-        run(ChunkMap{0, n_tiles, 0}, zmax && refresh_first);
+        run(ChunkMap{0, n_tiles, 0, 1, 0, 0}, zmax && refresh_first);
       }
       done = n_tiles * kTilePts;
     }
