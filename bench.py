@@ -1,7 +1,7 @@
 """Benchmark of the NAR hot path on B200 (BASELINE.json metric).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--workload c2|c1|c3|c4] [--no-e2e] [--no-cpu] [--no-pipeline]
+                  [--workload c2|c1|c3|c4|c5] [--no-e2e] [--no-cpu] [--no-pipeline]
                   [--no-morton]
 
 One step = one frame of the hot path over the workload's synthetic cloud,
@@ -47,6 +47,7 @@ WORKLOADS = {
     "c2": (350_000_000, 1920, 1080, "synthetic 350M-point cloud, single stream, 1920x1080 rasterize+resolve"),
     "c3": (400_000_000, 1920, 1080, "4 streams x 100M Lagrangian-like points, 1080p, RGB+D+Vel2D, one CUDA stream per data stream"),
     "c4": (350_000_000, 1920, 1080, "350M terrain-like points rasterized + U-Net (random init) at 1080p"),
+    "c5": (250_000_000, 3840, 2160, "C5 shard: 2B uniform points over 8 GPUs = 250M per GPU, 3840x2160 rasterize+resolve"),
 }
 
 
