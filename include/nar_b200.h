@@ -21,6 +21,10 @@
  *   nar_unet_*              <- neural/model.py:135-204 (`conv1x1_head`,
  *                              `build_pyramid`, `gated_conv`, `unet_forward`,
  *                              `forward`), neural/autodiff.py:186-288
+ *   nar_morton_keys         <- geometry/morton.py:23-37 `morton_keys`
+ *   nar_splat_blend         <- _kernels/__init__.py:97-166 `splat_blend_image`
+ *                              (native path: CSR tile binning +
+ *                              _kernels/_native.pyx:80-159 `splat_blend_tiles`)
  */
 #ifndef NAR_B200_H
 #define NAR_B200_H
@@ -120,6 +124,18 @@ int nar_render_host(uint64_t* keybuf_dev, const float* positions_host, int64_t n
  * sort by key gives the reference's morton_reorder permutation. */
 int nar_morton_keys(const float* positions_dev, int64_t n, const double* lo, const double* hi,
                     uint64_t* keys_dev, void* stream);
+
+/* ---- Gaussian splat blending (ground-truth renderer, gsplat/renderer.py) ------------
+ * Front-to-back alpha blending of n depth-sorted 2D Gaussians into rgb_out
+ * (height, width, 3) f64, all device pointers: mu (n,2), inv_abc (n,3) inverse
+ * covariance (a, b, c), boxes (n,4) int32 image-clipped (x0, x1, y0, y1), color
+ * (n,3), opacity (n,).  Splats are binned to tile_size^2 tiles and blended in
+ * id order per pixel until the transmittance drops below 1/255 (the
+ * reference's native semantics; f64, exp() within an ulp of libm).  Returns
+ * after the binning's size read-back; the blend itself is stream-ordered. */
+int nar_splat_blend(const double* mu, const double* inv_abc, const int32_t* boxes,
+                    const double* color, const double* opacity, int64_t n, int32_t width,
+                    int32_t height, int32_t tile_size, double* rgb_out, void* stream);
 
 /* ---- resolve ---------------------------------------------------------------------- */
 /* One contiguous point buffer (a "data stream" of the multi-stream config):

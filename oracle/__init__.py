@@ -15,6 +15,8 @@ Contents (each cites the reference file:line it restates):
   * init_params / forward -- numpy f32 restatement of neural/model.py:65-204 and the
     forward ops of neural/autodiff.py:186-288 (im2col + BLAS conv).
 
+  * splat_blend -- numpy restatement of the Gaussian-splat blend
+    (_kernels/python_impl.py:56-89 semantics, _native.pyx association).
   * morton_keys / morton_order -- numpy restatement of geometry/morton.py:9-46
     (21-bit f64 quantisation over the cloud AABB, magic-number bit spread,
     stable argsort).
@@ -407,3 +409,28 @@ def morton_order(positions):
     if len(positions) == 0:
         return np.zeros(0, np.int64)
     return np.argsort(morton_keys(positions), kind="stable")
+
+
+# ---- Gaussian splat blending (_kernels/python_impl.py:56-89, _native.pyx:80-159) --------
+
+MIN_TRANSMITTANCE = 1.0 / 255.0
+
+
+def splat_blend(mu, inv_abc, boxes, color, opacity, width, height):
+    """Sequential front-to-back blend, one splat at a time over its clipped box:
+    per pixel q = a dx^2 + 2 b dy dx + c dy^2, alpha = op * exp(-q/2); pixels whose
+    transmittance is below 1/255 no longer accumulate.  (H, W, 3) f64."""
+    rgb = np.zeros((height, width, 3), np.float64)
+    trans = np.ones((height, width), np.float64)
+    for i in range(len(mu)):
+        x0, x1, y0, y1 = (int(v) for v in boxes[i])
+        dx = np.arange(x0, x1 + 1, dtype=np.float64) - mu[i, 0]
+        dy = np.arange(y0, y1 + 1, dtype=np.float64) - mu[i, 1]
+        a, b, c = inv_abc[i]
+        q = a * (dx[None, :] * dx[None, :]) + (2.0 * b * dy[:, None]) * dx[None, :] + c * (dy[:, None] * dy[:, None])
+        alpha = opacity[i] * np.exp(-0.5 * q)
+        tb = trans[y0:y1 + 1, x0:x1 + 1]
+        on = tb >= MIN_TRANSMITTANCE
+        rgb[y0:y1 + 1, x0:x1 + 1] += np.where(on, alpha * tb, 0.0)[:, :, None] * color[i]
+        tb *= np.where(on, 1.0 - alpha, 1.0)
+    return rgb

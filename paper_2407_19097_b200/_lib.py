@@ -108,6 +108,7 @@ SIGNATURES = {
     "nar_host_alloc": (C.c_int, [C.POINTER(C.c_void_p), C.c_size_t]),
     "nar_host_free": (C.c_int, [_vp]),
     "nar_launch_count": (C.c_uint64, []),
+    "nar_splat_blend": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp]),
     "nar_host_mapped_pointer": (C.c_int, [_vp, C.POINTER(C.c_void_p)]),
     "nar_zbuffer_accumulate": (
         C.c_int,

@@ -28,7 +28,7 @@ LIB = PKG / "libnar_b200.so"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
           f"-I{INCLUDE}", f"-I{CSRC}", "--expt-relaxed-constexpr"]
-PER_FILE = {"raster.cu": ["-fmad=false"]}
+PER_FILE = {"raster.cu": ["-fmad=false"], "gsplat.cu": ["-fmad=false"]}
 
 
 def _nvcc() -> str:

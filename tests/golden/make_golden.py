@@ -256,6 +256,50 @@ def main() -> None:
     shutil.rmtree(tmp)
     np.savez_compressed(OUT / "preprocess.npz", **pre)
 
+    # ---- Gaussian splats (gsplat/renderer.py, _kernels splat_blend_image) ---------
+    from nar import _kernels as K
+    from nar.gsplat import build_splats, render_gsplat
+    from nar.gsplat.renderer import _prepare_splats
+
+    gs = {}
+    n = 3000
+    W, H = 160, 120
+    mu = np.c_[rng.uniform(-10, W + 10, n), rng.uniform(-10, H + 10, n)]
+    A = rng.normal(0, 1, (n, 2, 2))
+    cov = np.einsum("nij,nkj->nik", A, A) * rng.uniform(0.5, 40, n)[:, None, None] + 0.3 * np.eye(2)
+    det = cov[:, 0, 0] * cov[:, 1, 1] - cov[:, 0, 1] ** 2
+    inv_abc = np.stack([cov[:, 1, 1], -cov[:, 0, 1], cov[:, 0, 0]], axis=1) / det[:, None]
+    lam = np.linalg.eigvalsh(cov)[:, 1]
+    r3 = 3.0 * np.sqrt(lam)
+    boxes = np.stack([np.clip(np.floor(mu[:, 0] - r3), 0, W - 1), np.clip(np.ceil(mu[:, 0] + r3), 0, W - 1),
+                      np.clip(np.floor(mu[:, 1] - r3), 0, H - 1), np.clip(np.ceil(mu[:, 1] + r3), 0, H - 1)],
+                     axis=1).astype(np.int64)
+    color = rng.uniform(0, 1, (n, 3))
+    opac = rng.uniform(0.05, 0.99, n)
+    img_native = K.splat_blend_image(mu, inv_abc, boxes, color, opac, W, H, threads=4, backend="native")
+    img_py = K.splat_blend_image(mu, inv_abc, boxes, color, opac, W, H, backend="python")
+    assert np.allclose(img_native, img_py, rtol=0, atol=1e-12)
+    gs.update({"blend/mu": mu, "blend/inv_abc": inv_abc, "blend/boxes": boxes, "blend/color": color,
+               "blend/opacity": opac, "blend/wh": np.array([W, H]), "blend/rgb": img_native})
+    for style in ("vector_field", "terrain"):
+        m = 2500
+        pos = rng.normal(0, 1, (m, 3)).astype(np.float32) * [1.0, 1.0, 0.3]
+        streams = [Stream("rgb", "u8", rng.integers(0, 256, (m, 3), dtype=np.uint8)),
+                   Stream("velocity", "f32", rng.normal(0, 1, (m, 3)).astype(np.float32))]
+        pc = PointCloud(pos.astype(np.float32), streams)
+        cam = look_at((0.5, -4.0, 2.0), (0, 0, 0), Intrinsics(width=128, height=96))
+        sp = build_splats(pc, style)
+        img, cnt = render_gsplat(sp, cam, threads=4, backend="native", return_counters=True)
+        prep = _prepare_splats(sp, cam)
+        p = f"{style}/"
+        gs.update({p + "positions": pos.astype(np.float32), p + "rgb": streams[0].data,
+                   p + "velocity": streams[1].data, p + "R": cam.orientation,
+                   p + "campos": cam.position, p + "cov": sp.covariances, p + "colors": sp.colors,
+                   p + "opacities": sp.opacities, p + "img": img,
+                   p + "counters": np.array([cnt["total"], cnt["culled"], cnt["skipped_singular"]]),
+                   p + "prep_mu": prep[0], p + "prep_inv_abc": prep[1], p + "prep_boxes": prep[2]})
+    np.savez_compressed(OUT / "gsplat.npz", **gs)
+
     for f in sorted(OUT.glob("*.npz")):
         print(f.name, f.stat().st_size)
 
