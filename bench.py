@@ -260,6 +260,51 @@ def run_cpu_baseline(W, H, n_sample, passes=3):
             "sample_1_thread": f"{n1} points, 1 frame ({dt1:.2f} s)"}
 
 
+def run_gsplat(dev, W, H, n=400_000, cpu=True):
+    """Terrain-style splats of a random height field at the bench resolution:
+    host preparation (not timed), then the tile-binned f64 blend on the GPU
+    (binning + blend, CUDA events) vs the reference's native blend on all host
+    cores (oracle/_ref, one frame)."""
+    import numpy as np
+    import torch
+
+    import oracle
+    from paper_2407_19097_b200.geometry import Intrinsics, PointCloud, Stream, look_at
+    from paper_2407_19097_b200.gsplat import build_splats, prepare_splats, splat_blend_image
+
+    rng = np.random.default_rng(3)
+    xy = rng.uniform(-1, 1, (n, 2))
+    z = 0.15 * np.sin(3 * xy[:, 0]) * np.cos(2 * xy[:, 1])
+    pc = PointCloud(np.c_[xy, z].astype(np.float32),
+                    [Stream("rgb", "u8", rng.integers(0, 256, (n, 3), dtype=np.uint8))])
+    cam = look_at((0.0, -1.6, 1.2), (0, 0, 0), Intrinsics(width=W, height=H))
+    mu, abc, boxes, col, op, cnt = prepare_splats(build_splats(pc, "terrain"), cam)
+    for _ in range(2):
+        splat_blend_image(mu, abc, boxes, col, op, W, H, device=dev, return_device=True)
+    torch.cuda.synchronize()
+    ms = []
+    for _ in range(5):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        img = splat_blend_image(mu, abc, boxes, col, op, W, H, device=dev, return_device=True)
+        b.record()
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b))
+    out = {"splats": int(len(mu)), "width": W, "height": H, "style": "terrain (kNN radii)",
+           "gpu_ms_median": statistics.median(ms),
+           "note": "splat_blend_image: H2D of the prepared arrays + binning + f64 blend"}
+    if cpu:
+        oracle.build()
+        if oracle.ref_native() is not None:
+            th = os.cpu_count() or 1
+            t0 = time.perf_counter()
+            ref = oracle.splat_blend_reference(mu, abc, boxes, col, op, W, H, threads=th)
+            out["cpu_reference_ms"] = (time.perf_counter() - t0) * 1e3
+            out["cpu_threads"] = th
+            out["max_abs_err_vs_reference"] = float(np.max(np.abs(img.cpu().numpy() - ref)))
+    return out
+
+
 def main_reference(args):
     """--impl reference: the reference CPU implementation on the host cores."""
     rank = int(os.environ.get("RANK", "0"))
@@ -513,6 +558,11 @@ def main_ours(args):
         del mcloud
         torch.cuda.empty_cache()
 
+    # ---- Gaussian-splat ground-truth renderer (§8f): GPU blend vs the reference's
+    gsplat = None
+    if world == 1 and not args.no_gsplat:
+        gsplat = run_gsplat(dev, W, H, cpu=not args.no_cpu)
+
     cpu = None
     if not args.no_cpu and world == 1 and rank == 0:
         cpu = run_cpu_baseline(W, H, min(n_pts, 35_000_000))
@@ -549,6 +599,7 @@ def main_ours(args):
             "e2e": e2e,
             "pipeline": pipeline,
             "morton_order": morton,
+            "gsplat": gsplat,
             "gpu_launches": n_launches,
             "clocks": clocks,
         }
@@ -567,6 +618,7 @@ def main():
     ap.add_argument("--points", type=int, default=0, help="override points per GPU")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-morton", action="store_true")
+    ap.add_argument("--no-gsplat", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-pipeline", action="store_true")
     args = ap.parse_args()

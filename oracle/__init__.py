@@ -434,3 +434,45 @@ def splat_blend(mu, inv_abc, boxes, color, opacity, width, height):
         rgb[y0:y1 + 1, x0:x1 + 1] += np.where(on, alpha * tb, 0.0)[:, :, None] * color[i]
         tb *= np.where(on, 1.0 - alpha, 1.0)
     return rgb
+
+
+def splat_blend_reference(mu, inv_abc, boxes, color, opacity, width, height, tile_size=16,
+                          threads=1):
+    """The reference's native blend (oracle/_ref `splat_blend_tiles`) behind the
+    CSR tile binning and tile-range thread split of _kernels/__init__.py:123-166,
+    restated here (pair list in splat order, stable sort by tile).  CPU baseline
+    and cross-check of the GPU blend."""
+    nat = ref_native()
+    if nat is None:
+        raise RuntimeError("oracle/_ref not built")
+    ts = int(tile_size)
+    tiles_x, tiles_y = (width + ts - 1) // ts, (height + ts - 1) // ts
+    n_tiles = tiles_x * tiles_y
+    b = np.asarray(boxes, np.int64)
+    tx0, tx1, ty0, ty1 = b[:, 0] // ts, b[:, 1] // ts, b[:, 2] // ts, b[:, 3] // ts
+    sx = (tx1 - tx0 + 1).astype(np.int64)
+    cnt = sx * (ty1 - ty0 + 1)
+    sid = np.repeat(np.arange(len(b), dtype=np.int64), cnt)
+    off = np.arange(len(sid)) - np.repeat(np.cumsum(cnt) - cnt, cnt)
+    tile = (ty0[sid] + off // sx[sid]) * tiles_x + tx0[sid] + off % sx[sid]
+    order = np.argsort(tile, kind="stable")
+    tile_splats = sid[order]
+    tile_offsets = np.searchsorted(tile[order], np.arange(n_tiles + 1)).astype(np.int64)
+    rgb = np.zeros((height * width, 3), np.float64)
+    trans = np.ones(height * width, np.float64)
+    args = (np.ascontiguousarray(mu, np.float64), np.ascontiguousarray(inv_abc, np.float64),
+            np.ascontiguousarray(b, np.int32), np.ascontiguousarray(color, np.float64),
+            np.ascontiguousarray(opacity, np.float64), tile_offsets, tile_splats)
+
+    def span(t0, t1):
+        nat.splat_blend_tiles(rgb, trans, *args, int(width), int(height), ts, tiles_x,
+                              int(t0), int(t1))
+
+    nt = max(1, min(int(threads or 1), n_tiles))
+    if nt == 1:
+        span(0, n_tiles)
+    else:
+        bounds = np.linspace(0, n_tiles, nt + 1).astype(np.int64)
+        with ThreadPoolExecutor(max_workers=nt) as ex:
+            list(ex.map(lambda se: span(se[0], se[1]), zip(bounds[:-1], bounds[1:])))
+    return rgb.reshape(height, width, 3)
