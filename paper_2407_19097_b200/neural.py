@@ -219,6 +219,18 @@ class UNet:
 _nets: dict = {}
 
 
+def _params_digest(params: dict) -> bytes:
+    import hashlib
+
+    h = hashlib.blake2b(digest_size=16)
+    for name in sorted(params):
+        a = np.ascontiguousarray(getattr(params[name], "data", params[name]), np.float32)
+        h.update(name.encode())
+        h.update(str(a.shape).encode())
+        h.update(a.tobytes())
+    return h.digest()
+
+
 def forward(features, params: dict, config: UNetConfig):
     """Full inference path (model.py:194-204): descriptor head, pyramid, U-Net.
 
@@ -236,13 +248,15 @@ def forward(features, params: dict, config: UNetConfig):
     div = 2 ** (config.levels - 1)
     if shape[-3] % div or shape[-2] % div:
         raise ValueError(f"spatial dims {shape[-3]}x{shape[-2]} not divisible by {div}")
-    key = (id(params), config)
-    ent = _nets.get(key)
-    if ent is None or ent[0] is not params:
+    # packed weights are cached per (config, parameter contents): a dict updated in
+    # place (new arrays or mutated ones) repacks, as the reference reads params
+    # on every call
+    key = (config, _params_digest(params))
+    net = _nets.get(key)
+    if net is None:
         if len(_nets) > 4:
             _nets.clear()
-        ent = _nets[key] = (params, UNet(config, params))
-    net = ent[1]
+        net = _nets[key] = UNet(config, params)
     if isinstance(data, torch.Tensor):
         return net(data)
     x = torch.from_numpy(np.ascontiguousarray(data, dtype=np.float32))

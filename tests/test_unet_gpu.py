@@ -111,3 +111,19 @@ def test_pipeline_frame_psnr(cuda):
     y = forward(x[None], params, cfg)[0, :h, :w]
     ref = oracle.forward(x[None], params, cfg)[0, :h, :w]
     assert oracle.psnr(y, ref) >= PSNR_MIN
+
+
+def test_forward_sees_in_place_param_updates(cuda):
+    """forward() re-reads params like the reference (packed weights are cached by
+    content, so a dict mutated in place is repacked)."""
+    from paper_2407_19097_b200.neural import forward, init_params
+
+    cfg = _cfg(4, 16, 1)
+    params = init_params(cfg)
+    x = np.random.default_rng(2).uniform(size=(1, 32, 48, 4)).astype(np.float32)
+    y0 = forward(x, params, cfg)
+    params["out.b"][:] += 0.5
+    y1 = forward(x, params, cfg)
+    assert not np.allclose(y0, y1)
+    ref = oracle.forward(x, params, cfg)
+    assert oracle.psnr(y1, ref) >= PSNR_MIN
