@@ -19,6 +19,7 @@ also re-clears the keybuf for the next frame.
 from __future__ import annotations
 
 import ctypes as C
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -291,6 +292,7 @@ class Renderer:
         self.hiz = torch.empty(int(nb.value) // 4, dtype=torch.int32, device=self.device)
         self.use_hiz = True
         self.pad_multiple = pad_multiple
+        self._lock = threading.Lock()  # rasterize() serialises calls sharing this renderer
         self._streams: list = []
         self.clear()
 
@@ -422,16 +424,25 @@ def rasterize(pc: PointCloud, cam: CameraPose, sel: StreamSelection, threads: in
     ``threads`` is accepted for signature compatibility and ignored.  Points
     are copied host->device inside this call (async DMA when pinned); with a
     ``PointCloud(..., pinned=True)`` the attribute streams are not copied at
-    all -- the resolve reads the winners' attributes in place.
+    all -- the resolve reads the winners' attributes in place.  Thread-safe:
+    calls sharing a resolution share one cached Renderer and are serialised.
     """
     import torch
 
     _resolve(backend)
     sel.validate(pc)
     intr = cam.intrinsics
-    W, H = intr.width, intr.height
     dev = torch.device("cuda", torch.cuda.current_device())
-    r = _renderer_for(W, H, dev)
+    r = _renderer_for(intr.width, intr.height, dev)
+    with r._lock:
+        return _rasterize(pc, cam, sel, r, dev)
+
+
+def _rasterize(pc: PointCloud, cam: CameraPose, sel: StreamSelection, r: "Renderer", dev):
+    import torch
+
+    intr = cam.intrinsics
+    W, H = intr.width, intr.height
     main = torch.cuda.current_stream(dev)
     kc = cam.kernel_camera()
     names = sel.needed_streams()

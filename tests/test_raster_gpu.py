@@ -330,3 +330,19 @@ def test_host_path_chunked_hiz(cuda):
     plain.use_hiz = False
     plain.render(DeviceCloud.from_tensors(torch.from_numpy(pos).to(cuda)), cam)
     assert np.array_equal(kb, plain.keys())
+
+
+def test_rasterize_thread_safe(cuda, golden):
+    """Concurrent rasterize() calls (same resolution -> one cached renderer) give
+    the same frames as serial calls."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_2407_19097_b200.msr import rasterize
+
+    cases = [random_case(golden, ci) for ci in (0, 1, 4)]  # all 64x64
+    serial = [rasterize(pc, cam, sel).data for pc, cam, sel, _, _ in cases]
+    with ThreadPoolExecutor(max_workers=6) as ex:
+        futs = [ex.submit(rasterize, pc, cam, sel) for _ in range(4) for pc, cam, sel, _, _ in cases]
+        got = [f.result().data for f in futs]
+    for i, g in enumerate(got):
+        assert np.array_equal(g, serial[i % len(cases)])
