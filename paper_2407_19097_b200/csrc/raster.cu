@@ -508,7 +508,10 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
 // Each warp step takes one 128-point unit (4 points per lane) in one ring
 // stage; candidates are drained after each half, so the queue never holds
 // more than 31 + 64.
-constexpr int kPreStages = 3;
+#ifndef NAR_PRE_STAGES
+#define NAR_PRE_STAGES 3
+#endif
+constexpr int kPreStages = NAR_PRE_STAGES;
 constexpr int kPreRingBytes = kRenderWarps * kPreStages * kUnitBytes;
 constexpr int kCandCap = 32 + kChunkPts;  // queue entries per warp
 constexpr int kCandBytes = kRenderWarps * kCandCap * 16;
