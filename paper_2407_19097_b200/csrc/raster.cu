@@ -594,12 +594,9 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
     __syncwarp();
     {  // stage s is consumed: refill it with unit k + kPreStages
       const uint32_t jn = j + kPreStages * j_stride;
-      if (lane == 0 && jn < j_end) {
-        fence_proxy_async_smem();
-        mbar_expect_tx(&full[s], kUnitBytes);
-        bulk_g2s(ring + s * (kUnitPts * 3), pos + (size_t)cm.unit(jn) * (kUnitPts * 3),
-                 kUnitBytes, &full[s]);
-      }
+      if (jn < j_end)  // warp-uniform: one elected lane issues (no per-lane loop)
+        bulk_g2s_elect(ring + s * (kUnitPts * 3), pos + (size_t)cm.unit(jn) * (kUnitPts * 3),
+                       kUnitBytes, &full[s]);
     }
     // w = p - chi: the (x, y) or (y, z) halves of each point that sit in one
     // aligned register pair go through FADD2
