@@ -517,6 +517,14 @@ __global__ void __maxnreg__(96)
     constexpr bool do_head = kHead;
     const int rstep = do_pool ? 2 : 1;
     constexpr int RPW = R >= kEpiGroups ? R / kEpiGroups : 1;  // rows per warp, upper bound
+    // With fewer row slots than groups (small R, or pooled row pairs) the
+    // groups also split the channel chunks, so all 16 warps stay busy; the
+    // head layer keeps whole channel ranges per warp (its logits sum them).
+    const int rgroups = kHead ? kEpiGroups
+                              : (R / rstep < kEpiGroups ? (R / rstep > 0 ? R / rstep : 1)
+                                                        : kEpiGroups);
+    const int cgroups = kEpiGroups / rgroups;
+    const int rslot = grp % rgroups, cslot = grp / rgroups;
     const int nc8 = a.cout_stride / 8;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     int tl = 0;
@@ -538,7 +546,8 @@ __global__ void __maxnreg__(96)
       // parameter bank with compile-time offsets
       constexpr int NC8_HEAD = 2 * ((COUTP + 15) / 16);
 #pragma unroll
-      for (int c8 = 0; c8 < (kHead ? NC8_HEAD : 1 << 20); ++c8) {
+      for (int c8 = kHead ? 0 : cslot; c8 < (kHead ? NC8_HEAD : 1 << 20);
+           c8 += (kHead ? 1 : cgroups)) {
         if (c8 >= nc8) break;
         const int c0 = c8 * 8;
         const bool have = c0 < COUTP;
@@ -553,7 +562,7 @@ __global__ void __maxnreg__(96)
         // (the logit row) is a compile-time index (registers, not local memory)
 #pragma unroll
         for (int i = 0; i < RPW; ++i) {
-          const int r = grp * rstep + i * kEpiGroups * rstep;
+          const int r = rslot * rstep + i * rgroups * rstep;
           const int slot = i * rstep;
           if (r >= R || slot >= RPW) break;
           float o[2][8];
@@ -626,7 +635,7 @@ __global__ void __maxnreg__(96)
       if (do_head) {
 #pragma unroll
         for (int i = 0; i < RPW; ++i) {
-          const int r = grp * rstep + i * kEpiGroups * rstep;
+          const int r = rslot * rstep + i * rgroups * rstep;
           const int slot = i * rstep;
           if (r >= R || slot >= RPW) break;
 #pragma unroll
