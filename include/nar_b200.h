@@ -179,6 +179,19 @@ typedef struct nar_resolve_out {
 int nar_resolve(uint64_t* keybuf_dev, const nar_camera* cam, int32_t key_domain,
                 const nar_selection* sel, const nar_segment* segments,
                 int32_t n_segments, const nar_resolve_out* out, void* stream);
+/* Fused composite + resolve over peer memory (multi-GPU): the
+ * key of each pixel is the minimum over n_keybufs keybufs -- the ranks' own
+ * buffers mapped into this process (CUDA IPC / symmetric memory, NVLink loads)
+ * -- and only rows [row_begin, row_end) of the (padded) output are resolved,
+ * so every rank resolves its slice of the frame with no NCCL all-reduce.  The
+ * segment table lists every rank's shard (peer attribute pointers), so winners
+ * are gathered from their owner's memory.  clear_keybuf resets the slice in
+ * all n_keybufs buffers.  Identical results to nar_resolve on the min-composited
+ * keybuf. */
+int nar_resolve_peers(const uint64_t* const* keybufs, int32_t n_keybufs, int32_t row_begin,
+                      int32_t row_end, const nar_camera* cam, int32_t key_domain,
+                      const nar_selection* sel, const nar_segment* segments, int32_t n_segments,
+                      const nar_resolve_out* out, void* stream);
 
 /* ---- gated U-Net (neural/model.py) -------------------------------------------------- */
 typedef struct nar_unet_config {

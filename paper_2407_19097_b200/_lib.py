@@ -125,6 +125,11 @@ SIGNATURES = {
         [_vp, C.POINTER(Camera), _i32, C.POINTER(Selection), C.POINTER(Segment), _i32,
          C.POINTER(ResolveOut), _vp],
     ),
+    "nar_resolve_peers": (
+        C.c_int,
+        [C.POINTER(C.c_void_p), _i32, _i32, _i32, C.POINTER(Camera), _i32, C.POINTER(Selection),
+         C.POINTER(Segment), _i32, C.POINTER(ResolveOut), _vp],
+    ),
     "nar_unet_create": (C.c_int, [C.POINTER(UNetConfigC), C.POINTER(C.c_void_p)]),
     "nar_unet_destroy": (C.c_int, [_vp]),
     "nar_unet_set_param": (C.c_int, [_vp, C.c_char_p, _vp, _i64]),

@@ -757,6 +757,12 @@ struct ResolveParams {
   float* depth;
   int32_t C, data_h, data_w;
   int32_t owner_only, clear;
+  // composite + resolve over peer memory: the key of a pixel is the minimum
+  // over nkeys keybufs (other GPUs' buffers mapped into this address space);
+  // only padded-output rows [row0, row1) are resolved (this rank's slice)
+  const uint64_t* keys[NAR_MAX_SEGMENTS];
+  int32_t nkeys;
+  int32_t row0, row1;
 };
 
 __device__ __forceinline__ float stream_value(const void* base, int32_t fmt, int32_t arity,
@@ -777,9 +783,10 @@ template <bool kSigned, bool kRgbd>
 __global__ void __launch_bounds__(256)
     resolve_kernel(uint64_t* __restrict__ keybuf, const ResolveParams P) {
   const int32_t W = P.cam.w, H = P.cam.h;
-  const int64_t npix_out = (int64_t)P.data_h * P.data_w;
-  const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (gid >= npix_out) return;
+  const int64_t npix_out = (int64_t)(P.row1 - P.row0) * P.data_w;
+  const int64_t lid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (lid >= npix_out) return;
+  const int64_t gid = (int64_t)P.row0 * P.data_w + lid;
   const int32_t y = (int32_t)(gid / P.data_w);
   const int32_t x = (int32_t)(gid - (int64_t)y * P.data_w);
   float* dst = P.data ? P.data + gid * P.C : nullptr;
@@ -791,9 +798,22 @@ __global__ void __launch_bounds__(256)
     return;
   }
   const int64_t pix = (int64_t)y * W + x;
-  uint64_t key = keybuf[pix];
-  if (kSigned) key ^= NAR_SIGN_FLIP;
-  if (P.clear) keybuf[pix] = kSigned ? (NAR_EMPTY_KEY ^ NAR_SIGN_FLIP) : NAR_EMPTY_KEY;
+  const uint64_t empty_raw = kSigned ? (NAR_EMPTY_KEY ^ NAR_SIGN_FLIP) : NAR_EMPTY_KEY;
+  uint64_t key;
+  if (P.nkeys > 0) {  // composite: min over the ranks' keybufs (in the unsigned order)
+    key = NAR_EMPTY_KEY;
+    for (int k = 0; k < P.nkeys; ++k) {
+      uint64_t v = __ldcg(reinterpret_cast<const unsigned long long*>(P.keys[k]) + pix);
+      if (kSigned) v ^= NAR_SIGN_FLIP;
+      key = v < key ? v : key;
+    }
+    if (P.clear)
+      for (int k = 0; k < P.nkeys; ++k) const_cast<uint64_t*>(P.keys[k])[pix] = empty_raw;
+  } else {
+    key = keybuf[pix];
+    if (kSigned) key ^= NAR_SIGN_FLIP;
+    if (P.clear) keybuf[pix] = empty_raw;
+  }
   const bool covered = key != NAR_EMPTY_KEY;
   const int64_t idx = covered ? (int64_t)(key & 0xFFFFFFFFull) : -1;
   const float dep = covered ? __uint_as_float((uint32_t)(key >> 32)) : 0.0f;
@@ -1236,12 +1256,19 @@ int nar_zbuffer_accumulate(uint64_t* keybuf, const float* positions, int64_t n,
   return rc;
 }
 
-int nar_resolve(uint64_t* keybuf_dev, const nar_camera* cam, int32_t key_domain,
-                const nar_selection* sel, const nar_segment* segments, int32_t n_segments,
-                const nar_resolve_out* out, void* stream) {
+static int resolve_impl(uint64_t* keybuf_dev, const uint64_t* const* peers, int32_t n_peers,
+                        int32_t row_begin, int32_t row_end, const nar_camera* cam,
+                        int32_t key_domain, const nar_selection* sel,
+                        const nar_segment* segments, int32_t n_segments,
+                        const nar_resolve_out* out, void* stream) {
   int rc = validate_camera(cam);
   if (rc) return rc;
-  if (!keybuf_dev || !sel || !out) return set_error(NAR_ERR_INVALID, "NULL argument");
+  if ((!keybuf_dev && n_peers <= 0) || !sel || !out)
+    return set_error(NAR_ERR_INVALID, "NULL argument");
+  if (n_peers < 0 || n_peers > NAR_MAX_SEGMENTS)
+    return set_error(NAR_ERR_INVALID, "1..8 keybufs for a composite resolve");
+  for (int k = 0; k < n_peers; ++k)
+    if (!peers[k]) return set_error(NAR_ERR_INVALID, "NULL peer keybuf");
   if (n_segments < 0 || n_segments > NAR_MAX_SEGMENTS || (n_segments > 0 && !segments))
     return set_error(NAR_ERR_INVALID, "bad segment table");
   if (sel->n_scalars < 0 || sel->n_scalars > NAR_MAX_SCALARS)
@@ -1287,7 +1314,13 @@ int nar_resolve(uint64_t* keybuf_dev, const nar_camera* cam, int32_t key_domain,
     return set_error(NAR_ERR_INVALID, "padded data extent smaller than the image");
   P.owner_only = out->owner_only;
   P.clear = out->clear_keybuf;
-  const int64_t n_out = (int64_t)P.data_h * P.data_w;
+  P.nkeys = n_peers;
+  for (int k = 0; k < n_peers; ++k) P.keys[k] = peers[k];
+  P.row0 = row_begin < 0 ? 0 : row_begin;
+  P.row1 = (row_end < 0 || row_end > P.data_h) ? P.data_h : row_end;
+  if (P.row1 < P.row0) return set_error(NAR_ERR_INVALID, "empty row range");
+  const int64_t n_out = (int64_t)(P.row1 - P.row0) * P.data_w;
+  if (n_out == 0) return NAR_OK;
   const int64_t blocks = (n_out + 255) / 256;
   const bool rgbd = C == 4 && sel->rgb && sel->depth && sel->rgb_format == NAR_FMT_U8 &&
                     sel->rgb_arity >= 3 && (reinterpret_cast<uintptr_t>(out->data) & 15) == 0;
@@ -1297,6 +1330,22 @@ int nar_resolve(uint64_t* keybuf_dev, const nar_camera* cam, int32_t key_domain,
   nar::count_launch();
   kern<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(keybuf_dev, P);
   return check_launch("resolve");
+}
+
+int nar_resolve(uint64_t* keybuf_dev, const nar_camera* cam, int32_t key_domain,
+                const nar_selection* sel, const nar_segment* segments, int32_t n_segments,
+                const nar_resolve_out* out, void* stream) {
+  return resolve_impl(keybuf_dev, nullptr, 0, 0, -1, cam, key_domain, sel, segments, n_segments,
+                      out, stream);
+}
+
+int nar_resolve_peers(const uint64_t* const* keybufs, int32_t n_keybufs, int32_t row_begin,
+                      int32_t row_end, const nar_camera* cam, int32_t key_domain,
+                      const nar_selection* sel, const nar_segment* segments, int32_t n_segments,
+                      const nar_resolve_out* out, void* stream) {
+  if (!keybufs || n_keybufs < 1) return set_error(NAR_ERR_INVALID, "no keybufs");
+  return resolve_impl(nullptr, keybufs, n_keybufs, row_begin, row_end, cam, key_domain, sel,
+                      segments, n_segments, out, stream);
 }
 
 }  // extern "C"

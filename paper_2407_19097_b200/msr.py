@@ -360,7 +360,15 @@ class Renderer:
                 "depth": torch.empty((H, W), dtype=torch.float32, device=dev)}
 
     def resolve(self, cloud: DeviceCloud, cam: CameraPose, sel: StreamSelection, out=None,
-                stream=None, clear: bool = True, owner_only: bool = False) -> DeviceFeatureImage:
+                stream=None, clear: bool = True, owner_only: bool = False,
+                peers: list[int] | None = None, rows: tuple[int, int] | None = None
+                ) -> DeviceFeatureImage:
+        """Decode + channel fill.  ``peers`` (device addresses of keybufs, e.g.
+        other GPUs' buffers mapped here) makes it the fused composite + resolve
+        (``nar_resolve_peers``): the pixel key is the min over them, and only the
+        output ``rows`` [r0, r1) are written.  ``out`` tensors may themselves be
+        peer buffers (``_Mapped``) so a rank writes its slice straight into the
+        root's G-buffer."""
         sel.validate(cloud)
         kc = self._check_cam(cam)
         names = sel.channel_names(cloud)
@@ -375,8 +383,15 @@ class Renderer:
         ro.owner_only, ro.clear_keybuf = int(owner_only), int(clear)
         s = _selection_struct(sel, cloud)
         segs = _segments_struct(cloud, sel)
-        _lib.call("nar_resolve", self.keybuf.data_ptr(), C.byref(kc), self.domain, C.byref(s),
-                  segs, len(cloud.segments), C.byref(ro), _lib.stream_handle(stream))
+        if peers is None:
+            _lib.call("nar_resolve", self.keybuf.data_ptr(), C.byref(kc), self.domain, C.byref(s),
+                      segs, len(cloud.segments), C.byref(ro), _lib.stream_handle(stream))
+        else:
+            arr = (C.c_void_p * len(peers))(*[int(p) for p in peers])
+            r0, r1 = rows if rows is not None else (0, -1)
+            _lib.call("nar_resolve_peers", arr, len(peers), int(r0), int(r1), C.byref(kc),
+                      self.domain, C.byref(s), segs, len(cloud.segments), C.byref(ro),
+                      _lib.stream_handle(stream))
         return DeviceFeatureImage(self.width, self.height, names, out["data"], out["coverage"],
                                   out["index_plane"], out["depth"])
 

@@ -153,3 +153,45 @@ def test_nccl_single_rank_sharded_frame(cuda):
     assert p.exitcode == 0
     assert np.array_equal(gi, ri)
     assert np.array_equal(got.view(np.int32), ref.view(np.int32))
+
+
+@pytest.mark.gpu
+def test_fused_composite_resolve_virtual_ranks(cuda):
+    """nar_resolve_peers over several keybufs (the kernel a rank runs on its peers'
+    mapped buffers; here three shards rendered into three local buffers) with the
+    rows split into slices == the plain single-buffer frame, bit-exact."""
+    import torch
+
+    from paper_2407_19097_b200 import parallel
+    from paper_2407_19097_b200.msr import DeviceCloud, Renderer, StreamSelection
+
+    pc, cam = _scene()
+    i = cam.intrinsics
+    sel = StreamSelection(rgb=True, depth=True, vel2d=True, vel3d=True, velocity_scale=1.5)
+    whole = DeviceCloud.from_host(pc)
+    ref = Renderer(i.width, i.height, pad_multiple=16).rasterize(whole, cam, sel)
+    world = 3
+    shards, rens = [], []
+    for r in range(world):
+        lo, hi = parallel.shard_range(pc.count, r, world)
+        from paper_2407_19097_b200.geometry import PointCloud, Stream
+
+        sub = PointCloud(pc.positions[lo:hi], [Stream(s.name, s.format, s.data[lo:hi])
+                                               for s in pc.streams])
+        shards.append(DeviceCloud.from_host(sub, begin=lo))
+        rn = Renderer(i.width, i.height, pad_multiple=16)
+        rn.render(shards[-1], cam)
+        rens.append(rn)
+    segs = [sg for sh in shards for sg in sh.segments]
+    cloud = DeviceCloud(segs, shards[0].meta, cuda)
+    out = rens[0].alloc_outputs(len(sel.channel_names(cloud)))
+    peers = [rn.keybuf.data_ptr() for rn in rens]
+    ph = out["data"].shape[0]
+    cuts = [0, ph // 3, 2 * ph // 3, ph]
+    for r in range(world):
+        rens[r].resolve(cloud, cam, sel, out=out, peers=peers, rows=(cuts[r], cuts[r + 1]))
+    torch.cuda.synchronize()
+    assert torch.equal(out["index_plane"], ref.index_plane)
+    assert torch.equal(out["data"].view(torch.int32), ref.data.view(torch.int32))
+    for rn in rens:  # slices cleared every keybuf
+        assert bool((rn.keybuf == rn.keybuf[0]).all())
