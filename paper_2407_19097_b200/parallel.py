@@ -82,3 +82,112 @@ class ShardedRenderer:
         img = self.r.resolve(cloud, cam, sel, out=out, owner_only=True)
         reduce_planes(img.data, dst=root, group=self.group)
         return img
+
+
+def row_slice(rows: int, rank: int, world: int) -> tuple[int, int]:
+    """Rows [r0, r1) of the padded output resolved by `rank` in the fused path."""
+    return rows * rank // world, rows * (rank + 1) // world
+
+
+class PeerShardedRenderer:
+    """Fused composite + resolve over peer memory, no NCCL on
+    the data path.
+
+    The rank's keybuf, its shard (positions + attribute streams) and the root's
+    output G-buffer live in symmetric memory (``torch.distributed._symmetric_
+    memory``: every rank maps every other rank's buffers over NVLink).  A frame
+    is: render the local shard into the local keybuf; a device-side barrier;
+    ``nar_resolve_peers`` on this rank's row slice -- min over all ranks'
+    keybufs, winners' attributes gathered from their owners' shards, channels
+    stored straight into the root's G-buffer, every keybuf's slice reset for
+    the next frame; a barrier.  Each rank thus reads 1/P of every keybuf
+    (16.6 MB inbound per rank at 1080p in total) instead of all-reducing the
+    whole buffer and then reducing the planes.
+    """
+
+    def __init__(self, width: int, height: int, shard, group=None, pad_multiple: int = 16,
+                 root: int = 0):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+
+        from .msr import DeviceCloud, Renderer, _Mapped
+
+        self.group = group or dist.group.WORLD
+        self.rank, self.world = dist.get_rank(self.group), dist.get_world_size(self.group)
+        self.root = root
+        dev = shard.device
+        self.r = Renderer(width, height, device=dev, pad_multiple=pad_multiple)
+        npix = width * height
+        # keybuf in symmetric memory (the renderer renders into it)
+        kb = symm.empty(npix, dtype=torch.int64, device=dev)
+        kb.copy_(self.r.keybuf)
+        self._kh = symm.rendezvous(kb, self.group)
+        self.r.keybuf = kb
+        self.keybufs = [int(p) for p in self._kh.buffer_ptrs]
+        # shard arrays in symmetric memory (equal shapes on all ranks: padded to the max)
+        sg = shard.segments[0]
+        counts = [None] * self.world
+        dist.all_gather_object(counts, (int(sg["begin"]), int(sg["count"])), group=self.group)
+        nmax = max(c for _, c in counts)
+        self._hold = []
+
+        def share(t):
+            buf = symm.empty((nmax,) + tuple(t.shape[1:]), dtype=t.dtype, device=dev)
+            buf[: t.shape[0]].copy_(t)
+            h = symm.rendezvous(buf, self.group)
+            self._hold.append((buf, h))
+            return buf, [int(p) for p in h.buffer_ptrs]
+
+        pos, pos_ptrs = share(sg["positions"])
+        names = sorted(sg["streams"])
+        st_local, st_ptrs = {}, {}
+        for n in names:
+            st_local[n], st_ptrs[n] = share(sg["streams"][n])
+        self.local = DeviceCloud([{"begin": sg["begin"], "count": sg["count"],
+                                   "positions": pos[: sg["count"]],
+                                   "streams": {n: st_local[n][: sg["count"]] for n in names}}],
+                                 shard.meta, dev)
+        segs = []
+        for r, (b, c) in enumerate(counts):
+            segs.append({"begin": b, "count": c,
+                         "positions": _Mapped(pos_ptrs[r], (c, 3)),
+                         "streams": {n: _Mapped(st_ptrs[n][r], (c,) + tuple(sg["streams"][n].shape[1:]))
+                                     for n in names}})
+        self.all = DeviceCloud(segs, shard.meta, dev)
+        self._out = None
+
+    def _outputs(self, C: int):
+        """Root's G-buffer planes in symmetric memory; every rank writes its slice."""
+        import torch
+        import torch.distributed._symmetric_memory as symm
+
+        from .msr import _Mapped
+
+        if self._out is not None and self._out[0] == C:
+            return self._out[1], self._out[2]
+        ph, pw = self.r.alloc_outputs(C)["data"].shape[:2]
+        H, W = self.r.height, self.r.width
+        dev = self.r.device
+        local, peer = {}, {}
+        for k, shape, dt in (("data", (ph, pw, C), torch.float32), ("coverage", (H, W), torch.uint8),
+                             ("index_plane", (H, W), torch.int64), ("depth", (H, W), torch.float32)):
+            buf = symm.empty(shape, dtype=dt, device=dev)
+            h = symm.rendezvous(buf, self.group)
+            self._hold.append((buf, h))
+            local[k] = buf
+            peer[k] = _Mapped(int(h.buffer_ptrs[self.root]), shape)
+        self._out = (C, local, peer)
+        return local, peer
+
+    def frame(self, cam, sel):
+        """One sharded frame; returns the root's output dict (complete on root)."""
+        names = sel.channel_names(self.all)
+        local, peer = self._outputs(len(names))
+        self.r.render(self.local, cam)
+        self._kh.barrier(channel=0)
+        rows = local["data"].shape[0]
+        self.r.resolve(self.all, cam, sel, out=peer, peers=self.keybufs,
+                       rows=row_slice(rows, self.rank, self.world))
+        self._kh.barrier(channel=1)
+        return local

@@ -195,3 +195,41 @@ def test_fused_composite_resolve_virtual_ranks(cuda):
     assert torch.equal(out["data"].view(torch.int32), ref.data.view(torch.int32))
     for rn in rens:  # slices cleared every keybuf
         assert bool((rn.keybuf == rn.keybuf[0]).all())
+
+
+def _peer_worker(port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        from paper_2407_19097_b200.msr import DeviceCloud, Renderer, StreamSelection
+        from paper_2407_19097_b200.parallel import PeerShardedRenderer
+
+        pc, cam = _scene()
+        i = cam.intrinsics
+        cloud = DeviceCloud.from_host(pc)
+        sel = StreamSelection(rgb=True, depth=True, vel2d=True, vel3d=True, velocity_scale=1.5)
+        pr = PeerShardedRenderer(i.width, i.height, cloud)
+        outs = [pr.frame(cam, sel) for _ in range(2)]  # second frame: keybuf was re-cleared
+        torch.cuda.synchronize()
+        ref = Renderer(i.width, i.height, pad_multiple=16).rasterize(cloud, cam, sel)
+        q.put((outs[1]["data"].cpu().numpy(), ref.data.cpu().numpy(),
+               outs[1]["index_plane"].cpu().numpy(), ref.index_plane.cpu().numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_peer_sharded_frame_single_rank(cuda):
+    """The symmetric-memory fused path end to end with one rank (peer pointer =
+    own buffer): equals the plain frame, twice in a row."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_peer_worker, args=(_free_port(), q))
+    p.start()
+    got, ref, gi, ri = q.get(timeout=300)
+    p.join(timeout=60)
+    assert p.exitcode == 0
+    assert np.array_equal(gi, ri)
+    assert np.array_equal(got.view(np.int32), ref.view(np.int32))
