@@ -82,6 +82,26 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+C_CONSUMER_SRC = ROOT / "tests" / "c" / "abi_consumer.c"
+C_CONSUMER = ROOT / "tests" / "c" / "abi_consumer"
+
+
+def build_c_consumer() -> Path | None:
+    """gcc the plain-C ABI consumer (tests/c/abi_consumer.c) against the header
+    and libnar_b200.so -- proof that the boundary needs no Python or C++."""
+    if not C_CONSUMER_SRC.exists():
+        return None
+    cuda = Path(_nvcc()).resolve().parent.parent
+    cmd = ["gcc", "-std=c99", "-O2", "-Wall", f"-I{INCLUDE}", f"-I{cuda / 'include'}",
+           str(C_CONSUMER_SRC), "-o", str(C_CONSUMER), f"-L{PKG}", "-lnar_b200",
+           f"-L{cuda / 'lib64'}", "-lcudart", "-Wl,-rpath,$ORIGIN/../../paper_2407_19097_b200",
+           f"-Wl,-rpath,{cuda / 'lib64'}"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"C consumer build failed:\n{res.stderr}")
+    return C_CONSUMER
+
+
 if __name__ == "__main__":
     p = build(force="--force" in sys.argv, verbose="-v" in sys.argv)
     print(p)

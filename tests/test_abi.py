@@ -110,3 +110,46 @@ def test_pointcloud_limits():
         PointCloud(np.zeros((1, 3)), [Stream(f"s{i}", "u8", np.zeros((1, 1))) for i in range(9)])
     with pytest.raises(ValueError):
         PointCloud(np.zeros((2, 3)), [Stream("rgb", "u8", np.zeros((3, 3)))])
+
+
+@pytest.mark.gpu
+def test_plain_c_consumer(cuda, tmp_path):
+    """tests/c/abi_consumer (gcc, only include/nar_b200.h + libnar_b200.so + cudart):
+    host-parity and device entry points from C, checked against the oracle."""
+    import struct
+    import subprocess
+
+    import oracle
+    from paper_2407_19097_b200 import build as b
+    from paper_2407_19097_b200.geometry import Intrinsics, look_at
+
+    exe = b.C_CONSUMER if b.C_CONSUMER.exists() else b.build_c_consumer()
+    rng = np.random.default_rng(21)
+    n, W, H = 200_000, 160, 120
+    pos = rng.uniform(-1, 1, (n, 3)).astype(np.float32)
+    rgb = rng.integers(0, 256, (n, 3), dtype=np.uint8)
+    cam = look_at((0.2, -2.3, 0.9), (0, 0, 0), Intrinsics(width=W, height=H))
+    i = cam.intrinsics
+    fin, fout = tmp_path / "in.bin", tmp_path / "out.bin"
+    with open(fin, "wb") as f:
+        f.write(struct.pack("<qii", n, W, H))
+        f.write(np.ascontiguousarray(cam.orientation, np.float64).tobytes())
+        f.write(np.ascontiguousarray(cam.position, np.float64).tobytes())
+        f.write(struct.pack("<5d", i.focal_px, i.cx, i.cy, i.near, i.far))
+        f.write(pos.tobytes() + rgb.tobytes())
+    res = subprocess.run([str(exe), str(fin), str(fout)], capture_output=True, text=True)
+    assert res.returncode == 0, res.stderr
+    raw = fout.read_bytes()
+    npix = W * H
+    kb_host = np.frombuffer(raw, np.uint64, npix, 0)
+    kb_dev = np.frombuffer(raw, np.uint64, npix, npix * 8)
+    data = np.frombuffer(raw, np.float32, npix * 4, npix * 16).reshape(H, W, 4)
+    ref = oracle.zbuffer_render(pos, cam.orientation, cam.position, i.focal_px, i.cx, i.cy,
+                                i.near, i.far, W, H)
+    assert np.array_equal(kb_host, ref) and np.array_equal(kb_dev, ref)
+    from paper_2407_19097_b200.geometry import PointCloud, Stream
+    from paper_2407_19097_b200.msr import StreamSelection
+
+    want = oracle.rasterize(PointCloud(pos, [Stream("rgb", "u8", rgb)]), cam,
+                            StreamSelection(rgb=True, depth=True))["data"]
+    assert np.array_equal(data, want)
