@@ -45,7 +45,7 @@ def launches(tag):
         if "resolve_kernel" in k["name"]:
             frames.append(cur)
             cur = []
-    frame = frames[len(frames) // 2]  # a steady-state raster frame
+    frame = frames[min(4, len(frames) - 1)]  # a timed raster frame (after 3 warm-ups)
     tot = sum(k["gpu__time_duration.sum"] for k in frame)
     lines = [f"# {tag}: per-launch device time of one C2 frame (ncu, cold-cache, serialised)",
              "", "Command: `ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,"
@@ -65,9 +65,15 @@ def launches(tag):
               f"{rsum / 1e3:.1f} us = {100 * rsum / tot:.1f}% of the frame; their DRAM traffic "
               f"{rt_bytes / 1e9:.3f} GB per frame vs 4.200 GB algorithmic (350M x 12 B)."]
     # U-Net launches of one pipeline frame
-    last_resolve = max(i for i, k in enumerate(seq) if "resolve_kernel" in k["name"])
-    last = [k for k in seq[last_resolve + 1:] if "gated_conv" in k["name"] or
-            "head_pyramid" in k["name"] or "pool_bf16" in k["name"] or "out_head" in k["name"]]
+    unet_kernel = lambda k: any(t in k["name"] for t in ("gated_conv", "head_pyramid", "pool_bf16",
+                                                           "out_head"))
+    starts = [i for i, k in enumerate(seq) if "head_pyramid" in k["name"]]
+    last = []
+    if starts:
+        for k in seq[starts[-1]:]:
+            if not unet_kernel(k):
+                break
+            last.append(k)
     if last:
         ut = sum(k["gpu__time_duration.sum"] for k in last)
         lines += ["", "## U-Net forward (last pipeline frame)", "",
