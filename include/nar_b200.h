@@ -194,6 +194,20 @@ int nar_resolve_peers(const uint64_t* const* keybufs, int32_t n_keybufs, int32_t
                       const nar_resolve_out* out, void* stream);
 
 /* ---- gated U-Net (neural/model.py) -------------------------------------------------- */
+/* Standalone ops of the network (model.py:135-163), f32 device tensors in/out.
+ * nar_head_pyramid: the 1x1 descriptor head y = x W + b (use_head != 0; W (C,C)
+ * and b (C,) device f32) and the pyramid of 2x2 averages; out[k] is
+ * (H >> k, W >> k, C) f32 for k < levels (H, W divisible by 2^(levels-1)).
+ * nar_gated_conv: elu(conv3x3(x, f_w) + f_b) * sigmoid(conv3x3(x, g_w) + g_b),
+ * "same" zero padding, HWIO f32 weights on the HOST (packed to bf16 per call),
+ * bf16 tensor-core math with f32 accumulation; blocks until done. */
+int nar_head_pyramid(const float* in, int32_t H, int32_t W, int32_t C, const float* head_w,
+                     const float* head_b, int32_t use_head, int32_t levels, float* const* out,
+                     void* stream);
+int nar_gated_conv(const float* in, int32_t H, int32_t W, int32_t cin, const float* f_w,
+                   const float* f_b, const float* g_w, const float* g_b, int32_t cout, float* out,
+                   void* stream);
+
 typedef struct nar_unet_config {
   int32_t input_channels, levels, base_channels, channel_multiplier;
   int32_t max_channels, output_channels, use_descriptor_head;

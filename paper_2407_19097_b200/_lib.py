@@ -131,6 +131,9 @@ SIGNATURES = {
          C.POINTER(Segment), _i32, C.POINTER(ResolveOut), _vp],
     ),
     "nar_unet_create": (C.c_int, [C.POINTER(UNetConfigC), C.POINTER(C.c_void_p)]),
+    "nar_head_pyramid": (C.c_int, [_vp, _i32, _i32, _i32, _vp, _vp, _i32, _i32,
+                                   C.POINTER(C.c_void_p), _vp]),
+    "nar_gated_conv": (C.c_int, [_vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _i32, _vp, _vp]),
     "nar_unet_destroy": (C.c_int, [_vp]),
     "nar_unet_set_param": (C.c_int, [_vp, C.c_char_p, _vp, _i64]),
     "nar_unet_workspace_bytes": (C.c_int, [_vp, _i32, _i32, C.POINTER(C.c_size_t)]),

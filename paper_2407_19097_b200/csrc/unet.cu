@@ -43,6 +43,7 @@ static inline int rup(int x, int m) { return (x + m - 1) / m * m; }
 // bf16 NHWC padded to cp channels (zeros in the padding).
 struct PyrOut {
   __nv_bfloat16* lvl[8];
+  float* lvlf[8];  // standalone API (nar_head_pyramid): f32 (H>>k, W>>k, cin) levels instead
 };
 
 // CIN: compile-time upper bound of cin (4, 8 or 16) so the per-pixel channel
@@ -84,6 +85,12 @@ __global__ void __launch_bounds__(256, 4)
     }
     hv[j] = acc;
   }
+  if (out.lvlf[0]) {  // f32 levels for the standalone API
+    float* f0 = out.lvlf[0] + ((size_t)y * W + xx) * cin;
+#pragma unroll
+    for (int j = 0; j < CIN; ++j)
+      if (j < cin) f0[j] = hv[j];
+  } else {
   // bf16 level 0, padded to cp channels, 16-byte stores
   __nv_bfloat16* o0 = out.lvl[0] + ((size_t)y * W + xx) * cp;
 #pragma unroll
@@ -98,6 +105,7 @@ __global__ void __launch_bounds__(256, 4)
       (&pk.x)[e / 2] = *reinterpret_cast<uint32_t*>(&h2);
     }
     *reinterpret_cast<uint4*>(o0 + c8) = pk;
+  }
   }
   __syncthreads();
   // levels 1..L-1: 2x2 averages in f32, in place in shared memory
@@ -124,19 +132,26 @@ __global__ void __launch_bounds__(256, 4)
       for (int c = 0; c < CIN; ++c)
         if (c < cin) tile[t * cin + c] = m[c];
       const int Wk = W >> k;
-      __nv_bfloat16* ok = out.lvl[k] + ((size_t)(ty * ns + qy) * Wk + (tx * ns + qx)) * cp;
+      if (out.lvlf[k]) {
+        float* fk = out.lvlf[k] + ((size_t)(ty * ns + qy) * Wk + (tx * ns + qx)) * cin;
 #pragma unroll
-      for (int c8 = 0; c8 < 16; c8 += 8) {
-        if (c8 >= cp) break;
-        uint4 pk;
+        for (int c = 0; c < CIN; ++c)
+          if (c < cin) fk[c] = m[c];
+      } else {
+        __nv_bfloat16* ok = out.lvl[k] + ((size_t)(ty * ns + qy) * Wk + (tx * ns + qx)) * cp;
 #pragma unroll
-        for (int e = 0; e < 8; e += 2) {
-          const int c = c8 + e;
-          __nv_bfloat162 h2 = __floats2bfloat162_rn(c < CIN && c < cin ? m[c % CIN] : 0.f,
-                                                    c + 1 < CIN && c + 1 < cin ? m[(c + 1) % CIN] : 0.f);
-          (&pk.x)[e / 2] = *reinterpret_cast<uint32_t*>(&h2);
+        for (int c8 = 0; c8 < 16; c8 += 8) {
+          if (c8 >= cp) break;
+          uint4 pk;
+#pragma unroll
+          for (int e = 0; e < 8; e += 2) {
+            const int c = c8 + e;
+            __nv_bfloat162 h2 = __floats2bfloat162_rn(
+                c < CIN && c < cin ? m[c % CIN] : 0.f, c + 1 < CIN && c + 1 < cin ? m[(c + 1) % CIN] : 0.f);
+            (&pk.x)[e / 2] = *reinterpret_cast<uint32_t*>(&h2);
+          }
+          *reinterpret_cast<uint4*>(ok + c8) = pk;
         }
-        *reinterpret_cast<uint4*>(ok + c8) = pk;
       }
     }
     __syncthreads();
@@ -592,6 +607,7 @@ int nar_unet_forward(nar_unet* n, const float* in, int32_t H, int32_t W, float* 
   {
     const int T = 1 << (L - 1);
     PyrOut po;
+    memset(&po, 0, sizeof(po));
     for (int k = 0; k < L; ++k) po.lvl[k] = bf(p.off_pyr16[k]);
     const size_t sm = (size_t)T * T * cin * 4;
     if (T * T > 256) return set_error(NAR_ERR_CONFIG, "at most 5 pyramid levels supported");
@@ -639,6 +655,103 @@ int nar_unet_forward(nar_unet* n, const float* in, int32_t H, int32_t W, float* 
     x = bf(p.off_x[k]);
   }
   return NAR_OK;
+}
+
+// ---- standalone ops (model.py:135-163), f32 in/out on device ---------------------
+
+static __global__ void pack_bf16_kernel(const float* __restrict__ in, int64_t npx, int cin,
+                                        int cinp, __nv_bfloat16* __restrict__ out) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= npx * cinp) return;
+  const int64_t p = t / cinp;
+  const int c = (int)(t - p * cinp);
+  out[t] = __float2bfloat16_rn(c < cin ? in[p * cin + c] : 0.0f);
+}
+
+static __global__ void unpack_f32_kernel(const __nv_bfloat16* __restrict__ in, int64_t npx,
+                                         int cout, int cs, float* __restrict__ out) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= npx * cout) return;
+  const int64_t p = t / cout;
+  out[t] = __bfloat162float(in[p * cs + (t - p * cout)]);
+}
+
+int nar_head_pyramid(const float* in, int32_t H, int32_t W, int32_t C, const float* head_w,
+                     const float* head_b, int32_t use_head, int32_t levels, float* const* out,
+                     void* stream) {
+  if (!in || !out || (use_head && (!head_w || !head_b)))
+    return set_error(NAR_ERR_INVALID, "NULL argument");
+  if (C < 1 || C > 16) return set_error(NAR_ERR_CONFIG, "1..16 channels");
+  if (levels < 1 || levels > 5) return set_error(NAR_ERR_CONFIG, "1..5 pyramid levels");
+  const int T = 1 << (levels - 1);
+  if (H <= 0 || W <= 0 || H % T || W % T)
+    return set_error(NAR_ERR_INVALID, "spatial dims not divisible by 2^(levels-1)");
+  PyrOut po;
+  memset(&po, 0, sizeof(po));
+  for (int k = 0; k < levels; ++k) {
+    if (!out[k]) return set_error(NAR_ERR_INVALID, "NULL pyramid level");
+    po.lvlf[k] = out[k];
+  }
+  auto kern = C <= 4 ? head_pyramid_kernel<4> : (C <= 8 ? head_pyramid_kernel<8> : head_pyramid_kernel<16>);
+  if (C == 4 && (reinterpret_cast<uintptr_t>(in) & 15)) kern = head_pyramid_kernel<8>;
+  nar::count_launch();
+  kern<<<dim3(W / T, H / T), T * T, (size_t)T * T * C * 4, (cudaStream_t)stream>>>(
+      in, H, W, C, rup(C, 16), head_w, head_b, use_head, levels, po);
+  return check_launch("head_pyramid");
+}
+
+int nar_gated_conv(const float* in, int32_t H, int32_t W, int32_t cin, const float* f_w,
+                   const float* f_b, const float* g_w, const float* g_b, int32_t cout, float* out,
+                   void* stream) {
+  if (!in || !out || !f_w || !f_b || !g_w || !g_b) return set_error(NAR_ERR_INVALID, "NULL argument");
+  if (H <= 0 || W <= 0 || cin < 1 || cout < 1 || cout > 128 || cin > 2048)
+    return set_error(NAR_ERR_CONFIG, "unsupported gated conv shape");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int cinp = rup(cin, 16), cs = rup(cout, 16);
+  const int64_t npx = (int64_t)H * W;
+  std::vector<float> wf(f_w, f_w + (size_t)9 * cin * cout), wg(g_w, g_w + (size_t)9 * cin * cout);
+  std::vector<uint16_t> packed;
+  tc_pack_weights(wf, wg, cin, 0, cout, packed);
+  __nv_bfloat16 *x = nullptr, *y = nullptr, *w = nullptr;
+  float *bf = nullptr, *bg = nullptr;
+  int rc = NAR_OK;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&x), (size_t)npx * cinp * 2, st) ||
+      cudaMallocAsync(reinterpret_cast<void**>(&y), (size_t)npx * cs * 2, st) ||
+      cudaMallocAsync(reinterpret_cast<void**>(&w), packed.size() * 2, st) ||
+      cudaMallocAsync(reinterpret_cast<void**>(&bf), (size_t)cout * 4, st) ||
+      cudaMallocAsync(reinterpret_cast<void**>(&bg), (size_t)cout * 4, st))
+    rc = set_error(NAR_ERR_NOMEM, "gated conv scratch");
+  if (!rc) {
+    cudaMemcpyAsync(w, packed.data(), packed.size() * 2, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(bf, f_b, (size_t)cout * 4, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(bg, g_b, (size_t)cout * 4, cudaMemcpyHostToDevice, st);
+    nar::count_launch();
+    pack_bf16_kernel<<<(unsigned)((npx * cinp + 255) / 256), 256, 0, st>>>(in, npx, cin, cinp, x);
+    ConvArgs a;
+    memset(&a, 0, sizeof(a));
+    a.src_a = x;
+    a.ca = cin;
+    a.ca_stride = cinp;
+    a.H = H;
+    a.W = W;
+    a.cout = cout;
+    a.cout_stride = cs;
+    a.bias_f = bf;
+    a.bias_g = bg;
+    a.wtc = w;
+    a.out = y;
+    rc = tc_launch_gated_conv(a, st);
+    if (!rc) {
+      nar::count_launch();
+      unpack_f32_kernel<<<(unsigned)((npx * cout + 255) / 256), 256, 0, st>>>(y, npx, cout, cs, out);
+    }
+    // the host weight copy is stream-ordered: keep `packed` alive until it ran
+    cudaStreamSynchronize(st);
+  }
+  for (void* p : {(void*)x, (void*)y, (void*)w, (void*)bf, (void*)bg})
+    if (p) cudaFreeAsync(p, st);
+  if (!rc) rc = check_launch("gated_conv");
+  return rc;
 }
 
 }  // extern "C"

@@ -516,7 +516,7 @@ __global__ void __maxnreg__(96)
     const bool do_pool = !kHead && a.pool_out != nullptr;  // requires R even (host-checked)
     constexpr bool do_head = kHead;
     const int rstep = do_pool ? 2 : 1;
-    constexpr int RPW = R >= kEpiGroups ? R / kEpiGroups : 1;  // rows per warp, upper bound
+    constexpr int RPW = (R + kEpiGroups - 1) / kEpiGroups;  // rows per warp, upper bound
     // With fewer row slots than groups (small R, or pooled row pairs) the
     // groups also split the channel chunks, so all 16 warps stay busy; the
     // head layer keeps whole channel ranges per warp (its logits sum them).

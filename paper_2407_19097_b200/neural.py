@@ -116,6 +116,92 @@ def pad_to_multiple(img: np.ndarray, multiple: int = 16):
 # ---------------------------------------------------------------------------
 # device network (libnar_b200.so nar_unet_*)
 # ---------------------------------------------------------------------------
+# ---- standalone ops on the GPU (model.py:135-163) ------------------------------------
+
+def _dev_f32(x):
+    """(tensor on cuda f32 contiguous, was_torch)."""
+    import torch
+
+    data = getattr(x, "data", x) if not hasattr(x, "device") else x
+    if isinstance(data, torch.Tensor):
+        return data.to("cuda", torch.float32).contiguous(), True
+    return torch.from_numpy(np.ascontiguousarray(data, np.float32)).cuda(), False
+
+
+def _images(t):
+    """Iterate the (H, W, C) images of a (.., H, W, C) tensor."""
+    return t.reshape((-1,) + tuple(t.shape[-3:]))
+
+
+def conv1x1_head(x, w, b):
+    """Per-pixel affine y = x @ w + b (model.py:135-143) with the fused head kernel.
+    ``x`` (..., H, W, C), ``w`` (C, C), ``b`` (C,).  H, W any."""
+    return build_pyramid(x, levels=1, head=(w, b))[0]
+
+
+def build_pyramid(t, levels: int = 5, head=None):
+    """Levels 0..levels-1 of 2x2 averages (model.py:146-155) in f32 on the GPU
+    (optionally after the descriptor head ``head=(w, b)``).  Returns a list of
+    arrays / tensors like the input kind."""
+    import torch
+
+    x, was_torch = _dev_f32(t)
+    ch = int(x.shape[-1])
+    H, W = int(x.shape[-3]), int(x.shape[-2])
+    div = 2 ** (levels - 1)
+    if H % div or W % div:
+        raise ValueError(f"spatial dims {H}x{W} not divisible by {div}")
+    if head is not None:
+        hw, _ = _dev_f32(head[0])
+        hb, _ = _dev_f32(head[1])
+        if tuple(hw.shape) != (ch, ch) or tuple(hb.shape) != (ch,):
+            raise ConfigurationError(f"head weights must be ({ch},{ch}) and ({ch},)")
+    lead = tuple(x.shape[:-3])
+    imgs = _images(x)
+    outs = [torch.empty((imgs.shape[0], H >> k, W >> k, ch), dtype=torch.float32, device=x.device)
+            for k in range(levels)]
+    st = torch.cuda.current_stream(x.device)
+    for i in range(imgs.shape[0]):
+        arr = (C.c_void_p * levels)(*[o[i].data_ptr() for o in outs])
+        _lib.call("nar_head_pyramid", imgs[i].data_ptr(), H, W, ch,
+                  hw.data_ptr() if head is not None else None,
+                  hb.data_ptr() if head is not None else None, int(head is not None), levels,
+                  arr, int(st.cuda_stream))
+    res = [o.reshape(lead + tuple(o.shape[1:])) for o in outs]
+    if was_torch:
+        return res
+    st.synchronize()
+    return [r.cpu().numpy() for r in res]
+
+
+def gated_conv(x, f_w, f_b, g_w, g_b):
+    """elu(conv3x3(x, f_w) + f_b) * sigmoid(conv3x3(x, g_w) + g_b), same padding
+    (model.py:158-163), on the tensor cores (bf16 operands, f32 accumulation)."""
+    import torch
+
+    xd, was_torch = _dev_f32(x)
+    fw = np.ascontiguousarray(getattr(f_w, "data", f_w), np.float32)
+    gw = np.ascontiguousarray(getattr(g_w, "data", g_w), np.float32)
+    fb = np.ascontiguousarray(getattr(f_b, "data", f_b), np.float32)
+    gb = np.ascontiguousarray(getattr(g_b, "data", g_b), np.float32)
+    cin = int(xd.shape[-1])
+    if fw.shape[:3] != (3, 3, cin) or gw.shape != fw.shape:
+        raise ConfigurationError(f"gated conv kernels must be (3,3,{cin},Cout)")
+    cout = int(fw.shape[3])
+    if fb.shape != (cout,) or gb.shape != (cout,):
+        raise ConfigurationError("gated conv biases must be (Cout,)")
+    lead = tuple(xd.shape[:-3])
+    H, W = int(xd.shape[-3]), int(xd.shape[-2])
+    imgs = _images(xd)
+    out = torch.empty((imgs.shape[0], H, W, cout), dtype=torch.float32, device=xd.device)
+    st = torch.cuda.current_stream(xd.device)
+    for i in range(imgs.shape[0]):
+        _lib.call("nar_gated_conv", imgs[i].data_ptr(), H, W, cin, fw.ctypes.data, fb.ctypes.data,
+                  gw.ctypes.data, gb.ctypes.data, cout, out[i].data_ptr(), int(st.cuda_stream))
+    out = out.reshape(lead + (H, W, cout))
+    return out if was_torch else out.cpu().numpy()
+
+
 def _config_struct(cfg: UNetConfig) -> "_lib.UNetConfigC":
     c = _lib.UNetConfigC()
     c.input_channels, c.levels = cfg.input_channels, cfg.levels

@@ -127,3 +127,74 @@ def test_forward_sees_in_place_param_updates(cuda):
     assert not np.allclose(y0, y1)
     ref = oracle.forward(x, params, cfg)
     assert oracle.psnr(y1, ref) >= PSNR_MIN
+
+
+# ---- standalone ops: SPEC.md:348-376 examples ------------------------------------------
+
+def test_conv1x1_head_kats(cuda):
+    from paper_2407_19097_b200.neural import conv1x1_head
+
+    rng = np.random.default_rng(5)
+    x = rng.normal(size=(1, 24, 40, 6)).astype(np.float32)
+    assert np.array_equal(conv1x1_head(x, np.eye(6, dtype=np.float32), np.zeros(6, np.float32)), x)
+    w = rng.normal(size=(6, 6)).astype(np.float32)
+    b = rng.normal(size=6).astype(np.float32)
+    c = np.broadcast_to(rng.normal(size=6).astype(np.float32), (1, 16, 16, 6)).copy()
+    yc = conv1x1_head(c, w, b)
+    assert np.all(yc == yc[0, 0, 0])  # spatial invariance
+    y = conv1x1_head(x, w, b)
+    assert np.max(np.abs(y - (x.astype(np.float64) @ w + b))) < 1e-5
+
+
+def test_build_pyramid_kats(cuda):
+    from paper_2407_19097_b200.neural import build_pyramid
+
+    rng = np.random.default_rng(6)
+    lv = build_pyramid(np.zeros((1, 512, 512, 4), np.float32))
+    assert [l.shape[1] for l in lv] == [512, 256, 128, 64, 32]
+    c = np.full((1, 64, 96, 3), 0.3721, np.float32)
+    assert all(np.all(l == np.float32(0.3721)) for l in build_pyramid(c))
+    t = rng.normal(size=(1, 8, 8, 5)).astype(np.float32)
+    l1 = build_pyramid(t, levels=2)[1]
+    ref = ((t[:, 0::2, 0::2] + t[:, 0::2, 1::2]) + (t[:, 1::2, 0::2] + t[:, 1::2, 1::2])) * np.float32(0.25)
+    assert np.max(np.abs(l1 - ref)) <= 1e-6
+    with pytest.raises(ValueError):
+        build_pyramid(np.zeros((1, 20, 16, 4), np.float32))
+
+
+def test_gated_conv_kats(cuda):
+    from paper_2407_19097_b200.neural import gated_conv
+
+    rng = np.random.default_rng(7)
+    x = rng.uniform(-1, 1, size=(1, 33, 70, 12)).astype(np.float32)
+    f_w = rng.normal(0, 0.2, (3, 3, 12, 24)).astype(np.float32)
+    f_b = rng.normal(0, 0.1, 24).astype(np.float32)
+    zero = np.zeros_like(f_w)
+    # the f branch as the oracle computes it (f32, same padding)
+    f = oracle.conv3x3(x[0], f_w, f_b)[None]
+    elu = np.where(f > 0, f, np.expm1(np.minimum(f, 0)))
+    open_ = gated_conv(x, f_w, f_b, zero, np.full(24, 20.0, np.float32))
+    assert np.max(np.abs(open_ - elu)) <= 2e-2  # saturated gate: the elu branch (bf16 operands)
+    closed = gated_conv(x, f_w, f_b, zero, np.full(24, -20.0, np.float32))
+    assert np.max(np.abs(closed)) <= 1e-6      # closed gate
+    g_w = rng.normal(0, 0.2, (3, 3, 12, 24)).astype(np.float32)
+    g_b = rng.normal(0, 0.1, 24).astype(np.float32)
+    y = gated_conv(x, f_w, f_b, g_w, g_b)
+    ref = oracle.gated({"l.f_w": f_w, "l.f_b": f_b, "l.g_w": g_w, "l.g_b": g_b}, "l", x[0])[None]
+    assert y.shape == ref.shape
+    assert np.max(np.abs(y - ref)) <= 2e-2
+
+
+@pytest.mark.parametrize("base", [24, 12, 8])
+def test_forward_other_widths_vs_oracle(cuda, base):
+    """Widths whose N = 2*Cout hit the other kernel variants (N = 48/96/192 with a
+    5-row tile, 24, 16) against the f32 oracle."""
+    from paper_2407_19097_b200.neural import forward, init_params
+
+    cfg = _cfg(4, base, 11)
+    params = init_params(cfg)
+    x = np.random.default_rng(base).uniform(0, 1, (1, 80, 144, 4)).astype(np.float32)
+    y = forward(x, params, cfg)
+    ref = oracle.forward(x, params, cfg)
+    assert oracle.psnr(y, ref) >= PSNR_MIN
+    assert np.max(np.abs(y - ref)) <= MAX_ABS
