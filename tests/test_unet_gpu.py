@@ -198,3 +198,22 @@ def test_forward_other_widths_vs_oracle(cuda, base):
     ref = oracle.forward(x, params, cfg)
     assert oracle.psnr(y, ref) >= PSNR_MIN
     assert np.max(np.abs(y - ref)) <= MAX_ABS
+
+
+@pytest.mark.parametrize("cin,out_ch,head,levels", [(12, 3, True, 5), (7, 6, True, 5),
+                                                   (4, 3, False, 5), (4, 2, True, 4),
+                                                   (16, 1, True, 3)])
+def test_forward_config_variants_vs_oracle(cuda, cin, out_ch, head, levels):
+    """Input widths on the 8/16-channel head kernels, an unfused output head (> 4
+    outputs), no descriptor head, shallower pyramids."""
+    from paper_2407_19097_b200.neural import UNetConfig, forward, init_params
+
+    cfg = UNetConfig(input_channels=cin, output_channels=out_ch, use_descriptor_head=head,
+                     levels=levels, init_seed=cin)
+    params = init_params(cfg)
+    x = np.random.default_rng(cin).uniform(0, 1, (1, 64, 96, cin)).astype(np.float32)
+    y = forward(x, params, cfg)
+    ref = oracle.forward(x, params, cfg)
+    assert y.shape == ref.shape == (1, 64, 96, out_ch)
+    assert oracle.psnr(y, ref) >= PSNR_MIN
+    assert np.max(np.abs(y - ref)) <= MAX_ABS
