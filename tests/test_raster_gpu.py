@@ -346,3 +346,32 @@ def test_rasterize_thread_safe(cuda, golden):
         got = [f.result().data for f in futs]
     for i, g in enumerate(got):
         assert np.array_equal(g, serial[i % len(cases)])
+
+
+@pytest.mark.parametrize("case", ["wide_fov", "huge_width"])
+def test_exact_only_paths_vs_oracle(cuda, case, monkeypatch):
+    """Cameras outside the f32 pre-test bounds (170 deg FOV) or the certified-snap
+    bounds (70000 px wide: every point takes the exact f64 path), through the
+    forced multi-pass Hi-Z schedule -- keybufs bit-identical to the oracle."""
+    import os
+
+    import torch
+
+    from paper_2407_19097_b200.geometry import Intrinsics, look_at
+    from paper_2407_19097_b200.msr import DeviceCloud, Renderer
+
+    monkeypatch.setenv("NAR_RENDER_PASS_UNITS", "48")
+    rng = np.random.default_rng(99)
+    n = 600_000
+    pos = rng.uniform(-1, 1, (n, 3)).astype(np.float32)
+    if case == "wide_fov":
+        intr = Intrinsics(fov_y_deg=170.0, width=320, height=240)
+    else:
+        intr = Intrinsics(fov_y_deg=40.0, width=70000, height=3)
+    cam = look_at((0.3, -2.5, 0.7), (0, 0, 0), intr)
+    r = Renderer(intr.width, intr.height, device=cuda)
+    r.render(DeviceCloud.from_tensors(torch.from_numpy(pos).to(cuda)), cam)
+    i = cam.intrinsics
+    ref = oracle.zbuffer_render(pos, cam.orientation, cam.position, i.focal_px, i.cx, i.cy,
+                                i.near, i.far, i.width, i.height, threads=os.cpu_count() or 4)
+    assert np.array_equal(r.keys(), ref)
