@@ -273,8 +273,9 @@ __device__ __forceinline__ void fold_loaded(uint64_t* keybuf, uint32_t pix, uint
 }
 
 // ----------------------------------------------------------------------------
-// render: persistent CTAs, every warp streams its own 128-point chunks through
-// a private ring of TMA bulk copies (no cross-warp coupling on the data path)
+// render: persistent CTAs, every warp streams its own point chunks (64 points in
+// the exact kernel, 128-point units in the pre-test kernel) through a private
+// ring of TMA bulk copies (no cross-warp coupling on the data path)
 // ----------------------------------------------------------------------------
 #ifndef NAR_RENDER_WARPS
 #define NAR_RENDER_WARPS 24
@@ -346,13 +347,15 @@ __device__ __forceinline__ void flush_queue(const QEntry* q, int n, int lane, ui
   __syncwarp();
 }
 
-// Per warp step (one 128-point chunk, 4 points per lane):
+// Exact kernel (seed pass, small clouds, cameras outside the pre-test bounds).
+// Per warp step (one 64-point chunk, 2 points per lane):
 // (1) certified fast projection; uncertain points go to the warp's queue and
 //     are re-projected exactly once 32 have gathered;
 // (2) Hi-Z test against the smem coarse depth -- occluded points stop here;
 // (3) hand the ring slot back to TMA (chunk k + kWarpStages);
-// (4) fold the PREVIOUS chunk's survivors, whose keybuf reads were issued one
-//     step ago, so the random-L2 read latency overlaps a chunk of math;
+// (4) kRed (seed pass): atomicMin (RED) every hit; otherwise fold the PREVIOUS
+//     chunk's hits, whose keybuf reads were issued one step ago, so the
+//     random-L2 read latency overlaps a chunk of math, and
 // (5) issue this chunk's keybuf reads.
 template <bool kSigned, bool kRed>
 __global__ void __launch_bounds__(kRenderThreads, 1)
@@ -435,7 +438,7 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
     for (int j = 0; j < kPtsPerThread; ++j)
       project_fast(px[j], py[j], pz[j], cam, ixs[j], iys[j], dbs[j], hits[j], uncs[j]);
 
-    // (2) Hi-Z, optional warp pre-dedup of same-pixel hits, uncertain queue
+    // (2) Hi-Z test, uncertain queue
     uint32_t pix[kPtsPerThread], idxs[kPtsPerThread];
     uint64_t key[kPtsPerThread];
     uint32_t okmask = 0, umask = 0;
