@@ -322,9 +322,11 @@ static Plan make_plan(const nar_unet& n, int H, int W) {
     const size_t px = (size_t)p.H[k] * p.W[k];
     const int w = stride_of(n.cfg, k);
     p.off_pyr16[k] = take(px * p.cinp * 2);
-    p.off_skip[k] = take(px * w * 2);
+    // off_x[k] (k >= 1) and the bottleneck off_skip[L-1] feed an up2 and are
+    // written wide (H, 2W) on the tensor-core path
+    p.off_skip[k] = take(px * w * 2 * (k + 1 == p.L ? 2 : 1));
     p.off_tmp[k] = take(px * w * 2);
-    p.off_x[k] = take(px * w * 2);
+    p.off_x[k] = take(px * w * 2 * (k > 0 ? 2 : 1));
     p.off_pool[k] = k + 1 < p.L ? take(px / 4 * w * 2) : 0;
   }
   p.total = off + 256;
@@ -375,7 +377,8 @@ static int upload(nar_unet* n) {
 static int run_conv(nar_unet* n, Layer& l, const __nv_bfloat16* src_a, int ca_stride, int a_up2,
                     const __nv_bfloat16* src_b, int cb_stride, int H, int W,
                     __nv_bfloat16* out, cudaStream_t st, __nv_bfloat16* pool_out = nullptr,
-                    float* head_out = nullptr, __nv_bfloat16* scratch = nullptr) {
+                    float* head_out = nullptr, __nv_bfloat16* scratch = nullptr,
+                    int out_wide = 0) {
   ConvArgs a;
   memset(&a, 0, sizeof(a));
   a.src_a = src_a;
@@ -385,6 +388,7 @@ static int run_conv(nar_unet* n, Layer& l, const __nv_bfloat16* src_a, int ca_st
   a.ca_stride = ca_stride;
   a.cb_stride = cb_stride;
   a.a_up2 = a_up2;
+  a.out_wide = out_wide;
   a.H = H;
   a.W = W;
   a.cout = l.cout;
@@ -621,6 +625,7 @@ int nar_unet_forward(nar_unet* n, const float* in, int32_t H, int32_t W, float* 
     if ((rc = check_launch("head_pyramid"))) return rc;
   }
 
+  const bool wide = !n->simt;  // up2 sources written pre-repeated (see ConvArgs::a_up2)
   int li = 0;
   for (int k = 0; k < L; ++k) {
     Layer& la = n->layers[li++];
@@ -637,20 +642,20 @@ int nar_unet_forward(nar_unet* n, const float* in, int32_t H, int32_t W, float* 
     rc = run_conv(n, lb, bf(p.off_tmp[k]), stride_of(n->cfg, k), 0, nullptr, 0, p.H[k], p.W[k],
                   last ? nullptr : bf(p.off_skip[k]), st,
                   k + 1 < L ? bf(p.off_pool[k]) : nullptr, last ? out : nullptr,
-                  bf(p.off_skip[k]));
+                  bf(p.off_skip[k]), wide && !last && k + 1 == L);
     if (rc) return rc;
   }
   const __nv_bfloat16* x = bf(p.off_skip[L - 1]);
   for (int k = L - 2; k >= 0; --k) {
     Layer& la = n->layers[li++];
     Layer& lb = n->layers[li++];
-    rc = run_conv(n, la, x, stride_of(n->cfg, k + 1), 1, bf(p.off_skip[k]), stride_of(n->cfg, k),
-                  p.H[k], p.W[k], bf(p.off_tmp[k]), st);
+    rc = run_conv(n, la, x, stride_of(n->cfg, k + 1), wide ? 2 : 1, bf(p.off_skip[k]),
+                  stride_of(n->cfg, k), p.H[k], p.W[k], bf(p.off_tmp[k]), st);
     if (rc) return rc;
     // dec0b: the out head (1x1 conv + sigmoid) is fused into the epilogue
     rc = run_conv(n, lb, bf(p.off_tmp[k]), stride_of(n->cfg, k), 0, nullptr, 0, p.H[k], p.W[k],
                   k == 0 ? nullptr : bf(p.off_x[k]), st, nullptr, k == 0 ? out : nullptr,
-                  bf(p.off_x[k]));
+                  bf(p.off_x[k]), wide && k > 0);
     if (rc) return rc;
     x = bf(p.off_x[k]);
   }

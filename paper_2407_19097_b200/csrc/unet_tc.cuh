@@ -6,24 +6,25 @@
 //   M = pixels (tiles of R image rows x 128 pixels),  N = 2*Coutp (f | g),
 //   K = 9 taps x input channels (16-channel chunks).
 //
-// CTA roles (288 threads, 1 CTA per SM, persistent over tiles):
-//   warps 0-3  producer.  Lane 0 of warp 0 issues, per (tile, 16-channel
-//              chunk) stage, two TMA tensor loads (one per 8-channel slab) of
-//              the (R+2) x 130 pixel halo straight into the UMMA no-swizzle
+// CTA roles (576 threads, 1 CTA per SM, persistent over tiles):
+//   warp 0     producer.  One lane issues, per (tile, 16-channel chunk)
+//              stage, two TMA tensor loads (one per 8-channel slab) of the
+//              (R+2) x 130 pixel halo straight into the UMMA no-swizzle
 //              K-major layout [k8][row][px][16 B]; TMA zero-fills the image
 //              border ("same" padding) and the concat is just a second tensor
-//              map.  For the decoder's up2(srcA) chunks the low-resolution
-//              halo is TMA-loaded into a staging area and the 128 producer
-//              threads replicate it 2x2 into the halo.  A TMA bulk copy
-//              streams the chunk's pre-packed weights.
-//   warp 8     MMA issuer (one elected thread) + TMEM owner: for each of the
-//              9 taps and R rows one tcgen05.mma (M=128, N, K=16) whose A
-//              descriptor is the halo row shifted by the tap (a 16-byte start
-//              address offset: pixels are contiguous 16 B rows, SBO = 128 B).
-//   warps 4-7  epilogue: tcgen05.ld the f and g accumulators of their TMEM
-//              lane quarter, apply the gate; store bf16 NHWC, and optionally
-//              the 2x2 average pool of the output (encoder skips feeding the
-//              next level) and/or the final 1x1 out head + sigmoid
+//              map.  The decoder's up2(srcA) chunks come from a "wide" tensor
+//              (the previous layer stored every pixel twice, ConvArgs::a_up2 = 2),
+//              so they are plain TMA boxes of the LR low-res rows; the vertical
+//              repeat is the MMA's row addressing.  A TMA bulk copy streams the
+//              chunk's pre-packed weights.
+//   warp 17    MMA issuer (one thread) + TMEM owner: tcgen05.mma (M=128, N,
+//              K=16) whose A descriptor is a halo row shifted by the tap (a
+//              16-byte start-address offset: pixels are contiguous 16 B rows,
+//              SBO = 128 B); narrow layers slide (see tc_slide).
+//   warps 1-16 epilogue: tcgen05.ld the f and g accumulators of their TMEM
+//              lane quarter, apply the gate; store bf16 NHWC (or wide), and
+//              optionally the 2x2 average pool of the output (encoder skips
+//              feeding the next level) and/or the final 1x1 out head + sigmoid
 //              (model.py:189-191) in f32 instead of the bf16 activation.
 // Accumulators are double buffered in TMEM (2 x R x N <= 512 columns) so the
 // epilogue of tile i overlaps the MMAs of tile i+1.
@@ -45,8 +46,14 @@ namespace nar {
 struct ConvArgs {
   const __nv_bfloat16* src_a;  // NHWC, channel stride ca_stride (multiple of 16)
   const __nv_bfloat16* src_b;  // NHWC, channel stride cb_stride, or NULL
-  int ca, cb, ca_stride, cb_stride, a_up2;
+  int ca, cb, ca_stride, cb_stride;
+  // a_up2: srcA is nearest-upsampled 2x.  1 = srcA is (H/2, W/2) (SIMT path);
+  // 2 = srcA is "wide" (H/2, W): its producer already repeated every pixel
+  // horizontally (out_wide), so the tensor-core path TMA-loads it directly and
+  // resolves the vertical repeat by descriptor row addressing.
+  int a_up2;
   int H, W;                    // output (and src_b) resolution
+  int out_wide;                // tensor-core path: write out as (H, 2W), each pixel twice
   int cout, cout_stride;       // real output channels, output channel stride
   const float* wf32;           // SIMT path: HWIO f32
   const float* wg32;
@@ -65,14 +72,13 @@ struct ConvArgs {
   float head_bv[4];
 };
 
-constexpr int kProdWarps = 2;   // TMA issue + staging reshape
+constexpr int kProdWarps = 1;   // TMA issue (one lane)
 constexpr int kProdThreads = kProdWarps * 32;
 constexpr int kEpiGroups = 4;   // epilogue warps per TMEM lane quarter
 constexpr int kMmaWarp = kProdWarps + 4 * kEpiGroups;
-constexpr int kTcThreads = (kMmaWarp + 1) * 32;  // 2 producer + 16 epilogue + 1 MMA warps
+constexpr int kTcThreads = (kMmaWarp + 1) * 32;  // 1 producer + 16 epilogue + 1 MMA warps
 constexpr int kHaloPx = 130;
 constexpr int kHaloRowBytes = kHaloPx * 16;  // one 8-channel slab row
-constexpr int kLowPx = 66;                   // low-res pixels behind a 130-px halo
 
 __host__ __device__ constexpr int tc_rows(int N) { return N >= 256 ? 1 : (256 / N > 8 ? 8 : 256 / N); }
 __host__ __device__ constexpr int tc_low_rows(int N) { return tc_rows(N) / 2 + 2; }
@@ -81,15 +87,7 @@ __host__ __device__ constexpr int tc_r128(int x) { return (x + 127) / 128 * 128;
 __host__ __device__ constexpr int tc_slab(int N) { return tc_r128((tc_rows(N) + 2) * kHaloRowBytes); }
 __host__ __device__ constexpr int tc_a_bytes(int N) { return 2 * tc_slab(N); }
 __host__ __device__ constexpr int tc_b_bytes(int N) { return 9 * N * 32; }
-// staging: one TMA box of whole 16-channel chunks (32 B per pixel), either the
-// (R+2) x 130 halo or, for up2 sources, the low-res (LR x 66) halo
-__host__ __device__ constexpr int tc_stg_bytes(int N) { return tc_r128(tc_low_rows(N) * kLowPx * 32); }
 __host__ __device__ constexpr int tc_stage_bytes(int N) { return tc_a_bytes(N) + tc_b_bytes(N); }
-__host__ __device__ constexpr int tc_stages(int N) {
-  return (200 * 1024 - 2 * tc_stg_bytes(N)) / tc_stage_bytes(N) > 4
-             ? 4
-             : (200 * 1024 - 2 * tc_stg_bytes(N)) / tc_stage_bytes(N);
-}
 constexpr int kTcParamFloats = 3 * 144 + 128 * 4 + 4;  // bias_f, bias_f*log2e, bias_g/2, head_w, head_b
 // Narrow layers (N <= 48) use "sliding" MMAs: one MMA per (halo row, kx) with
 // the three ky weight blocks stacked along N (N' = 3N) accumulates into three
@@ -98,9 +96,20 @@ constexpr int kTcParamFloats = 3 * 144 + 128 * 4 + 4;  // bias_f, bias_f*log2e, 
 // Accumulators are zeroed first by one MMA with zero operands (kTcZeroBytes).
 __host__ __device__ constexpr bool tc_slide(int N) { return N <= 64; }
 constexpr int kTcZeroBytes = 256 * 32;  // B: 256 rows x K16 bf16 (A uses its first 4 KB)
+__host__ __device__ constexpr int tc_fixed_smem(int N) {
+  return 512 + kTcParamFloats * 4 + (tc_slide(N) ? kTcZeroBytes : 0);
+}
+// stages: as many (<= NAR_TC_MAX_STAGES) as fit the 227 KB opt-in shared memory
+#ifndef NAR_TC_MAX_STAGES
+#define NAR_TC_MAX_STAGES 3
+#endif
+__host__ __device__ constexpr int tc_stages(int N) {
+  return (227 * 1024 - tc_fixed_smem(N)) / tc_stage_bytes(N) > NAR_TC_MAX_STAGES
+             ? NAR_TC_MAX_STAGES
+             : (227 * 1024 - tc_fixed_smem(N)) / tc_stage_bytes(N);
+}
 __host__ __device__ constexpr int tc_smem(int N) {
-  return tc_stages(N) * tc_stage_bytes(N) + 2 * tc_stg_bytes(N) + 512 + kTcParamFloats * 4 +
-         (tc_slide(N) ? kTcZeroBytes : 0);
+  return tc_stages(N) * tc_stage_bytes(N) + tc_fixed_smem(N);
 }
 
 // Host: pack HWIO f32 weights into bf16 [chunk q][tap][k8][n][8] where
@@ -266,26 +275,24 @@ __global__ void __maxnreg__(96)
   constexpr int S = tc_stages(N);
   constexpr int A_BYTES = tc_a_bytes(N);
   constexpr int B_BYTES = tc_b_bytes(N);
-  constexpr int STG_BYTES = tc_stg_bytes(N);
   constexpr int STAGE = tc_stage_bytes(N);
   constexpr int SLAB = tc_slab(N);
-  static_assert(A_BYTES % 128 == 0 && B_BYTES % 128 == 0 && STG_BYTES % 128 == 0, "align");
+  static_assert(A_BYTES % 128 == 0 && B_BYTES % 128 == 0, "align");
   constexpr uint32_t A_TX = 2u * (R + 2) * kHaloPx * 16;  // bytes of the two direct slab boxes
-  constexpr uint32_t LOW_TX = LR * kLowPx * 32;          // bytes of an up2 low-res box
+  constexpr uint32_t UP_TX = 2u * LR * kHaloPx * 16;      // ... of the two wide up2 slab boxes
   constexpr int COUTP = N / 2;
   constexpr uint32_t IDESC = umma_idesc_bf16(128, N);
   static_assert(2 * R * N <= 512, "TMEM budget");
   static_assert(S >= 2, "pipeline depth");
 
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* stg_buf = smem + S * STAGE;  // 2 staging buffers
-  uint64_t* full = reinterpret_cast<uint64_t*>(stg_buf + 2 * STG_BYTES);
+  uint8_t* fixed = smem + S * STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(fixed);
   uint64_t* empty = full + S;
-  uint64_t* stg = empty + S;  // 2 used
-  uint64_t* tfull = stg + S;
+  uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
   uint32_t* tbase_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  float* sbias_f = reinterpret_cast<float*>(stg_buf + 2 * STG_BYTES + 512);
+  float* sbias_f = reinterpret_cast<float*>(fixed + 512);
   float* sbias_fl = sbias_f + 144;
   float* sbias_gh = sbias_fl + 144;
   float* shead_w = sbias_gh + 144;
@@ -301,9 +308,8 @@ __global__ void __maxnreg__(96)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 2);
+      mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
-      mbar_init(&stg[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
@@ -342,112 +348,30 @@ __global__ void __maxnreg__(96)
 
   if (warp < kProdWarps) {
     // ------------------------------ producer ------------------------------
-    // Stage `it` = (tile, chunk q).  Direct chunks: lane 0 of warp 0 TMA-loads
-    // the two 8-channel slabs of the (R+2) x 130 halo straight into the UMMA
-    // layout [k8][row][px][16 B] and streams the weights.  up2 chunks: the
-    // low-res halo (whole 16-channel pixels) is TMA-loaded into a double-
-    // buffered staging area one up2 stage ahead, and the producer threads
-    // replicate it 2x2 into the halo layout.
-    const int t = threadIdx.x;
-    const int my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    const int n_it = my_tiles * nq;
-    auto is_up2 = [&](int j) { return a.a_up2 && (j % nq) < nqa; };
-    auto next_up2 = [&](int j) {
-      for (++j; j < n_it; ++j)
-        if (is_up2(j)) return j;
-      return n_it;
-    };
-    auto issue_staging = [&](int j, int bsel) {
-      const int tile = blockIdx.x + (j / nq) * gridDim.x, q = j % nq;
-      const int y0 = (tile / tiles_x) * R, x0 = (tile % tiles_x) * 128;
-      mbar_expect_tx(&stg[bsel], LOW_TX);
-      tma_load_3d(stg_buf + bsel * STG_BYTES, &tma_a, 16 * q, (x0 - 1) >> 1, (y0 - 1) >> 1,
-                  &stg[bsel]);
-    };
-    int u = 0;  // up2 stages seen so far: staging buffer u & 1, parity (u >> 1) & 1
-    if (t == 0) {
-      const int j0 = next_up2(-1);
-      if (j0 < n_it) issue_staging(j0, 0);
-    }
-    for (int it = 0; it < n_it; ++it) {
-      const int tile = blockIdx.x + (it / nq) * gridDim.x, q = it % nq;
-      const int y0 = (tile / tiles_x) * R, x0 = (tile % tiles_x) * 128;
-      const int s = it % S;
-      const uint32_t ph = (uint32_t)(it / S) & 1u;
-      uint8_t* stA = smem + s * STAGE;
-      uint8_t* stB = stA + A_BYTES;
-      if (!is_up2(it)) {
-        // Every producer thread observes every phase of empty[s]: parity waits
-        // are only valid one phase ahead, so skipping a stage here would let a
-        // later wait succeed on a stale phase.
-        if (t != 0) mbar_wait(&empty[s], ph ^ 1u);
-        if (t == 0) {
-          const bool in_a = q < nqa;
-          const int cbase = 16 * (in_a ? q : q - nqa);
-          const CUtensorMap* map = in_a ? &tma_a : &tma_b;
-          mbar_wait(&empty[s], ph ^ 1u);
-          mbar_expect_tx(&full[s], A_TX + B_BYTES);
-          tma_load_3d(stA, map, cbase, x0 - 1, y0 - 1, &full[s]);
-          tma_load_3d(stA + SLAB, map, cbase + 8, x0 - 1, y0 - 1, &full[s]);
-          bulk_g2s(stB, a.wtc + (size_t)q * (B_BYTES / 2), B_BYTES, &full[s]);
-          mbar_arrive(&full[s]);
-        }
-        continue;
+    // Stage `it` = (tile, 16-channel chunk q).  One lane TMA-loads the two
+    // 8-channel slabs of the halo straight into the UMMA layout
+    // [k8][row][px][16 B] -- (R+2) x 130 pixels of a direct source, or for a
+    // wide up2 source the LR low-res rows behind them (already repeated
+    // horizontally, so 130 wide pixels per row) -- plus the chunk's weights.
+    if (lane == 0) {
+      const int my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+      const int n_it = my_tiles * nq;
+      for (int it = 0; it < n_it; ++it) {
+        const int tile = blockIdx.x + (it / nq) * gridDim.x, q = it % nq;
+        const int y0 = (tile / tiles_x) * R, x0 = (tile % tiles_x) * 128;
+        const int s = it % S;
+        uint8_t* stA = smem + s * STAGE;
+        const bool in_a = q < nqa;
+        const bool up = in_a && a.a_up2;
+        const int cbase = 16 * (in_a ? q : q - nqa);
+        const CUtensorMap* map = in_a ? &tma_a : &tma_b;
+        const int yr = up ? (y0 - 1) >> 1 : y0 - 1;  // arithmetic shift: row -1 stays OOB
+        mbar_wait(&empty[s], ((uint32_t)(it / S) & 1u) ^ 1u);
+        mbar_expect_tx(&full[s], (up ? UP_TX : A_TX) + B_BYTES);
+        tma_load_3d(stA, map, cbase, x0 - 1, yr, &full[s]);
+        tma_load_3d(stA + SLAB, map, cbase + 8, x0 - 1, yr, &full[s]);
+        bulk_g2s(stA + A_BYTES, a.wtc + (size_t)q * (B_BYTES / 2), B_BYTES, &full[s]);
       }
-      const uint8_t* buf = stg_buf + (u & 1) * STG_BYTES;
-      if (t == 0) {
-        const int j2 = next_up2(it);
-        if (j2 < n_it) issue_staging(j2, (u + 1) & 1);  // overlaps this stage's replication
-        mbar_wait(&empty[s], ph ^ 1u);
-        mbar_expect_tx(&full[s], B_BYTES);
-        bulk_g2s(stB, a.wtc + (size_t)q * (B_BYTES / 2), B_BYTES, &full[s]);
-      }
-      mbar_wait(&empty[s], ph ^ 1u);
-      mbar_wait(&stg[u & 1], (uint32_t)(u >> 1) & 1u);
-      {
-        // 2x2 replication: halo (row, j) <- low-res (ly, lx)
-        // fully unrolled: all loads of a row pair in flight before the stores
-        const int ly0 = (y0 - 1) >> 1, lx0 = (x0 - 1) >> 1;
-        constexpr int JIT = (kHaloPx + kProdThreads - 1) / kProdThreads;
-        int lxs[JIT];
-#pragma unroll
-        for (int i = 0; i < JIT; ++i) {
-          const int j = t + i * kProdThreads;
-          lxs[i] = ((x0 - 1 + (j < kHaloPx ? j : 0)) >> 1) - lx0;
-        }
-#pragma unroll
-        for (int row = 0; row < R + 2; row += 2) {
-          uint4 v[2][JIT][2];
-#pragma unroll
-          for (int rr = 0; rr < 2; ++rr) {
-            const int ly = ((y0 - 1 + row + rr) >> 1) - ly0;
-            const uint8_t* srow = buf + ly * (kLowPx * 32);
-#pragma unroll
-            for (int i = 0; i < JIT; ++i) {
-              if (row + rr < R + 2 && t + i * kProdThreads < kHaloPx) {
-                v[rr][i][0] = *reinterpret_cast<const uint4*>(srow + lxs[i] * 32);
-                v[rr][i][1] = *reinterpret_cast<const uint4*>(srow + lxs[i] * 32 + 16);
-              }
-            }
-          }
-#pragma unroll
-          for (int rr = 0; rr < 2; ++rr) {
-            uint8_t* d0 = stA + (row + rr) * kHaloRowBytes;
-#pragma unroll
-            for (int i = 0; i < JIT; ++i) {
-              const int j = t + i * kProdThreads;
-              if (row + rr < R + 2 && j < kHaloPx) {
-                *reinterpret_cast<uint4*>(d0 + j * 16) = v[rr][i][0];
-                *reinterpret_cast<uint4*>(d0 + SLAB + j * 16) = v[rr][i][1];
-              }
-            }
-          }
-        }
-      }
-      ++u;
-      fence_proxy_async_smem();
-      asm volatile("bar.sync 1, %0;" ::"n"(kProdThreads) : "memory");
-      if (t == 0) mbar_arrive(&full[s]);
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------ MMA issuer -----------------------------
@@ -457,7 +381,12 @@ __global__ void __maxnreg__(96)
       mbar_wait(&tempty[b], (((uint32_t)tl >> 1) & 1u) ^ 1u);
       tc_fence_after();
       const uint32_t dcol = tbase + (uint32_t)(b * R * N);
+      const int y0 = (tile / tiles_x) * R;
       for (int q = 0; q < nq; ++q, ++it) {
+        // halo row h -> smem row (h + par) >> sh: a wide up2 chunk holds each
+        // low-res row once, and image row y0-1+h reads low-res row (y0-1+h) >> 1
+        const bool up = a.a_up2 && q < nqa;
+        const int sh = up ? 1 : 0, par = up ? ((y0 - 1) & 1) : 0;
         const int s = it % S;
         mbar_wait(&full[s], (uint32_t)(it / S) & 1u);
         tc_fence_after();
@@ -480,7 +409,8 @@ __global__ void __maxnreg__(96)
                 const int kymin = h - (R - 1) > 0 ? h - (R - 1) : 0;
                 const int nb = kymax - kymin + 1;
                 const uint64_t bdesc = umma_desc(bk + (2 - kymax) * N * 16, 3 * N * 16, 128);
-                const uint64_t adesc = umma_desc(sa + h * kHaloRowBytes + kx * 16, SLAB, 128);
+                const uint64_t adesc =
+                    umma_desc(sa + ((h + par) >> sh) * kHaloRowBytes + kx * 16, SLAB, 128);
                 umma_bf16(dcol + (h - kymax) * N, adesc, bdesc, umma_idesc_bf16(128, nb * N), 1u);
               }
             }
@@ -492,7 +422,7 @@ __global__ void __maxnreg__(96)
 #pragma unroll
               for (int r = 0; r < R; ++r) {
                 const uint64_t adesc =
-                    umma_desc(sa + (r + ky) * kHaloRowBytes + kx * 16, SLAB, 128);
+                    umma_desc(sa + ((r + ky + par) >> sh) * kHaloRowBytes + kx * 16, SLAB, 128);
                 umma_bf16(dcol + r * N, adesc, bdesc, IDESC, (q > 0 || tap > 0) ? 1u : 0u);
               }
             }
@@ -595,7 +525,12 @@ __global__ void __maxnreg__(96)
                 __nv_bfloat162 hh = __floats2bfloat162_rn(o[h][e], o[h][e + 1]);
                 pw[e / 2] = *reinterpret_cast<uint32_t*>(&hh);
               }
-              *reinterpret_cast<uint4*>(a.out + ((size_t)y * a.W + x) * a.cout_stride + c0) = pk;
+              // wide (H, 2W) output: the consumer's horizontal up2 repeat
+              const int wsh = a.out_wide;
+              uint4* d = reinterpret_cast<uint4*>(
+                  a.out + (((size_t)y * a.W + x) << wsh) * a.cout_stride + c0);
+              *d = pk;
+              if (wsh) d[a.cout_stride / 8] = pk;
             }
             if (do_head) {
 #pragma unroll
@@ -718,8 +653,11 @@ static int tc_launch_nh(const ConvArgs& a, cudaStream_t st) {
   if (a.pool_out && (R & 1)) return set_error(NAR_ERR_CONFIG, "fused pool needs an even row tile");
   CUtensorMap ma, mb;
   int rc;
-  if (a.a_up2)
-    rc = tc_make_map(&ma, a.src_a, a.ca_stride, a.W / 2, a.H / 2, 16, kLowPx, tc_low_rows(N));
+  if (a.a_up2 == 1) return set_error(NAR_ERR_CONFIG, "tensor-core up2 needs a wide source");
+  if (a.out_wide && (a.pool_out || a.head_out))
+    return set_error(NAR_ERR_CONFIG, "wide output cannot be pooled or headed");
+  if (a.a_up2)  // wide (H/2, W) source: LR low-res rows, 130 wide pixels
+    rc = tc_make_map(&ma, a.src_a, a.ca_stride, a.W, a.H / 2, 8, kHaloPx, tc_low_rows(N));
   else
     rc = tc_make_map(&ma, a.src_a, a.ca_stride, a.W, a.H, 8, kHaloPx, R + 2);
   if (rc) return rc;
