@@ -8,9 +8,9 @@
 //
 // CTA roles (576 threads, 1 CTA per SM, persistent over tiles):
 //   warp 0     producer.  One lane issues, per (tile, 16-channel chunk)
-//              stage, two TMA tensor loads (one per 8-channel slab) of the
-//              (R+2) x 130 pixel halo straight into the UMMA no-swizzle
-//              K-major layout [k8][row][px][16 B]; TMA zero-fills the image
+//              stage, one TMA tensor load of the (R+2) x 136 pixel halo
+//              (32 B per pixel) straight into the UMMA SWIZZLE_32B K-major
+//              layout [row][px][32 B]; TMA zero-fills the image
 //              border ("same" padding) and the concat is just a second tensor
 //              map.  The decoder's up2(srcA) chunks come from a "wide" tensor
 //              (the previous layer stored every pixel twice, ConvArgs::a_up2 = 2),
@@ -77,17 +77,18 @@ constexpr int kProdThreads = kProdWarps * 32;
 constexpr int kEpiGroups = 4;   // epilogue warps per TMEM lane quarter
 constexpr int kMmaWarp = kProdWarps + 4 * kEpiGroups;
 constexpr int kTcThreads = (kMmaWarp + 1) * 32;  // 1 producer + 16 epilogue + 1 MMA warps
-constexpr int kHaloPx = 130;
-constexpr int kHaloRowBytes = kHaloPx * 16;  // one 8-channel slab row
+constexpr int kHaloPx = 130;                 // pixels a tile row reads (128 + 2 halo)
+constexpr int kHaloPitch = 136;              // loaded per row: 136 x 32 B = 17 swizzle atoms
+constexpr int kHaloRowBytes = kHaloPitch * 32;  // one 16-channel halo row, SWIZZLE_32B
 
 __host__ __device__ constexpr int tc_rows(int N) { return N >= 256 ? 1 : (256 / N > 8 ? 8 : 256 / N); }
 __host__ __device__ constexpr int tc_low_rows(int N) { return tc_rows(N) / 2 + 2; }
 // TMA tensor-load destinations must be 128-byte aligned: slabs are padded.
 __host__ __device__ constexpr int tc_r128(int x) { return (x + 127) / 128 * 128; }
-__host__ __device__ constexpr int tc_slab(int N) { return tc_r128((tc_rows(N) + 2) * kHaloRowBytes); }
-__host__ __device__ constexpr int tc_a_bytes(int N) { return 2 * tc_slab(N); }
+__host__ __device__ constexpr int tc_r1024(int x) { return (x + 1023) / 1024 * 1024; }
+__host__ __device__ constexpr int tc_a_bytes(int N) { return tc_r1024((tc_rows(N) + 2) * kHaloRowBytes); }
 __host__ __device__ constexpr int tc_b_bytes(int N) { return 9 * N * 32; }
-__host__ __device__ constexpr int tc_stage_bytes(int N) { return tc_a_bytes(N) + tc_b_bytes(N); }
+__host__ __device__ constexpr int tc_stage_bytes(int N) { return tc_r1024(tc_a_bytes(N) + tc_b_bytes(N)); }
 constexpr int kTcParamFloats = 3 * 144 + 128 * 4 + 4;  // bias_f, bias_f*log2e, bias_g/2, head_w, head_b
 // Narrow layers (N <= 48) use "sliding" MMAs: one MMA per (halo row, kx) with
 // the three ky weight blocks stacked along N (N' = 3N) accumulates into three
@@ -162,6 +163,19 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
   d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
   d |= (uint64_t)1 << 46;
+  return d;
+}
+
+// SWIZZLE_32B K-major (the TMA-written halo): rows of 32 B (K = 16 bf16),
+// 8-row atoms of 256 B (SBO), LBO unused, layout type 6 at [61,64).  The start
+// may sit at any 32-byte row: the XOR pattern follows absolute address bits.
+__device__ __forceinline__ uint64_t umma_desc_sw32(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(256 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)6 << 61;
   return d;
 }
 
@@ -276,10 +290,9 @@ __global__ void __maxnreg__(96)
   constexpr int A_BYTES = tc_a_bytes(N);
   constexpr int B_BYTES = tc_b_bytes(N);
   constexpr int STAGE = tc_stage_bytes(N);
-  constexpr int SLAB = tc_slab(N);
   static_assert(A_BYTES % 128 == 0 && B_BYTES % 128 == 0, "align");
-  constexpr uint32_t A_TX = 2u * (R + 2) * kHaloPx * 16;  // bytes of the two direct slab boxes
-  constexpr uint32_t UP_TX = 2u * LR * kHaloPx * 16;      // ... of the two wide up2 slab boxes
+  constexpr uint32_t A_TX = (R + 2) * kHaloRowBytes;  // bytes of a direct halo box
+  constexpr uint32_t UP_TX = LR * kHaloRowBytes;      // ... of a wide up2 halo box
   constexpr int COUTP = N / 2;
   constexpr uint32_t IDESC = umma_idesc_bf16(128, N);
   static_assert(2 * R * N <= 512, "TMEM budget");
@@ -348,9 +361,10 @@ __global__ void __maxnreg__(96)
 
   if (warp < kProdWarps) {
     // ------------------------------ producer ------------------------------
-    // Stage `it` = (tile, 16-channel chunk q).  One lane TMA-loads the two
-    // 8-channel slabs of the halo straight into the UMMA layout
-    // [k8][row][px][16 B] -- (R+2) x 130 pixels of a direct source, or for a
+    // Stage `it` = (tile, 16-channel chunk q).  One lane TMA-loads the halo
+    // straight into the UMMA SWIZZLE_32B layout [row][px][32 B] -- (R+2) x 136
+    // pixels of a direct source (one box: 32-byte rows cost the TMA unit half
+    // the row operations of two 16-byte slabs), or for a
     // wide up2 source the LR low-res rows behind them (already repeated
     // horizontally, so 130 wide pixels per row) -- plus the chunk's weights.
     if (lane == 0) {
@@ -369,7 +383,6 @@ __global__ void __maxnreg__(96)
         mbar_wait(&empty[s], ((uint32_t)(it / S) & 1u) ^ 1u);
         mbar_expect_tx(&full[s], (up ? UP_TX : A_TX) + B_BYTES);
         tma_load_3d(stA, map, cbase, x0 - 1, yr, &full[s]);
-        tma_load_3d(stA + SLAB, map, cbase + 8, x0 - 1, yr, &full[s]);
         bulk_g2s(stA + A_BYTES, a.wtc + (size_t)q * (B_BYTES / 2), B_BYTES, &full[s]);
       }
     }
@@ -410,7 +423,7 @@ __global__ void __maxnreg__(96)
                 const int nb = kymax - kymin + 1;
                 const uint64_t bdesc = umma_desc(bk + (2 - kymax) * N * 16, 3 * N * 16, 128);
                 const uint64_t adesc =
-                    umma_desc(sa + ((h + par) >> sh) * kHaloRowBytes + kx * 16, SLAB, 128);
+                    umma_desc_sw32(sa + ((h + par) >> sh) * kHaloRowBytes + kx * 32);
                 umma_bf16(dcol + (h - kymax) * N, adesc, bdesc, umma_idesc_bf16(128, nb * N), 1u);
               }
             }
@@ -422,7 +435,7 @@ __global__ void __maxnreg__(96)
 #pragma unroll
               for (int r = 0; r < R; ++r) {
                 const uint64_t adesc =
-                    umma_desc(sa + ((r + ky + par) >> sh) * kHaloRowBytes + kx * 16, SLAB, 128);
+                    umma_desc_sw32(sa + ((r + ky + par) >> sh) * kHaloRowBytes + kx * 32);
                 umma_bf16(dcol + r * N, adesc, bdesc, IDESC, (q > 0 || tap > 0) ? 1u : 0u);
               }
             }
@@ -629,7 +642,7 @@ static int tc_make_map(CUtensorMap* m, const void* base, int cs, int w, int h, i
   cuuint32_t box[3] = {(cuuint32_t)bc, (cuuint32_t)bw, (cuuint32_t)bh};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
-                  box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(NAR_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   return NAR_OK;
@@ -657,12 +670,12 @@ static int tc_launch_nh(const ConvArgs& a, cudaStream_t st) {
   if (a.out_wide && (a.pool_out || a.head_out))
     return set_error(NAR_ERR_CONFIG, "wide output cannot be pooled or headed");
   if (a.a_up2)  // wide (H/2, W) source: LR low-res rows, 130 wide pixels
-    rc = tc_make_map(&ma, a.src_a, a.ca_stride, a.W, a.H / 2, 8, kHaloPx, tc_low_rows(N));
+    rc = tc_make_map(&ma, a.src_a, a.ca_stride, a.W, a.H / 2, 16, kHaloPitch, tc_low_rows(N));
   else
-    rc = tc_make_map(&ma, a.src_a, a.ca_stride, a.W, a.H, 8, kHaloPx, R + 2);
+    rc = tc_make_map(&ma, a.src_a, a.ca_stride, a.W, a.H, 16, kHaloPitch, R + 2);
   if (rc) return rc;
   if (a.cb) {
-    rc = tc_make_map(&mb, a.src_b, a.cb_stride, a.W, a.H, 8, kHaloPx, R + 2);
+    rc = tc_make_map(&mb, a.src_b, a.cb_stride, a.W, a.H, 16, kHaloPitch, R + 2);
     if (rc) return rc;
   } else {
     mb = ma;
