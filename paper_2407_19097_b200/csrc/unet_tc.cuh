@@ -27,7 +27,8 @@
 //              feeding the next level) and/or the final 1x1 out head + sigmoid
 //              (model.py:189-191) in f32 instead of the bf16 activation.
 // Accumulators are double buffered in TMEM (2 x R x N <= 512 columns) so the
-// epilogue of tile i overlaps the MMAs of tile i+1.
+// epilogue of tile i overlaps the MMAs of tile i+1 -- except for wide layers,
+// which take a single buffer of twice the rows (see tc_bufs_for).
 #pragma once
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -81,14 +82,24 @@ constexpr int kHaloPx = 130;                 // pixels a tile row reads (128 + 2
 constexpr int kHaloPitch = 136;              // loaded per row: 136 x 32 B = 17 swizzle atoms
 constexpr int kHaloRowBytes = kHaloPitch * 32;  // one 16-channel halo row, SWIZZLE_32B
 
-__host__ __device__ constexpr int tc_rows(int N) { return N >= 256 ? 1 : (256 / N > 8 ? 8 : 256 / N); }
-__host__ __device__ constexpr int tc_low_rows(int N) { return tc_rows(N) / 2 + 2; }
+// NB = TMEM accumulator buffers.  2: the epilogue of tile i overlaps the MMAs
+// of tile i+1.  1 (N = 256 layers with enough tiles, see tc_bufs_for): twice
+// the rows per tile instead, which halves how often the weights (9*N*32 B per
+// 16-channel chunk, the bulk of such a layer's L2->SM traffic) are streamed.
+__host__ __device__ constexpr int tc_rows(int N, int NB) {
+  return 512 / (NB * N) > 8 ? 8 : 512 / (NB * N);
+}
+__host__ __device__ constexpr int tc_low_rows(int N, int NB) { return tc_rows(N, NB) / 2 + 2; }
 // TMA tensor-load destinations must be 128-byte aligned: slabs are padded.
 __host__ __device__ constexpr int tc_r128(int x) { return (x + 127) / 128 * 128; }
 __host__ __device__ constexpr int tc_r1024(int x) { return (x + 1023) / 1024 * 1024; }
-__host__ __device__ constexpr int tc_a_bytes(int N) { return tc_r1024((tc_rows(N) + 2) * kHaloRowBytes); }
+__host__ __device__ constexpr int tc_a_bytes(int N, int NB) {
+  return tc_r1024((tc_rows(N, NB) + 2) * kHaloRowBytes);
+}
 __host__ __device__ constexpr int tc_b_bytes(int N) { return 9 * N * 32; }
-__host__ __device__ constexpr int tc_stage_bytes(int N) { return tc_r1024(tc_a_bytes(N) + tc_b_bytes(N)); }
+__host__ __device__ constexpr int tc_stage_bytes(int N, int NB) {
+  return tc_r1024(tc_a_bytes(N, NB) + tc_b_bytes(N));
+}
 constexpr int kTcParamFloats = 3 * 144 + 128 * 4 + 4;  // bias_f, bias_f*log2e, bias_g/2, head_w, head_b
 // Narrow layers (N <= 48) use "sliding" MMAs: one MMA per (halo row, kx) with
 // the three ky weight blocks stacked along N (N' = 3N) accumulates into three
@@ -104,13 +115,13 @@ __host__ __device__ constexpr int tc_fixed_smem(int N) {
 #ifndef NAR_TC_MAX_STAGES
 #define NAR_TC_MAX_STAGES 3
 #endif
-__host__ __device__ constexpr int tc_stages(int N) {
-  return (227 * 1024 - tc_fixed_smem(N)) / tc_stage_bytes(N) > NAR_TC_MAX_STAGES
+__host__ __device__ constexpr int tc_stages(int N, int NB) {
+  return (227 * 1024 - tc_fixed_smem(N)) / tc_stage_bytes(N, NB) > NAR_TC_MAX_STAGES
              ? NAR_TC_MAX_STAGES
-             : (227 * 1024 - tc_fixed_smem(N)) / tc_stage_bytes(N);
+             : (227 * 1024 - tc_fixed_smem(N)) / tc_stage_bytes(N, NB);
 }
-__host__ __device__ constexpr int tc_smem(int N) {
-  return tc_stages(N) * tc_stage_bytes(N) + tc_fixed_smem(N);
+__host__ __device__ constexpr int tc_smem(int N, int NB) {
+  return tc_stages(N, NB) * tc_stage_bytes(N, NB) + tc_fixed_smem(N);
 }
 
 // Host: pack HWIO f32 weights into bf16 [chunk q][tap][k8][n][8] where
@@ -280,22 +291,22 @@ __device__ __forceinline__ float gate_b(float f, float g, float bf, float bfl, f
 // ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
-template <int N, bool kHead>
+template <int N, bool kHead, int NB>
 __global__ void __maxnreg__(96)
     gated_conv_tc(const ConvArgs a, const __grid_constant__ CUtensorMap tma_a,
                   const __grid_constant__ CUtensorMap tma_b) {
-  constexpr int R = tc_rows(N);
-  constexpr int LR = tc_low_rows(N);
-  constexpr int S = tc_stages(N);
-  constexpr int A_BYTES = tc_a_bytes(N);
+  constexpr int R = tc_rows(N, NB);
+  constexpr int LR = tc_low_rows(N, NB);
+  constexpr int S = tc_stages(N, NB);
+  constexpr int A_BYTES = tc_a_bytes(N, NB);
   constexpr int B_BYTES = tc_b_bytes(N);
-  constexpr int STAGE = tc_stage_bytes(N);
+  constexpr int STAGE = tc_stage_bytes(N, NB);
   static_assert(A_BYTES % 128 == 0 && B_BYTES % 128 == 0, "align");
   constexpr uint32_t A_TX = (R + 2) * kHaloRowBytes;  // bytes of a direct halo box
   constexpr uint32_t UP_TX = LR * kHaloRowBytes;      // ... of a wide up2 halo box
   constexpr int COUTP = N / 2;
   constexpr uint32_t IDESC = umma_idesc_bf16(128, N);
-  static_assert(2 * R * N <= 512, "TMEM budget");
+  static_assert(NB * R * N <= 512, "TMEM budget");
   static_assert(S >= 2, "pipeline depth");
 
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -390,8 +401,8 @@ __global__ void __maxnreg__(96)
     // ------------------------------ MMA issuer -----------------------------
     int it = 0, tl = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tl) {
-      const int b = tl & 1;
-      mbar_wait(&tempty[b], (((uint32_t)tl >> 1) & 1u) ^ 1u);
+      const int b = tl % NB;
+      mbar_wait(&tempty[b], (((uint32_t)(tl / NB)) & 1u) ^ 1u);
       tc_fence_after();
       const uint32_t dcol = tbase + (uint32_t)(b * R * N);
       const int y0 = (tile / tiles_x) * R;
@@ -472,9 +483,9 @@ __global__ void __maxnreg__(96)
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     int tl = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tl) {
-      const int b = tl & 1;
+      const int b = tl % NB;
       const int y0 = (tile / tiles_x) * R, x0 = (tile % tiles_x) * 128;
-      mbar_wait(&tfull[b], ((uint32_t)tl >> 1) & 1u);
+      mbar_wait(&tfull[b], ((uint32_t)(tl / NB)) & 1u);
       tc_fence_after();
       const int x = x0 + m;
       const bool xok = x < a.W;
@@ -648,29 +659,53 @@ static int tc_make_map(CUtensorMap* m, const void* base, int cs, int w, int h, i
   return NAR_OK;
 }
 
-template <int N, bool kHead>
-static int tc_launch_nh(const ConvArgs& a, cudaStream_t st) {
+// Single TMEM buffer (twice the rows) only for N = 256 layers where the bigger
+// tile costs no extra wave; small levels keep the overlap of double buffering.
+inline int tc_sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = 148;
+  }
+  return sms;
+}
+inline int tc_bufs_for(int N, int H, int W) {
+  if (N < 256) return 2;
+  const int R1 = tc_rows(N, 1), R2 = tc_rows(N, 2), sms = tc_sm_count();
+  const int w1 = (((W + 127) / 128) * ((H + R1 - 1) / R1) + sms - 1) / sms;  // waves of tiles
+  const int w2 = (((W + 127) / 128) * ((H + R2 - 1) / R2) + sms - 1) / sms;
+  return w1 * R1 <= w2 * R2 ? 1 : 2;  // no more row-waves with the bigger tile
+}
+inline int tc_rows_for(int cout, int H, int W) {
+  const int N = 2 * ((cout + 7) / 8 * 8);
+  return tc_rows(N, tc_bufs_for(N, H, W));
+}
+
+template <int N, bool kHead, int NB>
+static int tc_launch_nhb(const ConvArgs& a, cudaStream_t st) {
   static bool attr_done = false;
   if (!attr_done) {
-    const cudaError_t e = cudaFuncSetAttribute(
-        gated_conv_tc<N, kHead>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem(N));
+    const cudaError_t e =
+        cudaFuncSetAttribute(gated_conv_tc<N, kHead, NB>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem(N, NB));
     if (e != cudaSuccess) {
       char msg[160];
-      snprintf(msg, sizeof(msg), "cannot set conv smem size %d: %s", tc_smem(N),
+      snprintf(msg, sizeof(msg), "cannot set conv smem size %d: %s", tc_smem(N, NB),
                cudaGetErrorString(e));
       return set_error(NAR_ERR_CUDA, msg);
     }
     attr_done = true;
   }
-  constexpr int R = tc_rows(N);
+  constexpr int R = tc_rows(N, NB);
   if (a.pool_out && (R & 1)) return set_error(NAR_ERR_CONFIG, "fused pool needs an even row tile");
   CUtensorMap ma, mb;
   int rc;
   if (a.a_up2 == 1) return set_error(NAR_ERR_CONFIG, "tensor-core up2 needs a wide source");
   if (a.out_wide && (a.pool_out || a.head_out))
     return set_error(NAR_ERR_CONFIG, "wide output cannot be pooled or headed");
-  if (a.a_up2)  // wide (H/2, W) source: LR low-res rows, 130 wide pixels
-    rc = tc_make_map(&ma, a.src_a, a.ca_stride, a.W, a.H / 2, 16, kHaloPitch, tc_low_rows(N));
+  if (a.a_up2)  // wide (H/2, W) source: LR low-res rows, 136 wide pixels
+    rc = tc_make_map(&ma, a.src_a, a.ca_stride, a.W, a.H / 2, 16, kHaloPitch, tc_low_rows(N, NB));
   else
     rc = tc_make_map(&ma, a.src_a, a.ca_stride, a.W, a.H, 16, kHaloPitch, R + 2);
   if (rc) return rc;
@@ -680,14 +715,20 @@ static int tc_launch_nh(const ConvArgs& a, cudaStream_t st) {
   } else {
     mb = ma;
   }
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = tc_sm_count();
   const int tiles = ((a.W + 127) / 128) * ((a.H + R - 1) / R);
   const int grid = tiles < sms ? tiles : sms;
   nar::count_launch();
-  gated_conv_tc<N, kHead><<<grid, kTcThreads, tc_smem(N), st>>>(a, ma, mb);
+  gated_conv_tc<N, kHead, NB><<<grid, kTcThreads, tc_smem(N, NB), st>>>(a, ma, mb);
   return check_launch("gated_conv_tc");
+}
+
+template <int N, bool kHead>
+static int tc_launch_nh(const ConvArgs& a, cudaStream_t st) {
+  if constexpr (N >= 256) {
+    if (tc_bufs_for(N, a.H, a.W) == 1) return tc_launch_nhb<N, kHead, 1>(a, st);
+  }
+  return tc_launch_nhb<N, kHead, 2>(a, st);
 }
 
 template <int N>
@@ -700,8 +741,6 @@ static int tc_launch_n(const ConvArgs& a, cudaStream_t st) {
     return set_error(NAR_ERR_CONFIG, "fused out head needs a layer of <= 32 channels");
   }
 }
-
-inline int tc_rows_for(int cout) { return tc_rows(2 * ((cout + 7) / 8 * 8)); }
 
 inline int tc_launch_gated_conv(const ConvArgs& a, cudaStream_t st) {
   const int coutp = (a.cout + 7) / 8 * 8;
