@@ -420,7 +420,8 @@ static int run_conv(nar_unet* n, Layer& l, const __nv_bfloat16* src_a, int ca_st
     if (head_out) head_kernel(a.out);
     return check_launch(l.name.c_str());
   }
-  const bool fuse_pool = pool_out && (tc_rows_for(l.cout, H, W) % 2 == 0);
+  const bool fuse_pool =
+      pool_out && (tc_rows_for(l.cout, H, W, (l.ca + 15) / 16 + (l.cb + 15) / 16) % 2 == 0);
   if (fuse_pool) a.pool_out = pool_out;
   if (head_out) {
     a.head_out = head_out;

@@ -659,8 +659,8 @@ static int tc_make_map(CUtensorMap* m, const void* base, int cs, int w, int h, i
   return NAR_OK;
 }
 
-// Single TMEM buffer (twice the rows) only for N = 256 layers where the bigger
-// tile costs no extra wave; small levels keep the overlap of double buffering.
+// Single TMEM buffer (twice the rows) only for weight-heavy layers where the
+// bigger tile costs no extra wave; the rest keep double buffering's overlap.
 inline int tc_sm_count() {
   static int sms = 0;
   if (!sms) {
@@ -670,16 +670,17 @@ inline int tc_sm_count() {
   }
   return sms;
 }
-inline int tc_bufs_for(int N, int H, int W) {
-  if (N < 256) return 2;
+inline int tc_bufs_for(int N, int H, int W, int nq) {
+  // weight-heavy: N = 256 always; N = 128 from 8 chunks (decoder concat layers)
+  if (N < 128 || (N < 256 && nq < 8)) return 2;
   const int R1 = tc_rows(N, 1), R2 = tc_rows(N, 2), sms = tc_sm_count();
   const int w1 = (((W + 127) / 128) * ((H + R1 - 1) / R1) + sms - 1) / sms;  // waves of tiles
   const int w2 = (((W + 127) / 128) * ((H + R2 - 1) / R2) + sms - 1) / sms;
   return w1 * R1 <= w2 * R2 ? 1 : 2;  // no more row-waves with the bigger tile
 }
-inline int tc_rows_for(int cout, int H, int W) {
+inline int tc_rows_for(int cout, int H, int W, int nq) {
   const int N = 2 * ((cout + 7) / 8 * 8);
-  return tc_rows(N, tc_bufs_for(N, H, W));
+  return tc_rows(N, tc_bufs_for(N, H, W, nq));
 }
 
 template <int N, bool kHead, int NB>
@@ -725,8 +726,9 @@ static int tc_launch_nhb(const ConvArgs& a, cudaStream_t st) {
 
 template <int N, bool kHead>
 static int tc_launch_nh(const ConvArgs& a, cudaStream_t st) {
-  if constexpr (N >= 256) {
-    if (tc_bufs_for(N, a.H, a.W) == 1) return tc_launch_nhb<N, kHead, 1>(a, st);
+  if constexpr (N == 128 || N == 256) {
+    const int nq = (a.ca + 15) / 16 + (a.cb + 15) / 16;
+    if (tc_bufs_for(N, a.H, a.W, nq) == 1) return tc_launch_nhb<N, kHead, 1>(a, st);
   }
   return tc_launch_nhb<N, kHead, 2>(a, st);
 }
