@@ -835,9 +835,16 @@ __global__ void __launch_bounds__(256)
     if (s >= 0) {
       const uint8_t* c = static_cast<const uint8_t*>(P.seg[s].rgb) +
                          (idx - P.seg[s].begin) * sel.rgb_arity;
-      v.x = __fdiv_rn((float)__ldg(c), 255.0f);
-      v.y = __fdiv_rn((float)__ldg(c + 1), 255.0f);
-      v.z = __fdiv_rn((float)__ldg(c + 2), 255.0f);
+      // the 3 bytes through one aligned 8-byte load (two when they straddle):
+      // attributes in mapped host memory cost one PCIe read per load
+      const uintptr_t ca = reinterpret_cast<uintptr_t>(c);
+      const uint32_t off = (uint32_t)(ca & 7u);
+      const unsigned long long* w8 = reinterpret_cast<const unsigned long long*>(ca - off);
+      uint64_t w = __ldg(w8) >> (8u * off);
+      if (off > 5u) w |= __ldg(w8 + 1) << (8u * (8u - off));
+      v.x = __fdiv_rn((float)(uint32_t)(w & 0xFFu), 255.0f);
+      v.y = __fdiv_rn((float)(uint32_t)((w >> 8) & 0xFFu), 255.0f);
+      v.z = __fdiv_rn((float)(uint32_t)((w >> 16) & 0xFFu), 255.0f);
       v.w = fminf(fmaxf(__fdiv_rn(P.near_f, dep), 0.0f), 1.0f);
     }
     if (dst) *reinterpret_cast<float4*>(dst) = v;

@@ -487,19 +487,48 @@ def _rasterize(pc: PointCloud, cam: CameraPose, sel: StreamSelection, r: "Render
     cloud = DeviceCloud([{"begin": 0, "count": pc.count, "positions": pos_dev,
                           "streams": segs_streams}], meta, dev)
     res = r.resolve(cloud, cam, sel, stream=main)
-    # D2H into pinned staging buffers cached on the renderer (reused per call)
-    cache = getattr(r, "_host_out", None)
-    if cache is None or cache["data"].shape != res.data.shape:
-        cache = r._host_out = {k: torch.empty(getattr(res, k).shape, dtype=getattr(res, k).dtype,
-                                              pin_memory=True)
-                               for k in ("data", "coverage", "index_plane", "depth")}
-    host = cache
-    for k in ("data", "coverage", "index_plane", "depth"):
-        host[k].copy_(getattr(res, k), non_blocking=True)
+    # D2H straight into pinned arrays that the returned FeatureImage owns: a
+    # pool of output sets on the renderer, recycled once no FeatureImage views
+    # them any more (no host-side copy, no page faults on fresh memory)
+    host = _pinned_outputs(r, res)
+    for k in _OUT_KEYS:
+        torch.from_numpy(host[k]).copy_(getattr(res, k), non_blocking=True)
     main.synchronize()  # also keeps the uploaded tensors alive until consumed
     names_out = sel.channel_names(pc)
-    # torch's CPU copy is multi-threaded (numpy's is not): ~60 MB at 1080p
-    own = {k: host[k].clone().numpy() for k in ("coverage", "index_plane", "depth")}
-    data = host["data"][:H, :W].clone().numpy()
-    return FeatureImage(W, H, names_out, data, own["coverage"], own["index_plane"],
-                        own["depth"])
+    data = host["data"]
+    if data.shape[:2] != (H, W):
+        data = np.ascontiguousarray(data[:H, :W])
+    else:
+        data = data[...]
+    return FeatureImage(W, H, names_out, data, host["coverage"][...], host["index_plane"][...],
+                        host["depth"][...])
+
+
+_OUT_KEYS = ("data", "coverage", "index_plane", "depth")
+
+
+def _pinned_outputs(r: "Renderer", res) -> dict:
+    """A free set of pinned host arrays shaped like ``res`` (a device FeatureImage).
+
+    Each array in a set is the numpy owner of a pinned torch buffer; the arrays
+    handed out are views (``.base`` is the owner), so a set is free again when
+    the owners' reference counts drop back to the pool's own references.
+    """
+    import sys
+
+    import torch
+
+    pool = getattr(r, "_host_pool", None)
+    if pool is None:
+        pool = r._host_pool = []
+    shapes = {k: tuple(getattr(res, k).shape) for k in _OUT_KEYS}
+    pool[:] = [h for h in pool if all(h[k].shape == shapes[k] for k in _OUT_KEYS)]
+    for h in pool:
+        # references: the set dict + getrefcount's argument
+        if all(sys.getrefcount(h[k]) <= 2 for k in _OUT_KEYS):
+            return h
+    h = {k: torch.empty(shapes[k], dtype=getattr(res, k).dtype, pin_memory=True).numpy()
+         for k in _OUT_KEYS}
+    if len(pool) < 4:  # beyond 4 live images, fresh sets are not pooled
+        pool.append(h)
+    return h
