@@ -314,6 +314,15 @@ struct ChunkMap {
     const uint32_t jj = period * (j >> lshift) + r0 + (j & ((1u << lshift) - 1u));
     return mode == 0 ? jj : (mode == 1 ? jj * kHizSeedStride : jj + jj / (kHizSeedStride - 1) + 1);
   }
+  // unit() for a compile-time mode (modes 0 and 1 always have period 1, r0 0,
+  // lshift 0: slot j is unit j, resp. unit j * kHizSeedStride)
+  template <int M>
+  __device__ __forceinline__ uint32_t unit_m(uint32_t j) const {
+    if (M == 0) return j;
+    if (M == 1) return j * kHizSeedStride;
+    const uint32_t jj = period * (j >> lshift) + r0 + (j & ((1u << lshift) - 1u));
+    return jj + jj / (kHizSeedStride - 1) + 1;
+  }
   // first point of 64-point chunk c (c counts halves of slots)
   __device__ __forceinline__ uint32_t off64(uint32_t c) const {
     return unit(c >> 1) * kUnitPts + (c & 1u) * kChunkPts;
@@ -542,10 +551,11 @@ __device__ __forceinline__ void exact_candidate(const QEntry e, uint64_t* keybuf
   }
 }
 
-template <bool kSigned>
+template <bool kSigned, int kMode>
 __global__ void __launch_bounds__(kRenderThreads, 1)
     render_pre_kernel(uint64_t* __restrict__ keybuf, const float* __restrict__ pos,
                       const ChunkMap cm, uint64_t base_index, const DevCam cam, const HizArgs hz) {
+  static_assert(kMode >= 0 && kMode <= 2, "ChunkMap mode");
   extern __shared__ __align__(128) uint8_t smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   float* ring = reinterpret_cast<float*>(smem) + warp * (kPreStages * kUnitPts * 3);
@@ -557,15 +567,21 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
   const uint32_t j_first = (uint32_t)cm.j0 + blockIdx.x * kRenderWarps + warp;
   const uint32_t j_stride = gridDim.x * kRenderWarps;
   const uint32_t j_end = (uint32_t)cm.j1;
+  // unit indices of the kPreStages slots in flight, oldest first (a register
+  // FIFO: each slot's index is computed once, when its refill is issued)
+  uint32_t uq[kPreStages];
+#pragma unroll
+  for (int s = 0; s < kPreStages; ++s) uq[s] = cm.unit_m<kMode>(j_first + s * j_stride);
   if (lane == 0) {
     for (int s = 0; s < kPreStages; ++s) mbar_init(&full[s], 1);
     fence_mbar_init();
+#pragma unroll
     for (int s = 0; s < kPreStages; ++s) {
       const uint32_t j = j_first + s * j_stride;
       if (j < j_end) {
         mbar_expect_tx(&full[s], kUnitBytes);
-        bulk_g2s(ring + s * (kUnitPts * 3), pos + (size_t)cm.unit(j) * (kUnitPts * 3),
-                 kUnitBytes, &full[s]);
+        bulk_g2s(ring + s * (kUnitPts * 3), pos + (size_t)uq[s] * (kUnitPts * 3), kUnitBytes,
+                 &full[s]);
       }
     }
   }
@@ -582,12 +598,12 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
   const uint32_t kraw = kb * (uint32_t)hz.zw + kb;
   const uint32_t zaddr = smem_u32(zs) - 2u * kraw;
   int qn = 0;  // warp-uniform queue fill
-  int k = 0;
-  for (uint32_t j = j_first; j < j_end; j += j_stride, ++k) {
-    const int s = k % kPreStages;
-    mbar_wait(&full[s], (uint32_t)(k / kPreStages) & 1u);
+  int s = 0;          // ring slot of this iteration: k % kPreStages
+  uint32_t ph = 0u;    // its mbarrier phase parity: (k / kPreStages) & 1
+  for (uint32_t j = j_first; j < j_end; j += j_stride) {
+    mbar_wait(&full[s], ph);
     const float* unit = ring + s * (kUnitPts * 3);
-    const uint32_t cb = (uint32_t)base_index + cm.unit(j) * kUnitPts;
+    const uint32_t cb = (uint32_t)base_index + uq[0] * kUnitPts;
     // lane l takes points 4l .. 4l+3: three conflict-free 16-byte loads
     const float4* u4 = reinterpret_cast<const float4*>(unit) + 3 * lane;
     const float4 a0 = u4[0], a1 = u4[1], a2 = u4[2];
@@ -597,9 +613,13 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
     __syncwarp();
     {  // stage s is consumed: refill it with unit k + kPreStages
       const uint32_t jn = j + kPreStages * j_stride;
+      const uint32_t un = cm.unit_m<kMode>(jn);
       if (jn < j_end)  // warp-uniform: one elected lane issues (no per-lane loop)
-        bulk_g2s_elect(ring + s * (kUnitPts * 3), pos + (size_t)cm.unit(jn) * (kUnitPts * 3),
-                       kUnitBytes, &full[s]);
+        bulk_g2s_elect(ring + s * (kUnitPts * 3), pos + (size_t)un * (kUnitPts * 3), kUnitBytes,
+                       &full[s]);
+#pragma unroll
+      for (int i = 0; i + 1 < kPreStages; ++i) uq[i] = uq[i + 1];
+      uq[kPreStages - 1] = un;
     }
     // w = p - chi: the (x, y) or (y, z) halves of each point that sit in one
     // aligned register pair go through FADD2
@@ -643,6 +663,10 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
           exact_candidate<kSigned>(e2, keybuf, cam);
         }
       }
+    }
+    if (++s == kPreStages) {
+      s = 0;
+      ph ^= 1u;
     }
   }
   __syncwarp();
@@ -937,10 +961,10 @@ static int device_init() {
                          cudaFuncAttributeMaxDynamicSharedMemorySize, kRenderSmem);
     cudaFuncSetAttribute(render_tma_kernel<true, true>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, kRenderSmem);
-    cudaFuncSetAttribute(render_pre_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kPreSmem);
-    cudaFuncSetAttribute(render_pre_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kPreSmem);
+    for (auto k : {render_pre_kernel<false, 0>, render_pre_kernel<false, 1>,
+                   render_pre_kernel<false, 2>, render_pre_kernel<true, 0>,
+                   render_pre_kernel<true, 1>, render_pre_kernel<true, 2>})
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kPreSmem);
     const char* np = getenv("NAR_RENDER_NO_PRETEST");
     g_no_pre = np && np[0] == '1';
   });
@@ -978,7 +1002,9 @@ static int launch_render(uint64_t* keybuf, const float* pos, int64_t n, uint64_t
       const int64_t sms = g_num_sms;
       auto kern = sgn ? render_tma_kernel<true, false> : render_tma_kernel<false, false>;
       auto kseed = sgn ? render_tma_kernel<true, true> : render_tma_kernel<false, true>;
-      auto kpre = sgn ? render_pre_kernel<true> : render_pre_kernel<false>;
+      decltype(&render_pre_kernel<false, 0>) kpres[2][3] = {
+          {render_pre_kernel<false, 0>, render_pre_kernel<false, 1>, render_pre_kernel<false, 2>},
+          {render_pre_kernel<true, 0>, render_pre_kernel<true, 1>, render_pre_kernel<true, 2>}};
       const bool pre = cam.pre && !g_no_pre;
       auto run = [&](ChunkMap cm, bool with_hiz) {
         HizArgs hz{nullptr, shift, zw, zw * zh};
@@ -992,7 +1018,8 @@ static int launch_render(uint64_t* keybuf, const float* pos, int64_t n, uint64_t
         if (grid <= 0) return;
         if (with_hiz && pre) {
           nar::count_launch();
-          kpre<<<grid, kRenderThreads, kPreSmem, st>>>(keybuf, pos, cm, base, cam, hz);
+          kpres[sgn ? 1 : 0][cm.mode]<<<grid, kRenderThreads, kPreSmem, st>>>(keybuf, pos, cm,
+                                                                              base, cam, hz);
         } else if (cm.mode == 1 && !with_hiz) {
           nar::count_launch();
           kseed<<<grid, kRenderThreads, kRenderSmem, st>>>(keybuf, pos, cm, base, cam, hz);
