@@ -1,7 +1,7 @@
 """Profiling driver: C2-sized render (+ resolve) frames on the device path,
 timed with CUDA events.  Used under ncu (one GPU) and for quick A/B runs.
 
-  python scripts/prof_render.py [--points N] [--frames F] [--sorted] [--unet]
+  python scripts/prof_render.py [--points N] [--frames F] [--sorted] [--terrain] [--unet]
 """
 
 import argparse
@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--height", type=int, default=1080)
     ap.add_argument("--sorted", action="store_true", help="pixel-coherent (sorted) point order")
     ap.add_argument("--unet", action="store_true")
+    ap.add_argument("--terrain", action="store_true", help="C4 height-field cloud and camera")
     ap.add_argument("--no-hiz", action="store_true")
     args = ap.parse_args()
     import torch
@@ -29,14 +30,16 @@ def main():
     from paper_2407_19097_b200.msr import DeviceCloud, Renderer, StreamSelection
 
     dev = torch.device("cuda", 0)
-    pos, rgb = bench.make_uniform(args.points, dev, 1234)
+    gen = bench.make_terrain if args.terrain else bench.make_uniform
+    pos, rgb = gen(args.points, dev, 1234)
     if args.sorted:
         key = ((pos[:, 0] + 1) * 1023).long() * 4096 + ((pos[:, 2] + 1) * 1023).long()
         order = torch.argsort(key)
         pos, rgb = pos[order].contiguous(), rgb[order].contiguous()
         del order, key
     cloud = DeviceCloud.from_tensors(pos, {"rgb": rgb})
-    cam = look_at((0.0, -2.2, 1.0), (0, 0, 0), Intrinsics(width=args.width, height=args.height))
+    eye = (0.0, -1.6, 1.2) if args.terrain else (0.0, -2.2, 1.0)
+    cam = look_at(eye, (0, 0, 0), Intrinsics(width=args.width, height=args.height))
     r = Renderer(args.width, args.height, device=dev, pad_multiple=16)
     r.use_hiz = not args.no_hiz
     sel = StreamSelection(rgb=True, depth=True)
