@@ -375,3 +375,40 @@ def test_exact_only_paths_vs_oracle(cuda, case, monkeypatch):
     ref = oracle.zbuffer_render(pos, cam.orientation, cam.position, i.focal_px, i.cx, i.cy,
                                 i.near, i.far, i.width, i.height, threads=os.cpu_count() or 4)
     assert np.array_equal(r.keys(), ref)
+
+
+def test_pass_kernel_choice_over_frames(cuda, monkeypatch):
+    """2.5-D cloud (height field seen obliquely): most points pass the coarse
+    test, so after the statistics of the first render come back the passes
+    switch to the exact kernel (render 17 collects again).  Every frame of both
+    choices must equal the oracle; a volumetric cloud interleaved on another
+    renderer keeps its own statistics."""
+    import os
+
+    import torch
+
+    from paper_2407_19097_b200.geometry import Intrinsics, look_at
+    from paper_2407_19097_b200.msr import DeviceCloud, Renderer
+
+    monkeypatch.setenv("NAR_RENDER_PASS_UNITS", "48")
+    rng = np.random.default_rng(5)
+    n = 900_000
+    xy = rng.uniform(-1, 1, (n, 2))
+    z = 0.15 * np.sin(3 * xy[:, 0]) * np.cos(2 * xy[:, 1])
+    terrain = np.column_stack([xy, z]).astype(np.float32)
+    volume = rng.uniform(-1, 1, (n, 3)).astype(np.float32)
+    cam = look_at((0.0, -1.6, 1.2), (0, 0, 0), Intrinsics(width=320, height=200))
+    i = cam.intrinsics
+    refs, rends, clouds = [], [], []
+    for pos in (terrain, volume):
+        refs.append(oracle.zbuffer_render(pos, cam.orientation, cam.position, i.focal_px, i.cx,
+                                          i.cy, i.near, i.far, 320, 200,
+                                          threads=os.cpu_count() or 4))
+        rends.append(Renderer(320, 200, device=cuda))
+        clouds.append(DeviceCloud.from_tensors(torch.from_numpy(pos).to(cuda)))
+    for frame in range(20):
+        for r, c, ref in zip(rends, clouds, refs):
+            r.clear()
+            r.render(c, cam)
+            assert np.array_equal(r.keys(), ref), frame
+            torch.cuda.synchronize()  # lets the statistics copy land
