@@ -471,9 +471,9 @@ def main_ours(args):
         if unet is not None and rank == 0:
             unet.forward_into(out["data"], unet_out)
 
-    for _ in range(args.warmup):
+    for _ in range(args.warmup):  # synchronised: the renderer's pass statistics land
         frame()
-    torch.cuda.synchronize()
+        torch.cuda.synchronize()
     sampler = ClockSampler(local) if rank == 0 else None
     if world > 1:
         dist.barrier()
@@ -584,6 +584,7 @@ def main_ours(args):
         for _ in range(3):
             r.render(mcloud, cam)
             r.resolve(mcloud, cam, sel, out=out)
+            torch.cuda.synchronize()
         evm = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
                 torch.cuda.Event(enable_timing=True)) for _ in range(km)]
         for a_, b_, c_ in evm:

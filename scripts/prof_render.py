@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--sorted", action="store_true", help="pixel-coherent (sorted) point order")
     ap.add_argument("--unet", action="store_true")
     ap.add_argument("--terrain", action="store_true", help="C4 height-field cloud and camera")
+    ap.add_argument("--morton", action="store_true", help="Morton-reorder the cloud first")
     ap.add_argument("--no-hiz", action="store_true")
     args = ap.parse_args()
     import torch
@@ -38,6 +39,11 @@ def main():
         pos, rgb = pos[order].contiguous(), rgb[order].contiguous()
         del order, key
     cloud = DeviceCloud.from_tensors(pos, {"rgb": rgb})
+    if args.morton:
+        from paper_2407_19097_b200.preprocess import morton_reorder
+
+        cloud = morton_reorder(cloud)
+        del pos, rgb
     eye = (0.0, -1.6, 1.2) if args.terrain else (0.0, -2.2, 1.0)
     cam = look_at(eye, (0, 0, 0), Intrinsics(width=args.width, height=args.height))
     r = Renderer(args.width, args.height, device=dev, pad_multiple=16)
