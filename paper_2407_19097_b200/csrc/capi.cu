@@ -5,6 +5,7 @@
 #include <stdio.h>
 
 #include <atomic>
+#include <mutex>
 #include <string>
 
 #include "common.cuh"
@@ -29,6 +30,21 @@ int check_launch(const char* what) {
 static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 uint64_t launch_total() { return g_launches.load(std::memory_order_relaxed); }
+
+// Scratch from cudaMallocAsync stays mapped in the device's default pool (its
+// release threshold is 0 by default, so every synchronisation would hand the
+// memory back and the next call would map it again).
+void keep_pool_memory() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
+}
 
 }  // namespace nar
 

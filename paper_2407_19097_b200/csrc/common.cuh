@@ -15,6 +15,8 @@ int check_launch(const char* what);
 // every kernel launch of the library is counted (nar_launch_count)
 void count_launch();
 uint64_t launch_total();
+// keeps cudaMallocAsync scratch mapped across calls (default pool threshold)
+void keep_pool_memory();
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

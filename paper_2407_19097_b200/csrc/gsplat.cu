@@ -158,6 +158,7 @@ int nar_splat_blend(const double* mu, const double* inv_abc, const int32_t* boxe
   if (n > 0 && (!mu || !inv_abc || !boxes || !color || !opacity))
     return set_error(NAR_ERR_INVALID, "NULL splat array");
   cudaStream_t st = (cudaStream_t)stream;
+  nar::keep_pool_memory();
   const int tiles_x = (width + tile_size - 1) / tile_size;
   const int tiles_y = (height + tile_size - 1) / tile_size;
   const int64_t n_tiles = (int64_t)tiles_x * tiles_y;

@@ -1393,6 +1393,7 @@ int nar_zbuffer_accumulate(uint64_t* keybuf, const float* positions, int64_t n,
   if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess)
     return set_error(NAR_ERR_CUDA, "stream creation failed");
   uint64_t* dkey = nullptr;
+  nar::keep_pool_memory();
   if (cudaMallocAsync(reinterpret_cast<void**>(&dkey), (size_t)npix * 8, st) != cudaSuccess) {
     cudaStreamDestroy(st);
     return set_error(NAR_ERR_NOMEM, "cudaMallocAsync of keybuf failed");

@@ -721,6 +721,7 @@ int nar_gated_conv(const float* in, int32_t H, int32_t W, int32_t cin, const flo
   __nv_bfloat16 *x = nullptr, *y = nullptr, *w = nullptr;
   float *bf = nullptr, *bg = nullptr;
   int rc = NAR_OK;
+  nar::keep_pool_memory();
   if (cudaMallocAsync(reinterpret_cast<void**>(&x), (size_t)npx * cinp * 2, st) ||
       cudaMallocAsync(reinterpret_cast<void**>(&y), (size_t)npx * cs * 2, st) ||
       cudaMallocAsync(reinterpret_cast<void**>(&w), packed.size() * 2, st) ||

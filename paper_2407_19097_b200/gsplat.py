@@ -233,19 +233,24 @@ def splat_blend_image(mu, inv_abc, boxes, color, opacity, width: int, height: in
                       tile_size: int = 16, threads: int | None = None,
                       backend: str | None = None, device=None, return_device: bool = False):
     """(H, W, 3) f64 front-to-back blend of depth-sorted splats on the GPU
-    (_kernels/__init__.py:97-166; ``threads`` accepted and ignored)."""
+    (_kernels/__init__.py:97-166; ``threads`` accepted and ignored).  The splat
+    arrays may be numpy (uploaded here) or torch tensors already on the device."""
     import torch
 
     _resolve(backend)
     dev = torch.device(device or "cuda")
 
-    def up(a, dt):
-        return torch.from_numpy(np.ascontiguousarray(a, dt)).to(dev)
+    tdt = {np.float64: torch.float64, np.int32: torch.int32}
+
+    def up(a, shape, dt):  # numpy arrays are uploaded; device tensors are used in place
+        if isinstance(a, torch.Tensor):
+            return a.reshape(shape).to(dev, tdt[dt]).contiguous()
+        return torch.from_numpy(np.ascontiguousarray(np.reshape(a, shape), dt)).to(dev)
 
     n = int(len(mu))
-    t_mu, t_abc = up(np.reshape(mu, (n, 2)), np.float64), up(np.reshape(inv_abc, (n, 3)), np.float64)
-    t_box = up(np.reshape(boxes, (n, 4)), np.int32)
-    t_col, t_op = up(np.reshape(color, (n, 3)), np.float64), up(np.reshape(opacity, (n,)), np.float64)
+    t_mu, t_abc = up(mu, (n, 2), np.float64), up(inv_abc, (n, 3), np.float64)
+    t_box = up(boxes, (n, 4), np.int32)
+    t_col, t_op = up(color, (n, 3), np.float64), up(opacity, (n,), np.float64)
     rgb = torch.empty((height, width, 3), dtype=torch.float64, device=dev)
     st = torch.cuda.current_stream(dev)
     _lib.call("nar_splat_blend", t_mu.data_ptr(), t_abc.data_ptr(), t_box.data_ptr(),
