@@ -430,11 +430,16 @@ def main_ours(args):
         chk = sr.r.alloc_outputs(len(names))
         sr.r.resolve(cloud, cam, sel, out=chk, owner_only=True)
         reduce_planes(chk["data"], dst=0)
-        got = pr.frame(cam, sel)
         ok = torch.ones(1, device=dev)
-        if rank == 0 and not torch.equal(got["data"].view(torch.int32), chk["data"].view(torch.int32)):
+        try:
+            got = pr.frame(cam, sel)
+            if rank == 0 and not torch.equal(got["data"].view(torch.int32),
+                                             chk["data"].view(torch.int32)):
+                ok.zero_()
+        except Exception as e:  # every rank learns of a failure through the MIN below
+            log(f"[rank {rank}] fused composite failed ({e})")
             ok.zero_()
-        dist.broadcast(ok, 0)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
         if ok.item() == 1.0:
             cloud = pr.local  # render the symmetric-memory copy of the shard
             composite += " (validated against the NCCL path)"
