@@ -214,8 +214,8 @@ __device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
 // (w0, w1) = (x, y) - chi[0..1] as one FADD2 (x, y adjacent in the lane's
 // registers); returns the reject decision for one point.
 __device__ __forceinline__ bool pretest_reject_w(float w0, float w1, float w2, const DevCam& k,
-                                                 uint32_t zaddr, uint32_t kraw, int shift,
-                                                 int zw) {
+                                                 uint32_t zaddr, uint32_t umax, uint32_t vmax,
+                                                 int shift, int zw) {
   const float uz = fmaf(w2, k.r2f[2], fmaf(w1, k.r2f[1], fmaf(w0, k.r2f[0], k.uz0)));
   // (T' uz for x, for y) with the rows paired: three FFMA2
   const uint64_t fxy =
@@ -228,16 +228,17 @@ __device__ __forceinline__ bool pretest_reject_w(float w0, float w1, float w2, c
   // constant part of the block index is folded into the caller's `zd` base
   float sx, sy;
   upk2(fma2(fxy, pk2(rz, rz), pk2(12582913.0f, 12582913.0f)), sx, sy);
-  const uint32_t bu = (uint32_t)__float_as_int(sx), bv = (uint32_t)__float_as_int(sy);
-  const bool near_img = bu - 0x4B400000u <= (uint32_t)k.w + 1u && bv - 0x4B400000u <= (uint32_t)k.h + 1u;
-  // shared address of the block: zaddr = &zs[0] - 2 * kraw, kraw = raw index of u = v = 0
-  const uint32_t raw = (bv >> shift) * (uint32_t)zw + (bu >> shift);
+  // u, v clamped (unsigned: u < 0 wraps high) to the table's zero column /
+  // row, whose entries reject any depth: no separate range test.  u in
+  // (W+1, umax) lands in the last real column -- a candidate the exact path culls.
+  const uint32_t u = min((uint32_t)__float_as_int(sx) - 0x4B400000u, umax);
+  const uint32_t v = min((uint32_t)__float_as_int(sy) - 0x4B400000u, vmax);
+  const uint32_t b = (v >> shift) * (uint32_t)zw + (u >> shift);
   uint16_t zq;
-  asm("ld.shared.u16 %0, [%1];" : "=h"(zq) : "r"(zaddr + 2u * (near_img ? raw : kraw)));
+  asm("ld.shared.u16 %0, [%1];" : "=h"(zq) : "r"(zaddr + 2u * b));
   // (f32 bits of uz32 * (1 - 2^-14)) >> 16 > zd: strictly behind (negative / NaN uz32
   // compare high and are rejected unless the block is still empty)
-  const bool behind = (__float_as_uint(uz * 0.99993896484375f) >> 16) > (uint32_t)zq;
-  return !near_img || behind;
+  return (__float_as_uint(uz * 0.99993896484375f) >> 16) > (uint32_t)zq;
 }
 
 template <bool kSigned>
@@ -335,7 +336,8 @@ struct ChunkMap {
 // behind every pixel of the block (strictly deeper), so it cannot win.
 struct HizArgs {
   const uint16_t* zmax;  // NULL: no coarse test in this pass
-  int32_t shift, zw, entries;
+  int32_t shift, zw, entries;  // zw: table pitch incl. the zero column
+  int32_t zh;                  // table rows incl. the zero row
   unsigned long long* stats;  // NULL, or this pass's counter of points passing the coarse test
   unsigned long long* stats_clear;  // seed pass: counters to zero (block 0), else NULL
 };
@@ -608,11 +610,9 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
     __syncthreads();
   }
   const uint32_t lt_mask = (1u << lane) - 1u;
-  // zs shifted back by the block index of u = 0, v = 0 (see pretest_reject_w);
-  // only dereferenced for in-range u, v
-  const uint32_t kb = 0x4B400000u >> hz.shift;
-  const uint32_t kraw = kb * (uint32_t)hz.zw + kb;
-  const uint32_t zaddr = smem_u32(zs) - 2u * kraw;
+  const uint32_t zaddr = smem_u32(zs);
+  // first u (v) of the zero column (row): see pretest_reject_w
+  const uint32_t umax = (uint32_t)(hz.zw - 1) << hz.shift, vmax = (uint32_t)(hz.zh - 1) << hz.shift;
   int qn = 0;  // warp-uniform queue fill
   uint32_t n_drained = 0;  // candidates drained in full batches of 32 (pass statistics)
   int s = 0;          // ring slot of this iteration: k % kPreStages
@@ -655,7 +655,8 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
     bool cand[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q)
-      cand[q] = !pretest_reject_w(w[q][0], w[q][1], w[q][2], cam, zaddr, kraw, hz.shift, hz.zw);
+      cand[q] = !pretest_reject_w(w[q][0], w[q][1], w[q][2], cam, zaddr, umax, vmax, hz.shift,
+                                  hz.zw);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
 #pragma unroll
@@ -710,8 +711,9 @@ __global__ void __launch_bounds__(256)
   const int b = (int)(t >> shift), row = (int)(t & (side - 1));
   const bool valid = b < zw * zh;
   uint32_t m = 0;
-  if (valid) {
-    const int bx = b % zw, by = b / zw;
+  const int bx = valid ? b % zw : 0, by = valid ? b / zw : 0;
+  const bool edge = bx == zw - 1 || by == zh - 1;  // zero column / row: rejects every point
+  if (valid && !edge) {
     const int x0 = max((bx << shift) - 2, 0), x1 = min((bx << shift) + side, W);
     // rows are 16-byte aligned when W is even: pairs of keys per load, all
     // issued before the max (x0 is even)
@@ -751,15 +753,16 @@ __global__ void __launch_bounds__(256)
   for (int o = 1; o < side; o <<= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
   if (valid && row == 0) {
     const uint32_t q = (m >> 16) + ((m & 0xFFFFu) != 0u);  // round up: conservative
-    zmax[b] = (uint16_t)(q > 0xFFFFu ? 0xFFFFu : q);
+    zmax[b] = edge ? (uint16_t)0 : (uint16_t)(q > 0xFFFFu ? 0xFFFFu : q);
   }
 }
 
 static void hiz_geometry(int W, int H, int& shift, int& zw, int& zh) {
   shift = 3;  // <= 5 (one warp per coarse block row set) for any image < 2^32 pixels
   for (;;) {
-    zw = ((W + 1) >> shift) + 1;  // u = x + 1 in [0, W]... the shifted grid
-    zh = ((H + 1) >> shift) + 1;
+    // u = x + 1 in [0, W + 1] on the shifted grid, plus a zero column / row
+    zw = ((W + 1) >> shift) + 2;
+    zh = ((H + 1) >> shift) + 2;
     if ((int64_t)zw * zh <= kHizMaxEntries) return;
     ++shift;
   }
@@ -1111,7 +1114,7 @@ static int launch_render(uint64_t* keybuf, const float* pos, int64_t n, uint64_t
       int pass_no = 0;
       auto run = [&](ChunkMap cm, bool with_hiz) {
         const int pno = pass_no++;
-        HizArgs hz{nullptr, shift, zw, zw * zh, nullptr, nullptr};
+        HizArgs hz{nullptr, shift, zw, zw * zh, zh, nullptr, nullptr};
         if (dstats && pno == 0) hz.stats_clear = dstats;  // the seed pass (never counted)
         if (dstats && pno > 0 && pno < kPassStats) {
           hz.stats = dstats + pno;
