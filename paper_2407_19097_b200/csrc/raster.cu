@@ -385,6 +385,7 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
                       const ChunkMap cm, uint64_t base_index, const DevCam cam, const HizArgs hz) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t pol = l2_evict_first_policy();  // the point stream (see bulk_g2s_stream)
   float* ring = reinterpret_cast<float*>(smem) + warp * (kWarpStages * kChunkPts * 3);
   QEntry* wq = reinterpret_cast<QEntry*>(smem + kRingBytes) + warp * 32;
   uint16_t* zs = reinterpret_cast<uint16_t*>(smem + kRingBytes + kQueueBytes);
@@ -401,8 +402,8 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
       const int64_t c = c_first + (int64_t)s * c_stride;
       if (c < n_chunks) {
         mbar_expect_tx(&full[s], kChunkBytes);
-        bulk_g2s(ring + s * (kChunkPts * 3), pos + (size_t)cm.off64((uint32_t)c) * 3, kChunkBytes,
-                 &full[s]);
+        bulk_g2s_stream(ring + s * (kChunkPts * 3), pos + (size_t)cm.off64((uint32_t)c) * 3,
+                        kChunkBytes, &full[s], pol);
       }
     }
   }
@@ -454,8 +455,8 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
       if (lane == 0 && cn < n_chunks) {
         fence_proxy_async_smem();
         mbar_expect_tx(&full[s], kChunkBytes);
-        bulk_g2s(ring + s * (kChunkPts * 3), pos + (size_t)cm.off64((uint32_t)cn) * 3,
-                 kChunkBytes, &full[s]);
+        bulk_g2s_stream(ring + s * (kChunkPts * 3), pos + (size_t)cm.off64((uint32_t)cn) * 3,
+                        kChunkBytes, &full[s], pol);
       }
     }
 #pragma unroll
@@ -576,6 +577,7 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
   if (hz.stats_clear && blockIdx.x == 0 && threadIdx.x < kPassStats) hz.stats_clear[threadIdx.x] = 0ull;
   extern __shared__ __align__(128) uint8_t smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t pol = l2_evict_first_policy();  // the point stream (see bulk_g2s_stream)
   float* ring = reinterpret_cast<float*>(smem) + warp * (kPreStages * kUnitPts * 3);
   QEntry* wq = reinterpret_cast<QEntry*>(smem + kPreRingBytes) + warp * kCandCap;
   uint16_t* zs = reinterpret_cast<uint16_t*>(smem + kPreRingBytes + kCandBytes);
@@ -598,8 +600,8 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
       const uint32_t j = j_first + s * j_stride;
       if (j < j_end) {
         mbar_expect_tx(&full[s], kUnitBytes);
-        bulk_g2s(ring + s * (kUnitPts * 3), pos + (size_t)uq[s] * (kUnitPts * 3), kUnitBytes,
-                 &full[s]);
+        bulk_g2s_stream(ring + s * (kUnitPts * 3), pos + (size_t)uq[s] * (kUnitPts * 3),
+                        kUnitBytes, &full[s], pol);
       }
     }
   }
@@ -632,8 +634,8 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
       const uint32_t jn = j + kPreStages * j_stride;
       const uint32_t un = cm.unit_m<kMode>(jn);
       if (jn < j_end)  // warp-uniform: one elected lane issues (no per-lane loop)
-        bulk_g2s_elect(ring + s * (kUnitPts * 3), pos + (size_t)un * (kUnitPts * 3), kUnitBytes,
-                       &full[s]);
+        bulk_g2s_elect_stream(ring + s * (kUnitPts * 3), pos + (size_t)un * (kUnitPts * 3),
+                              kUnitBytes, &full[s], pol);
 #pragma unroll
       for (int i = 0; i + 1 < kPreStages; ++i) uq[i] = uq[i + 1];
       uq[kPreStages - 1] = un;
