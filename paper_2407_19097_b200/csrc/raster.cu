@@ -569,6 +569,30 @@ __device__ __forceinline__ void exact_candidate(const QEntry e, uint64_t* keybuf
   }
 }
 
+// Seed units (kMode 1) skip the pre-test: every point goes straight down the
+// exact path, 4 independent projections per lane (the keybuf is still nearly
+// empty, so neither the coarse test nor early z would filter); with a coarse
+// depth present (the keybuf already holds this frame) the exact pixel is tested.
+template <bool kSigned>
+__device__ __forceinline__ void exact_direct(float x, float y, float z, uint32_t idx,
+                                             uint64_t* keybuf, const DevCam& cam,
+                                             const uint16_t* zs, const HizArgs& hz) {
+  uint32_t ix, iy, db;
+  bool hit, unc;
+  project_fast(x, y, z, cam, ix, iy, db, hit, unc);
+  if (hit) {
+    if (hz.zmax) {
+      const uint32_t zb = ((iy + 1u) >> hz.shift) * (uint32_t)hz.zw + ((ix + 1u) >> hz.shift);
+      hit = (db >> 16) <= zs[zb];
+    }
+    if (hit) red_key<kSigned>(keybuf, iy * (uint32_t)cam.w + ix, ((uint64_t)db << 32) | idx);
+  } else if (unc) {
+    uint32_t pix;
+    if (project_point(x, y, z, cam, pix, db))
+      red_key<kSigned>(keybuf, pix, ((uint64_t)db << 32) | idx);
+  }
+}
+
 template <bool kSigned, int kMode, bool kStats>
 __global__ void __launch_bounds__(kRenderThreads, 1)
     render_pre_kernel(uint64_t* __restrict__ keybuf, const float* __restrict__ pos,
@@ -605,12 +629,12 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
       }
     }
   }
-  {
+  if (hz.zmax) {
     const uint4* src = reinterpret_cast<const uint4*>(hz.zmax);
     uint4* dst = reinterpret_cast<uint4*>(zs);
     for (int i = tid; i < (hz.entries + 7) / 8; i += kRenderThreads) dst[i] = __ldcg(src + i);
-    __syncthreads();
   }
+  __syncthreads();
   const uint32_t lt_mask = (1u << lane) - 1u;
   const uint32_t zaddr = smem_u32(zs);
   // first u (v) of the zero column (row): see pretest_reject_w
@@ -639,6 +663,17 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
 #pragma unroll
       for (int i = 0; i + 1 < kPreStages; ++i) uq[i] = uq[i + 1];
       uq[kPreStages - 1] = un;
+    }
+    if (kMode == 1) {  // seed units: straight down the exact path
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        exact_direct<kSigned>(px[q], py[q], pz[q], cb + (uint32_t)(4 * lane + q), keybuf, cam, zs,
+                              hz);
+      if (++s == kPreStages) {
+        s = 0;
+        ph ^= 1u;
+      }
+      continue;
     }
     // w = p - chi: the (x, y) or (y, z) halves of each point that sit in one
     // aligned register pair go through FADD2
@@ -1134,6 +1169,10 @@ static int launch_render(uint64_t* keybuf, const float* pos, int64_t n, uint64_t
           nar::count_launch();
           kpres[sgn ? 1 : 0][hz.stats ? 1 : 0][cm.mode]<<<grid, kRenderThreads, kPreSmem, st>>>(
               keybuf, pos, cm, base, cam, hz);
+        } else if (cm.mode == 1 && pre) {  // seed units: the direct path of the pre kernel
+          nar::count_launch();
+          kpres[sgn ? 1 : 0][0][1]<<<grid, kRenderThreads, kPreSmem, st>>>(keybuf, pos, cm, base,
+                                                                          cam, hz);
         } else if (cm.mode == 1 && !with_hiz) {
           nar::count_launch();
           kseed<<<grid, kRenderThreads, kRenderSmem, st>>>(keybuf, pos, cm, base, cam, hz);
