@@ -739,7 +739,7 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
 // in the block plus a one-pixel border -- the window the f32 pre-test needs.
 // S = 2^shift threads per block, one row each (threads 0, 1 take the two extra
 // rows), max-reduced with warp shuffles.
-template <bool kSigned>
+template <bool kSigned, int kNv>  // kNv: 16-byte loads per row, (side + 2) / 2
 __global__ void __launch_bounds__(256)
     hiz_kernel(const uint64_t* __restrict__ keybuf, int W, int H, int shift, int zw, int zh,
                uint16_t* __restrict__ zmax) {
@@ -753,24 +753,27 @@ __global__ void __launch_bounds__(256)
   if (valid && !edge) {
     const int x0 = max((bx << shift) - 2, 0), x1 = min((bx << shift) + side, W);
     // rows are 16-byte aligned when W is even: pairs of keys per load, all
-    // issued before the max (x0 is even)
-    const bool vec = ((W & 1) == 0) && side == 8;
+    // issued before the max (x0 is even); (side + 2) / 2 loads for 8-, 16- and
+    // 32-pixel blocks (4K frames take 16)
+    const bool vec = ((W & 1) == 0) && 2 * kNv == side + 2;
     auto scan = [&](int y) {
       if (y < 0 || y >= H) return;
       const unsigned long long* p =
           reinterpret_cast<const unsigned long long*>(keybuf) + (size_t)y * W;
       if (vec) {
-        ulonglong2 v[5];
+        ulonglong2 v[kNv];
 #pragma unroll
-        for (int i = 0; i < 5; ++i)
-          v[i] = x0 + 2 * i + 1 < x1 ? __ldcg(reinterpret_cast<const ulonglong2*>(p + x0) + i)
-                                     : make_ulonglong2(0ull, 0ull);
+        for (int i = 0; i < kNv; ++i)
+          v[i] = x0 + 2 * i + 1 < x1
+                     ? __ldcg(reinterpret_cast<const ulonglong2*>(p + x0) + i)
+                     : make_ulonglong2(0ull, 0ull);
 #pragma unroll
-        for (int i = 0; i < 5; ++i) {
+        for (int i = 0; i < kNv; ++i) {
+          const bool in = x0 + 2 * i + 1 < x1;
           uint64_t a = v[i].x, b = v[i].y;
           if (kSigned) {
-            a = x0 + 2 * i + 1 < x1 ? a ^ NAR_SIGN_FLIP : 0ull;
-            b = x0 + 2 * i + 1 < x1 ? b ^ NAR_SIGN_FLIP : 0ull;
+            a = in ? a ^ NAR_SIGN_FLIP : 0ull;
+            b = in ? b ^ NAR_SIGN_FLIP : 0ull;
           }
           m = max(m, max((uint32_t)(a >> 32), (uint32_t)(b >> 32)));
         }
@@ -1088,13 +1091,13 @@ static int launch_render(uint64_t* keybuf, const float* pos, int64_t n, uint64_t
   auto refresh = [&]() {
     const int64_t nt = ((int64_t)zw * zh) << shift;
     const unsigned g = (unsigned)((nt + 255) / 256);
-    if (sgn) {
-      nar::count_launch();
-      hiz_kernel<true><<<g, 256, 0, st>>>(keybuf, cam.w, cam.h, shift, zw, zh, zmax);
-    } else {
-      nar::count_launch();
-      hiz_kernel<false><<<g, 256, 0, st>>>(keybuf, cam.w, cam.h, shift, zw, zh, zmax);
-    }
+    // vectorised row scans for 8/16/32-pixel blocks, scalar beyond
+    auto k = sgn ? (shift == 3 ? hiz_kernel<true, 5> : shift == 4 ? hiz_kernel<true, 9>
+                                                     : hiz_kernel<true, 17>)
+                 : (shift == 3 ? hiz_kernel<false, 5> : shift == 4 ? hiz_kernel<false, 9>
+                                                      : hiz_kernel<false, 17>);
+    nar::count_launch();
+    k<<<g, 256, 0, st>>>(keybuf, cam.w, cam.h, shift, zw, zh, zmax);
   };
   if ((reinterpret_cast<uintptr_t>(pos) & 15) == 0) {
     const int64_t n_tiles = n / kTilePts;

@@ -412,3 +412,32 @@ def test_pass_kernel_choice_over_frames(cuda, monkeypatch):
             r.render(c, cam)
             assert np.array_equal(r.keys(), ref), frame
             torch.cuda.synchronize()  # lets the statistics copy land
+
+
+@pytest.mark.parametrize("W,H", [(3840, 2160), (7680, 4320)])
+def test_hiz_large_frames_multipass(cuda, monkeypatch, W, H):
+    """4K and 8K frames take 16- and 32-pixel coarse blocks (vectorised Hi-Z row
+    scans of 9 and 17 loads); the forced multi-pass schedule must stay exact."""
+    import os
+
+    import torch
+
+    from paper_2407_19097_b200.geometry import Intrinsics, look_at
+    from paper_2407_19097_b200.msr import DeviceCloud, Renderer
+
+    monkeypatch.setenv("NAR_RENDER_PASS_UNITS", "96")
+    rng = np.random.default_rng(W)
+    n = 1_500_000
+    pos = rng.uniform(-1, 1, (n, 3)).astype(np.float32)
+    pos[: n // 2, 2] = np.round(pos[: n // 2, 2] * 4) / 4  # layered surfaces
+    cam = look_at((0.2, -2.4, 0.9), (0, 0, 0), Intrinsics(width=W, height=H))
+    i = cam.intrinsics
+    ref = oracle.zbuffer_render(pos, cam.orientation, cam.position, i.focal_px, i.cx, i.cy,
+                                i.near, i.far, W, H, threads=os.cpu_count() or 4)
+    r = Renderer(W, H, device=cuda)
+    c = DeviceCloud.from_tensors(torch.from_numpy(pos).to(cuda))
+    for _ in range(2):  # the second render may switch passes to the exact kernel
+        r.clear()
+        r.render(c, cam)
+        torch.cuda.synchronize()
+        assert np.array_equal(r.keys(), ref)
