@@ -6,7 +6,7 @@ timeout 600 $B > gpurun_out/prof_bench_plain.json 2> gpurun_out/prof_bench_plain
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/bench_launches.csv $B > /dev/null 2> gpurun_out/ncu1.err
 echo "launches rc=$?"
 C="python scripts/prof_render.py --frames 2"
-timeout 300 $C > /dev/null 2>&1 && timeout 600 ncu --set full --import-source on --clock-control none -k regex:render_pre -s 7 -c 1 -o gpurun_out/r01_render_full -f $C > /dev/null 2>&1
+timeout 300 $C > /dev/null 2>&1 && timeout 600 ncu --set full --import-source on --clock-control none -k regex:render_pre -s 9 -c 1 -o gpurun_out/r01_render_full -f $C > /dev/null 2>&1
 echo "render full rc=$?"
 U="python scripts/prof_unet.py --frames 1"
 timeout 300 $U > /dev/null 2>&1 && timeout 600 ncu --set full --import-source on --clock-control none -k regex:gated_conv_tc -s 1 -c 1 -o gpurun_out/r01_conv_full -f $U > /dev/null 2>&1
