@@ -500,7 +500,7 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
         }
       }
     }
-    if (kRed) {  // seed pass: the keybuf is still mostly empty, early-z would not filter
+    if constexpr (kRed) {  // seed units: the keybuf is still mostly empty, early-z would not filter
 #pragma unroll
       for (int j = 0; j < kPtsPerThread; ++j)
         if ((okmask >> j) & 1u) red_key<kSigned>(keybuf, pix[j], key[j]);
