@@ -374,6 +374,8 @@ class Renderer:
         names = sel.channel_names(cloud)
         if out is None:
             out = self.alloc_outputs(len(names))
+        else:
+            _check_outputs(out, len(names), self.height, self.width)
         ro = _lib.ResolveOut()
         ro.data = out["data"].data_ptr()
         ro.data_h, ro.data_w = int(out["data"].shape[0]), int(out["data"].shape[1])
@@ -420,6 +422,27 @@ class _Mapped:
 
 
 _renderers: dict = {}
+
+
+def _check_outputs(out: dict, n_channels: int, H: int, W: int) -> None:
+    """Caller-provided G-buffer tensors must match the selection and the frame:
+    the kernel writes through raw pointers, so a mismatch would corrupt memory."""
+    import torch
+
+    d = out["data"]
+    ds = tuple(d.shape)
+    if len(ds) != 3 or ds[2] != n_channels or ds[0] < H or ds[1] < W:
+        raise ValueError(f"out['data'] must be (>= {H}, >= {W}, {n_channels}) for this selection, "
+                         f"got {ds}")
+    want = {"data": torch.float32, "coverage": torch.uint8, "index_plane": torch.int64,
+            "depth": torch.float32}
+    for k, dt in want.items():
+        t = out[k]
+        if k != "data" and tuple(t.shape) != (H, W):
+            raise ValueError(f"out[{k!r}] must be ({H}, {W}), got {tuple(t.shape)}")
+        if isinstance(t, torch.Tensor) and (t.dtype != dt or not t.is_contiguous()
+                                            or (isinstance(d, torch.Tensor) and t.device != d.device)):
+            raise ValueError(f"out[{k!r}] must be a contiguous {dt} tensor on the data's device")
 
 
 def _renderer_for(width: int, height: int, device) -> Renderer:

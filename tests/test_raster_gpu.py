@@ -441,3 +441,32 @@ def test_hiz_large_frames_multipass(cuda, monkeypatch, W, H):
         r.render(c, cam)
         torch.cuda.synchronize()
         assert np.array_equal(r.keys(), ref)
+
+
+def test_resolve_rejects_mismatched_outputs(cuda):
+    """Caller-provided G-buffers are validated (the kernel writes through raw
+    pointers): a wrong channel count, plane shape or dtype raises ValueError."""
+    import torch
+
+    from paper_2407_19097_b200.geometry import Intrinsics, look_at
+    from paper_2407_19097_b200.msr import DeviceCloud, Renderer, StreamSelection
+
+    pos = torch.rand((5000, 3), device=cuda) * 2 - 1
+    rgb = torch.randint(0, 256, (5000, 3), dtype=torch.uint8, device=cuda)
+    cloud = DeviceCloud.from_tensors(pos, {"rgb": rgb})
+    cam = look_at((0.0, -2.5, 1.0), (0, 0, 0), Intrinsics(width=64, height=48))
+    r = Renderer(64, 48, device=cuda)
+    sel = StreamSelection(rgb=True, depth=True)
+    r.render(cloud, cam)
+    with pytest.raises(ValueError, match="out\\['data'\\]"):
+        r.resolve(cloud, cam, sel, out=r.alloc_outputs(1))
+    bad = r.alloc_outputs(4)
+    bad["depth"] = torch.empty((48, 64), dtype=torch.float64, device=cuda)
+    with pytest.raises(ValueError, match="depth"):
+        r.resolve(cloud, cam, sel, out=bad)
+    bad = r.alloc_outputs(4)
+    bad["coverage"] = torch.empty((47, 64), dtype=torch.uint8, device=cuda)
+    with pytest.raises(ValueError, match="coverage"):
+        r.resolve(cloud, cam, sel, out=bad)
+    good = r.resolve(cloud, cam, sel, out=r.alloc_outputs(4))
+    assert good.data.shape == (48, 64, 4)
