@@ -223,6 +223,8 @@ class UNet:
 
         self.config = config
         self.device = torch.device(device or "cuda")
+        if self.device.type == "cuda" and self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
         lib = _lib.load()
         h = C.c_void_p()
         _lib.check(lib.nar_unet_create(C.byref(_config_struct(config)), C.byref(h)))
@@ -273,6 +275,17 @@ class UNet:
                 f"features have {int(x.shape[-1])}")
         if not (x.is_contiguous() and out.is_contiguous()):
             raise ValueError("forward_into needs contiguous tensors")
+        import torch
+
+        n_out = self.config.output_channels
+        if x.dtype != torch.float32 or out.dtype != torch.float32:
+            raise ValueError("forward_into needs float32 tensors")
+        if x.device != self.device or out.device != self.device:
+            raise ValueError(f"forward_into needs tensors on {self.device}")
+        if tuple(out.shape[-3:]) != (H, W, n_out) or out.numel() != H * W * n_out:
+            raise ValueError(f"out must be ({H}, {W}, {n_out}), got {tuple(out.shape)}")
+        if x.numel() != H * W * int(x.shape[-1]):
+            raise ValueError("forward_into takes one image (H, W, C) or (1, H, W, C)")
         ws = self._workspace(H, W)
         _lib.check(_lib.load().nar_unet_forward(self._h, x.data_ptr(), H, W, out.data_ptr(),
                                                 ws.data_ptr(), ws.numel(),

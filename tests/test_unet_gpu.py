@@ -217,3 +217,25 @@ def test_forward_config_variants_vs_oracle(cuda, cin, out_ch, head, levels):
     assert y.shape == ref.shape == (1, 64, 96, out_ch)
     assert oracle.psnr(y, ref) >= PSNR_MIN
     assert np.max(np.abs(y - ref)) <= MAX_ABS
+
+
+def test_forward_into_validates_buffers(cuda):
+    """forward_into writes through raw pointers: wrong output shape, dtype or
+    device is refused."""
+    import torch
+
+    from paper_2407_19097_b200.neural import UNet, init_params
+
+    cfg = _cfg(4, 8, 0)
+    net = UNet(cfg, init_params(cfg), device=cuda)
+    x = torch.rand((32, 48, 4), device=cuda)
+    with pytest.raises(ValueError):
+        net.forward_into(x, torch.empty((32, 48, 2), device=cuda))
+    with pytest.raises(ValueError):
+        net.forward_into(x, torch.empty((32, 48, 3), dtype=torch.float64, device=cuda))
+    with pytest.raises(ValueError):
+        net.forward_into(x.double(), torch.empty((32, 48, 3), device=cuda))
+    y = torch.empty((32, 48, 3), device=cuda)
+    net.forward_into(x, y)
+    torch.cuda.synchronize()
+    assert torch.all((y > 0) & (y < 1))
