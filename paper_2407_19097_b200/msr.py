@@ -197,10 +197,23 @@ class DeviceCloud:
     @classmethod
     def from_tensors(cls, positions, streams: dict | None = None, formats: dict | None = None,
                      begin: int = 0) -> "DeviceCloud":
-        """Wrap device tensors generated in place (no host copy)."""
+        """Wrap device tensors generated in place (no host copy).  The kernels read
+        them through raw pointers, so layouts are checked here: positions (n, 3)
+        float32, streams (n, arity) uint8 / float32, all contiguous on one GPU."""
+        import torch
+
+        _check_positions(positions)
+        n = int(positions.shape[0])
         meta, st = {}, {}
         for name, t in (streams or {}).items():
+            if (not isinstance(t, torch.Tensor) or t.dim() != 2 or int(t.shape[0]) != n
+                    or not t.is_contiguous() or t.device != positions.device
+                    or t.dtype not in (torch.uint8, torch.float32)):
+                raise ValueError(f"stream {name!r} must be a contiguous (n, arity) uint8 or "
+                                 f"float32 tensor on {positions.device} with n = {n}")
             fmt = (formats or {}).get(name, "u8" if str(t.dtype) == "torch.uint8" else "f32")
+            if (fmt == "u8") != (t.dtype == torch.uint8):
+                raise ValueError(f"stream {name!r}: format {fmt!r} does not match {t.dtype}")
             meta[name] = _StreamMeta(name, fmt, int(t.shape[1]))
             st[name] = t
         return cls([{"begin": int(begin), "positions": positions, "streams": st}], meta,
@@ -422,6 +435,15 @@ class _Mapped:
 
 
 _renderers: dict = {}
+
+
+def _check_positions(positions) -> None:
+    import torch
+
+    if (not isinstance(positions, torch.Tensor) or not positions.is_cuda
+            or positions.dtype != torch.float32 or positions.dim() != 2
+            or int(positions.shape[1]) != 3 or not positions.is_contiguous()):
+        raise ValueError("positions must be a contiguous (n, 3) float32 CUDA tensor")
 
 
 def _check_outputs(out: dict, n_channels: int, H: int, W: int) -> None:

@@ -126,6 +126,10 @@ def morton_keys_device(positions, lo=None, hi=None):
     """63-bit Morton keys (int64 tensor) of device positions (n, 3) f32."""
     import torch
 
+    from .msr import _check_positions
+
+    _check_positions(positions)
+
     if lo is None or hi is None:
         lo, hi = _aabb(positions)
     lo = np.ascontiguousarray(lo, np.float64)
