@@ -183,3 +183,27 @@ def test_feature_dump_roundtrip_and_errors(pre, tmp_path):
         pp.load_features(_write(tmp_path, "t", raw[:-4]))
     with pytest.raises(ValueError):
         pp.save_features(names[:4], pre["feat/data"], tmp_path / "x.feat")
+
+
+def test_device_buffer_validation_cpu():
+    """Layout checks in front of the raw-pointer kernels run without a GPU: CPU
+    tensors, wrong dtypes or shapes and mismatched streams raise ValueError."""
+    import torch
+
+    from paper_2407_19097_b200.msr import DeviceCloud, _check_outputs, _check_positions
+
+    with pytest.raises(ValueError):
+        _check_positions(torch.zeros((4, 3)))  # not on a GPU
+    with pytest.raises(ValueError):
+        DeviceCloud.from_tensors(torch.zeros((4, 3), dtype=torch.float64))
+    with pytest.raises(ValueError):
+        pp.morton_keys_device(torch.zeros((4, 2)))
+    ok = {"data": torch.zeros((8, 8, 4)), "coverage": torch.zeros((6, 7), dtype=torch.uint8),
+          "index_plane": torch.zeros((6, 7), dtype=torch.int64), "depth": torch.zeros((6, 7))}
+    _check_outputs(ok, 4, 6, 7)
+    with pytest.raises(ValueError, match="data"):
+        _check_outputs(ok, 3, 6, 7)
+    with pytest.raises(ValueError, match="index_plane"):
+        _check_outputs(dict(ok, index_plane=torch.zeros((6, 7), dtype=torch.int32)), 4, 6, 7)
+    with pytest.raises(ValueError, match="depth"):
+        _check_outputs(dict(ok, depth=torch.zeros((7, 6))), 4, 6, 7)
