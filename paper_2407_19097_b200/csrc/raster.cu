@@ -9,7 +9,8 @@
 //
 // Data layout in HBM:
 //   positions : f32 AoS (n, 3), 12 B/point, streamed once per frame by TMA
-//               bulk copies (cp.async.bulk) into a 4-stage smem ring;
+//               bulk copies (cp.async.bulk, L2 evict-first) into per-warp
+//               smem rings (3 x 1.5 KB units, or 6 x 768 B chunks);
 //   keybuf    : u64 (H*W,) row-major, L2-resident (16.6 MB at 1080p);
 //               key = f32bits(depth) << 32 | (index & 0xFFFFFFFF).
 #include <cuda_runtime.h>
@@ -527,17 +528,17 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
   add_warp_count(hz.stats, n_surv);
 }
 
-// Hi-Z passes: the f32 pre-test rejects most points in ~35 instructions; the
+// Hi-Z passes: the f32 pre-test rejects most points in ~25 instructions; the
 // rest (candidates) are compacted into a per-warp shared-memory queue and run
 // through the exact path 32 at a time with every lane busy:
-// (1) pre-test both points of the lane; ballot-compact candidates (xyz, index)
+// (1) pre-test the lane's 4 points; ballot-compact candidates (xyz, index)
 //     onto the queue; hand the ring slot back to TMA;
 // (2) while >= 32 are queued, pop 32: certified projection (uncertain ones
-//     take the exact f64 path inline -- they are ~1e-6 of points), early-z
-//     read of the keybuf and atomicMin if smaller.
+//     take the exact f64 path inline -- they are ~1e-6 of points) and a
+//     fire-and-forget atomicMin (RED).
 // Each warp step takes one 128-point unit (4 points per lane) in one ring
 // stage; candidates are drained after each half, so the queue never holds
-// more than 31 + 64.
+// more than 31 + 64.  Seed units (kMode 1) skip (1) and (2): exact_direct.
 #ifndef NAR_PRE_STAGES
 #define NAR_PRE_STAGES 3
 #endif
