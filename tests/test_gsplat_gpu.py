@@ -61,3 +61,18 @@ def test_blend_large_vs_oracle_and_empty(cuda):
     empty = splat_blend_image(np.zeros((0, 2)), np.zeros((0, 3)), np.zeros((0, 4), np.int64),
                               np.zeros((0, 3)), np.zeros(0), 40, 30)
     assert empty.shape == (30, 40, 3) and not empty.any()
+
+
+def test_blend_device_resident_inputs(cuda, gs):
+    """Splat arrays already on the device (the bench's resident case) give the
+    same image as the numpy inputs, to the last bit."""
+    import torch
+
+    from paper_2407_19097_b200.gsplat import splat_blend_image
+
+    W, H = (int(v) for v in gs["blend/wh"])
+    arrs = [gs[f"blend/{k}"] for k in ("mu", "inv_abc", "boxes", "color", "opacity")]
+    host = splat_blend_image(*arrs, W, H)
+    dev = splat_blend_image(*[torch.from_numpy(np.ascontiguousarray(a)).to(cuda) for a in arrs],
+                            W, H, device=cuda, return_device=True)
+    assert np.array_equal(dev.cpu().numpy(), host)

@@ -470,3 +470,33 @@ def test_resolve_rejects_mismatched_outputs(cuda):
         r.resolve(cloud, cam, sel, out=bad)
     good = r.resolve(cloud, cam, sel, out=r.alloc_outputs(4))
     assert good.data.shape == (48, 64, 4)
+
+
+def test_rasterize_output_pool_ownership(cuda):
+    """rasterize() returns arrays in pooled pinned buffers: an image that is
+    still referenced is never overwritten by later calls, and released sets
+    are reused."""
+    from paper_2407_19097_b200.geometry import Intrinsics, PointCloud, Stream, look_at
+    from paper_2407_19097_b200.msr import StreamSelection, _renderer_for, rasterize
+
+    rng = np.random.default_rng(17)
+    n = 100_000
+    sel = StreamSelection(rgb=True, depth=True)
+    cam = look_at((0.3, -2.4, 0.8), (0, 0, 0), Intrinsics(width=96, height=64))
+    clouds = [PointCloud(rng.uniform(-1, 1, (n, 3)).astype(np.float32),
+                         [Stream("rgb", "u8", rng.integers(0, 256, (n, 3), dtype=np.uint8))])
+              for _ in range(3)]
+    refs = [oracle.rasterize(pc, cam, sel) for pc in clouds]
+    kept = [rasterize(pc, cam, sel) for pc in clouds]  # all three alive at once
+    for img, ref in zip(kept, refs):
+        assert np.array_equal(img.data, ref["data"])
+        assert np.array_equal(img.index_plane, ref["index_plane"])
+    view = kept[0].depth[:10]  # a view keeps its set busy after the image is dropped
+    del kept, img
+    r = _renderer_for(96, 64, cuda)
+    before = len(r._host_pool)
+    again = [rasterize(pc, cam, sel) for pc in clouds[1:]]
+    assert len(r._host_pool) == before  # released sets were reused, no new ones pooled
+    assert np.array_equal(view, refs[0]["depth"][:10])
+    for img, ref in zip(again, refs[1:]):
+        assert np.array_equal(img.data, ref["data"])
