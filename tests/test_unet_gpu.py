@@ -239,3 +239,23 @@ def test_forward_into_validates_buffers(cuda):
     net.forward_into(x, y)
     torch.cuda.synchronize()
     assert torch.all((y > 0) & (y < 1))
+
+
+@pytest.mark.parametrize("H,W,cin,cout", [(144, 256, 32, 128), (272, 480, 128, 64)])
+def test_gated_conv_single_tmem_buffer(cuda, H, W, cin, cout):
+    """Shapes where the launcher takes one TMEM buffer with twice the rows
+    (N = 256; N = 128 with 8 input chunks) against the f32 oracle."""
+    from paper_2407_19097_b200.neural import gated_conv
+
+    rng = np.random.default_rng(H + cin)
+    x = rng.uniform(-1, 1, size=(1, H, W, cin)).astype(np.float32)
+    s = 1.0 / np.sqrt(9 * cin)
+    p = {"l.f_w": rng.normal(0, s, (3, 3, cin, cout)).astype(np.float32),
+         "l.f_b": rng.normal(0, 0.1, cout).astype(np.float32),
+         "l.g_w": rng.normal(0, s, (3, 3, cin, cout)).astype(np.float32),
+         "l.g_b": rng.normal(0, 0.1, cout).astype(np.float32)}
+    y = gated_conv(x, p["l.f_w"], p["l.f_b"], p["l.g_w"], p["l.g_b"])
+    ref = oracle.gated(p, "l", x[0])[None]
+    assert y.shape == ref.shape
+    assert np.max(np.abs(y - ref)) <= 2e-2
+    assert oracle.psnr(y, ref) >= PSNR_MIN
