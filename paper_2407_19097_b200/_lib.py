@@ -214,12 +214,17 @@ def make_camera(R, campos, f, cx, cy, near, far, width, height) -> Camera:
     return cam
 
 
-def stream_handle(stream) -> int:
-    """cudaStream_t of a torch.cuda.Stream (or None -> current stream)."""
+def stream_handle(stream, device_index: int | None = None) -> int:
+    """cudaStream_t of a torch.cuda.Stream (or None -> torch's current stream of
+    ``device_index``, default the current device)."""
     import torch
 
-    if stream is None:
-        stream = torch.cuda.current_stream()
+    if stream is None:  # the raw handle, without building a Stream object
+        raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+        idx = torch.cuda.current_device() if device_index is None else device_index
+        if raw is not None:
+            return int(raw(idx))
+        stream = torch.cuda.current_stream(idx)
     return int(stream.cuda_stream)
 
 

@@ -81,12 +81,20 @@ class CameraPose:
         return replace(self, intrinsics=intr)
 
     def kernel_camera(self):
-        """The C-ABI ``nar_camera`` for this pose."""
+        """The C-ABI ``nar_camera`` for this pose (cached per pose: a frame-rate
+        loop builds it once; the key includes the arrays' bytes, so an in-place
+        edit of position / orientation is still seen)."""
         from . import _lib
 
         i = self.intrinsics
-        return _lib.make_camera(self.orientation.reshape(-1), self.position, i.focal_px,
-                                i.cx, i.cy, i.near, i.far, i.width, i.height)
+        key = (self.position.tobytes(), self.orientation.tobytes(), i)
+        cached = self.__dict__.get("_kc")
+        if cached is not None and cached[0] == key:
+            return cached[1]
+        kc = _lib.make_camera(self.orientation.reshape(-1), self.position, i.focal_px,
+                              i.cx, i.cy, i.near, i.far, i.width, i.height)
+        object.__setattr__(self, "_kc", (key, kc))
+        return kc
 
 
 def _unit(v: np.ndarray) -> np.ndarray:

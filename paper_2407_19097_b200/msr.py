@@ -296,6 +296,8 @@ class Renderer:
 
         self.width, self.height = int(width), int(height)
         self.device = torch.device(device or "cuda")
+        if self.device.type == "cuda" and self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
         self.domain = _lib.KEYS_SIGNED if signed_keys else _lib.KEYS_UNSIGNED
         self.empty = (_lib.EMPTY_KEY ^ _lib.SIGN_FLIP) if signed_keys else _lib.EMPTY_KEY
         npix = self.width * self.height
@@ -315,7 +317,7 @@ class Renderer:
 
     def clear(self, stream=None) -> None:
         _lib.call("nar_keybuf_fill", self.keybuf.data_ptr(), self.npix,
-                  C.c_uint64(self.empty), _lib.stream_handle(stream))
+                  C.c_uint64(self.empty), _lib.stream_handle(stream, self.device.index))
 
     def _check_cam(self, cam: CameraPose):
         i = cam.intrinsics
@@ -330,31 +332,31 @@ class Renderer:
         import torch
 
         kc = self._check_cam(cam)
-        main = stream or torch.cuda.current_stream(self.device)
         segs = cloud.segments
 
-        def launch(sg, st, has_frame):
+        def launch(sg, handle, has_frame):
             n = int(sg["positions"].shape[0])
             if self.use_hiz:
                 _lib.call("nar_render_hiz", self.keybuf.data_ptr(), self.hiz.data_ptr(),
                           sg["positions"].data_ptr(), n, C.c_uint64(sg["begin"]), C.byref(kc),
-                          self.domain, int(has_frame), int(st.cuda_stream))
+                          self.domain, int(has_frame), handle)
             else:
                 _lib.call("nar_render", self.keybuf.data_ptr(), sg["positions"].data_ptr(), n,
-                          C.c_uint64(sg["begin"]), C.byref(kc), self.domain,
-                          int(st.cuda_stream))
+                          C.c_uint64(sg["begin"]), C.byref(kc), self.domain, handle)
 
         if len(segs) <= 1 or not multi_stream:
+            handle = _lib.stream_handle(stream, self.device.index)
             for k, sg in enumerate(segs):
-                launch(sg, main, k > 0)
+                launch(sg, handle, k > 0)
             return
+        main = stream or torch.cuda.current_stream(self.device)
         while len(self._streams) < len(segs):
             self._streams.append(torch.cuda.Stream(self.device))
         start = torch.cuda.Event()
         start.record(main)
         for sg, st in zip(segs, self._streams):
             st.wait_event(start)
-            launch(sg, st, False)
+            launch(sg, int(st.cuda_stream), False)
         for st in self._streams[: len(segs)]:
             ev = torch.cuda.Event()
             ev.record(st)
@@ -400,13 +402,14 @@ class Renderer:
         segs = _segments_struct(cloud, sel)
         if peers is None:
             _lib.call("nar_resolve", self.keybuf.data_ptr(), C.byref(kc), self.domain, C.byref(s),
-                      segs, len(cloud.segments), C.byref(ro), _lib.stream_handle(stream))
+                      segs, len(cloud.segments), C.byref(ro),
+                      _lib.stream_handle(stream, self.device.index))
         else:
             arr = (C.c_void_p * len(peers))(*[int(p) for p in peers])
             r0, r1 = rows if rows is not None else (0, -1)
             _lib.call("nar_resolve_peers", arr, len(peers), int(r0), int(r1), C.byref(kc),
                       self.domain, C.byref(s), segs, len(cloud.segments), C.byref(ro),
-                      _lib.stream_handle(stream))
+                      _lib.stream_handle(stream, self.device.index))
         return DeviceFeatureImage(self.width, self.height, names, out["data"], out["coverage"],
                                   out["index_plane"], out["depth"])
 
