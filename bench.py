@@ -41,13 +41,33 @@ sys.path.insert(0, str(ROOT))
 METRIC = "points/sec rasterized (Gpts/s, % HBM roofline) and end-to-end fps at 1080p"
 BYTES_PER_POINT = 12  # f32 xyz, read once per frame
 
+class Workload:
+    """points: per GPU ("weak") or total over all GPUs ("strong")."""
+
+    def __init__(self, points, width, height, desc, scaling="weak", unet=False, cloud="uniform",
+                 eye=(0.0, -2.2, 1.0)):
+        self.points, self.width, self.height, self.desc = points, width, height, desc
+        self.scaling, self.unet, self.cloud, self.eye = scaling, unet, cloud, eye
+
+
 WORKLOADS = {
-    # name: (points per GPU, width, height, description)
-    "c1": (1_000_000, 512, 512, "synthetic uniform cloud 1M points, single stream, 512x512 rasterize+resolve"),
-    "c2": (350_000_000, 1920, 1080, "synthetic 350M-point cloud, single stream, 1920x1080 rasterize+resolve"),
-    "c3": (400_000_000, 1920, 1080, "4 streams x 100M Lagrangian-like points, 1080p, RGB+D+Vel2D, one CUDA stream per data stream"),
-    "c4": (350_000_000, 1920, 1080, "350M terrain-like points rasterized + U-Net (random init) at 1080p"),
-    "c5": (250_000_000, 3840, 2160, "C5 shard: 2B uniform points over 8 GPUs = 250M per GPU, 3840x2160 rasterize+resolve"),
+    "c1": Workload(1_000_000, 512, 512,
+                   "synthetic uniform cloud 1M points, single stream, 512x512 rasterize+resolve"),
+    "c2": Workload(350_000_000, 1920, 1080,
+                   "synthetic 350M-point cloud, single stream, 1920x1080 rasterize+resolve"),
+    "c3": Workload(400_000_000, 1920, 1080,
+                   "4 streams x 100M Lagrangian-like points, 1080p, RGB+D+Vel2D, one CUDA stream "
+                   "per data stream", cloud="trajectories", eye=(0.0, -2.6, 1.4)),
+    "c4": Workload(350_000_000, 1920, 1080,
+                   "350M terrain-like points rasterized + U-Net (random init) at 1080p",
+                   unet=True, cloud="terrain", eye=(0.0, -1.6, 1.2)),
+    # north-star multi-GPU workloads: a fixed cloud sharded over the ranks
+    "c5": Workload(2_000_000_000, 3840, 2160,
+                   "2B-point synthetic cloud sharded across the GPUs at 3840x2160, "
+                   "min-composite + resolve", scaling="strong"),
+    "nar1b": Workload(1_000_000_000, 1920, 1080,
+                      "1B points at 1080p sharded across the GPUs: raster + composite + U-Net "
+                      "(random init) on the root", scaling="strong", unet=True),
 }
 
 
@@ -124,18 +144,45 @@ def measured_peaks() -> tuple[dict, str]:
 # ---------------------------------------------------------------------------
 # synthetic clouds (generated on the device)
 # ---------------------------------------------------------------------------
-def make_uniform(n, device, seed):
+def make_uniform(n, device, seed, alloc=None):
     import torch
 
+    alloc = alloc or (lambda shape, dt: torch.empty(shape, dtype=dt, device=device))
     g = torch.Generator(device=device).manual_seed(seed)
-    pos = torch.empty((n, 3), dtype=torch.float32, device=device)
-    rgb = torch.empty((n, 3), dtype=torch.uint8, device=device)
+    pos = alloc((n, 3), torch.float32)
+    rgb = alloc((n, 3), torch.uint8)
     step = 50_000_000
     for lo in range(0, n, step):
         hi = min(n, lo + step)
         pos[lo:hi].uniform_(-1.0, 1.0, generator=g)
         rgb[lo:hi] = torch.randint(0, 256, (hi - lo, 3), device=device, generator=g,
                                    dtype=torch.int32).to(torch.uint8)
+    return pos, rgb
+
+
+UNIFORM_BLOCK = 50_000_000
+
+
+def make_uniform_range(lo, hi, device, seed, alloc=None):
+    """Points [lo, hi) of a fixed uniform cloud whose 50M-point blocks are
+    seeded by block number: every shard layout (any GPU count) sees the same
+    global cloud, so strong-scaling runs render identical frames."""
+    import torch
+
+    alloc = alloc or (lambda shape, dt: torch.empty(shape, dtype=dt, device=device))
+    pos = alloc((hi - lo, 3), torch.float32)
+    rgb = alloc((hi - lo, 3), torch.uint8)
+    for b in range(lo // UNIFORM_BLOCK, (hi + UNIFORM_BLOCK - 1) // UNIFORM_BLOCK):
+        b0, b1 = b * UNIFORM_BLOCK, (b + 1) * UNIFORM_BLOCK
+        g = torch.Generator(device=device).manual_seed(seed * 1_000_003 + b)
+        bp = torch.empty((UNIFORM_BLOCK, 3), dtype=torch.float32, device=device).uniform_(
+            -1.0, 1.0, generator=g)
+        bc = torch.randint(0, 256, (UNIFORM_BLOCK, 3), device=device, generator=g,
+                           dtype=torch.int32).to(torch.uint8)
+        s0, s1 = max(lo, b0), min(hi, b1)
+        pos[s0 - lo:s1 - lo] = bp[s0 - b0:s1 - b0]
+        rgb[s0 - lo:s1 - lo] = bc[s0 - b0:s1 - b0]
+        del bp, bc
     return pos, rgb
 
 
@@ -313,39 +360,138 @@ def run_gsplat(dev, W, H, n=400_000, cpu=True):
     return out
 
 
+def _reference_package():
+    """The unmodified reference package installed into baseline/_ref
+    (``pip install --no-deps --target baseline/_ref``), or None."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "nar" / "__init__.py").exists():
+        return None
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    try:
+        import nar  # noqa: F401
+        from nar import _kernels
+
+        if "native" not in _kernels.available_backends():
+            return None
+        return nar
+    except Exception as e:  # broken install: fall back to oracle/_ref
+        log(f"[reference] baseline/_ref unusable ({e})")
+        return None
+
+
+def _host_cloud(workload, n_pts, seed=1234):
+    wl = WORKLOADS[workload]
+    """The workload's synthetic cloud on the host: generated on the GPU with the
+    same generator and seed as our arm's rank 0 (so both arms render the same
+    points), or with numpy when no GPU is present."""
+    import numpy as np
+
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            dev = torch.device("cuda", 0)
+            if wl.cloud == "trajectories":
+                parts = [make_trajectories(n_pts // 4, dev, seed=s) for s in range(4)]
+                out = tuple(torch.cat([p[k] for p in parts]).cpu().numpy() for k in range(3))
+            elif wl.cloud == "terrain":
+                out = tuple(t.cpu().numpy() for t in make_terrain(n_pts, dev, seed=seed))
+            elif wl.scaling == "strong":
+                out = tuple(t.cpu().numpy() for t in make_uniform_range(0, n_pts, dev, seed))
+            else:
+                out = tuple(t.cpu().numpy() for t in make_uniform(n_pts, dev, seed=seed))
+            torch.cuda.empty_cache()
+            return out, "same device-generated cloud as the GPU arm (rank 0), copied to the host"
+    except Exception as e:
+        log(f"[reference] GPU generation failed ({e}); numpy cloud")
+    rng = np.random.default_rng(seed)
+    pos = np.empty((n_pts, 3), np.float32)
+    for lo in range(0, n_pts, 50_000_000):
+        hi = min(n_pts, lo + 50_000_000)
+        pos[lo:hi] = rng.uniform(-1, 1, (hi - lo, 3))
+    rgb = rng.integers(0, 256, (n_pts, 3), dtype=np.uint8)
+    return (pos, rgb), "numpy uniform cloud (no GPU for the shared generator)"
+
+
 def main_reference(args):
-    """--impl reference: the reference CPU implementation on the host cores."""
+    """--impl reference: the reference's own CPU implementation on the host cores,
+    on the same workload as our arm.  With the reference package installed in
+    baseline/_ref, every step is its public ``nar.msr.rasterize(pc, cam, sel,
+    threads=cores, backend="native")`` (rasterizer.py:123-188: the Cython render
+    kernel under its chunked thread pool, then the numpy resolve) over the FULL
+    cloud; without it, the reference's Cython kernel from oracle/_ref plus the
+    restated resolve."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import oracle
-    from paper_2407_19097_b200.geometry import Intrinsics, look_at
-
-    n_pts, W, H, desc = WORKLOADS[args.workload]
-    oracle.build()
+    wl = WORKLOADS[args.workload]
+    n_pts, W, H, desc, eye = wl.points, wl.width, wl.height, wl.desc, wl.eye
+    if args.points:
+        n_pts = args.points
+    if wl.scaling == "weak":
+        n_pts *= args.gpus  # the whole job's points (one CPU renders all of them)
     threads = os.cpu_count() or 1
-    n_sample = min(n_pts, 20_000_000)
-    pos, rgb = cpu_sample(n_sample, W, H)
-    cam = look_at((0.0, -2.2, 1.0), (0, 0, 0), Intrinsics(width=W, height=H))
+    t0 = time.time()
+    arrays, origin = _host_cloud(args.workload, n_pts)
+    log(f"[reference] {n_pts / 1e6:.0f}M points ready in {time.time() - t0:.1f}s ({origin})")
+    nar = _reference_package()
+    if nar is not None:
+        from nar.geometry import Intrinsics as RI, PointCloud as RPC, Stream as RS, look_at as rla
+        from nar.msr import StreamSelection as RSel, rasterize as rrast
+
+        streams = [RS("rgb", "u8", arrays[1])]
+        if args.workload == "c3":
+            streams.append(RS("velocity", "f32", arrays[2]))
+        pc = RPC(arrays[0], streams)
+        cam = rla(eye, (0.0, 0.0, 0.0), RI(width=W, height=H))
+        sel = RSel(rgb=True, depth=True, vel2d=args.workload == "c3")
+        kind, api = "reference", "nar.msr.rasterize(pc, cam, sel, threads=cores, backend='native') from baseline/_ref"
+        if wl.unet:  # + pad_to_multiple + the numpy U-Net forward (model.py:194-215)
+            from nar.neural import model as rmodel
+            from nar.neural.autodiff import Tensor as RT
+
+            rcfg = rmodel.UNetConfig(input_channels=4)
+            rparams = {k: RT(v) for k, v in rmodel.init_params(rcfg).items()}
+
+            def step():
+                fi = rrast(pc, cam, sel, threads=threads, backend="native")
+                x, _ = rmodel.pad_to_multiple(fi.data, 16)
+                return rmodel.forward(RT(x[None]), rparams, rcfg)
+
+            api += " + nar.neural.forward (pad_to_multiple(16), random init)"
+        else:
+            step = lambda: rrast(pc, cam, sel, threads=threads, backend="native")
+    else:
+        import oracle
+        from paper_2407_19097_b200.geometry import Intrinsics, look_at
+
+        oracle.build()
+        cam = look_at(eye, (0, 0, 0), Intrinsics(width=W, height=H))
+        step = lambda: reference_frame(arrays[0], arrays[1], cam, threads)
+        kind = "reference" if oracle.ref_native() is not None else "port"
+        api = "oracle/_ref Cython kernel + restated resolve" if kind == "reference" else "oracle C port"
     for _ in range(args.warmup):
-        impl = reference_frame(pos, rgb, cam, threads)
+        step()
     times = []
     for _ in range(args.steps):
-        t0 = time.perf_counter()
-        impl = reference_frame(pos, rgb, cam, threads)
-        times.append(time.perf_counter() - t0)
+        t1 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t1)
     dt = sum(times) / len(times)
-    v = n_sample / dt / 1e9
-    kind = "reference" if impl == "reference" else "port"
-    sample = f"{n_sample} of {n_pts} points per step at {W}x{H} (RGB+D render+resolve)"
+    v = n_pts / dt / 1e9
+    sample = f"full workload: {n_pts} points per step at {W}x{H} ({origin})"
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "Gpts/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": wl.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": desc, "sample_points": n_sample, "width": W, "height": H},
+        "config": {"workload": desc, "points": n_pts, "width": W, "height": H,
+                   "same_config": True},
+        "fps": 1.0 / dt,
         "cpu_baseline": {"value": v, "unit": "Gpts/s", "cores": threads, "kind": kind,
-                         "sample": sample},
+                         "sample": sample, "api": api,
+                         "ms_per_step_min": min(times) * 1e3},
         "e2e": {"value": v, "unit": "Gpts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -353,6 +499,56 @@ def main_reference(args):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+def _parity_check(cloud, cam, sel, r, out_names, threads):
+    """After timing (N=1): the frame's keybuf and G-buffer against the CPU oracle
+    on the same points (oracle/zbuffer.c under a pthread pool + the numpy
+    resolve -- both pinned to the reference's golden vectors by
+    tests/test_oracle.py).  Keybuf: SHA-256 equality; planes and rgb/d
+    channels bit-exact, vel channels <= 1 f32 ulp."""
+    import hashlib
+
+    import numpy as np
+    import torch
+
+    import oracle
+    from paper_2407_19097_b200.geometry import PointCloud, Stream
+
+    oracle.build()
+    t0 = time.time()
+    r.render(cloud, cam)
+    ours_kb = r.keys()
+    img = r.resolve(cloud, cam, sel).to_host()
+    torch.cuda.synchronize()
+    segs = sorted(cloud.segments, key=lambda sg: sg["begin"])
+    if segs[0]["begin"] != 0 or any(a["begin"] + a["count"] != b["begin"]
+                                    for a, b in zip(segs, segs[1:])):
+        return {"checked": False, "why": "segments are not one contiguous index range"}
+    pos = torch.cat([sg["positions"] for sg in segs]).cpu().numpy()
+    streams = [Stream(name, m.format, torch.cat([sg["streams"][name] for sg in segs]).cpu().numpy())
+               for name, m in cloud.meta.items()]
+    pc = PointCloud(pos, streams)
+    t1 = time.time()
+    ref = oracle.rasterize(pc, cam, sel, threads=threads)
+    t2 = time.time()
+    sha = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+    ours_sha, ref_sha = sha(ours_kb), sha(ref["keybuf"])
+    nexact = 4 if sel.rgb and sel.depth else len(out_names)
+    ai = img.data[..., nexact:].view(np.int32).astype(np.int64)
+    bi = ref["data"][..., nexact:].view(np.int32).astype(np.int64)
+    ulp = int(np.abs(np.where(ai < 0, -(ai & 0x7FFFFFFF), ai) -
+                     np.where(bi < 0, -(bi & 0x7FFFFFFF), bi)).max()) if ai.size else 0
+    gb = (np.array_equal(img.index_plane, ref["index_plane"]) and
+          np.array_equal(img.depth, ref["depth"]) and
+          np.array_equal(img.coverage, ref["coverage"]) and
+          np.array_equal(img.data[..., :nexact], ref["data"][..., :nexact]) and ulp <= 1)
+    return {"checked": True, "keybuf_sha_match": ours_sha == ref_sha, "keybuf_sha256": ours_sha,
+            "gbuffer_match": bool(gb), "vel_max_ulp": ulp if ai.size else None,
+            "points": int(pos.shape[0]),
+            "oracle": f"oracle.rasterize (C restatement of _native.pyx:56-77, {threads} threads, "
+                      f"+ numpy resolve of rasterizer.py:140-178)",
+            "oracle_s": round(t2 - t1, 2), "total_s": round(time.time() - t0, 2)}
+
+
 def main_ours(args):
     import numpy as np
     import torch
@@ -361,6 +557,7 @@ def main_ours(args):
     from paper_2407_19097_b200 import _lib
     from paper_2407_19097_b200.geometry import Intrinsics, PointCloud, Stream, look_at
     from paper_2407_19097_b200.msr import DeviceCloud, Renderer, StreamSelection, rasterize
+    from paper_2407_19097_b200.parallel import shard_range
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -370,41 +567,60 @@ def main_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     _lib.load()
-    n_pts, W, H, desc = WORKLOADS[args.workload]
-    if args.points:
-        n_pts = args.points
+    wl = WORKLOADS[args.workload]
+    W, H, desc = wl.width, wl.height, wl.desc
+    n_arg = args.points or wl.points
+    if wl.scaling == "strong":  # a fixed cloud, 1/N of it per rank
+        lo, hi = shard_range(n_arg, rank, world)
+    else:  # a fixed shard per rank
+        lo, hi = rank * n_arg, (rank + 1) * n_arg
+    n_local = hi - lo
+    peer_wanted = world > 1 and args.composite == "peer" and wl.cloud != "trajectories"
 
-    # ---- data (per-rank shard: weak scaling) --------------------------------
+    # ---- data: the rank's shard, generated in place ------------------------------
+    alloc = None
+    if peer_wanted:
+        # the shard lives in symmetric memory from the start, so the fused
+        # composite maps it into every rank without a copy (equal shapes needed)
+        import torch.distributed._symmetric_memory as symm
+
+        counts = [None] * world
+        dist.all_gather_object(counts, n_local)
+        if len(set(counts)) == 1:
+            alloc = lambda shape, dt: symm.empty(shape, dtype=dt, device=dev)
     t_gen = time.time()
-    if args.workload == "c3":
-        clouds, streams = [], []
+    if wl.cloud == "trajectories":
+        clouds = []
         for s in range(4):
-            p, c, v = make_trajectories(n_pts // 4, dev, seed=rank * 4 + s)
-            clouds.append({"begin": rank * n_pts + s * (n_pts // 4), "positions": p,
+            p, c, v = make_trajectories(n_local // 4, dev, seed=rank * 4 + s)
+            clouds.append({"begin": lo + s * (n_local // 4), "positions": p,
                            "streams": {"rgb": c, "velocity": v}})
         from paper_2407_19097_b200.msr import _StreamMeta
 
         meta = {"rgb": _StreamMeta("rgb", "u8", 3), "velocity": _StreamMeta("velocity", "f32", 3)}
         cloud = DeviceCloud(clouds, meta, dev)
         sel = StreamSelection(rgb=True, depth=True, vel2d=True)
-        eye = (0.0, -2.6, 1.4)
     else:
-        gen = make_terrain if args.workload == "c4" else make_uniform
-        pos, rgb = gen(n_pts, dev, seed=1234 + rank)
-        cloud = DeviceCloud.from_tensors(pos, {"rgb": rgb}, begin=rank * n_pts)
+        if wl.cloud == "terrain":
+            pos, rgb = make_terrain(n_local, dev, seed=1234 + rank)
+        elif wl.scaling == "strong":
+            pos, rgb = make_uniform_range(lo, hi, dev, seed=1234, alloc=alloc)
+        else:
+            pos, rgb = make_uniform(n_local, dev, seed=1234 + rank, alloc=alloc)
+        cloud = DeviceCloud.from_tensors(pos, {"rgb": rgb}, begin=lo)
         sel = StreamSelection(rgb=True, depth=True)
-        eye = (0.0, -1.6, 1.2) if args.workload == "c4" else (0.0, -2.2, 1.0)
     torch.cuda.synchronize()
+    torch.cuda.empty_cache()
     log(f"[rank {rank}] generated {cloud.count / 1e6:.0f}M points in {time.time() - t_gen:.1f}s")
-    cam = look_at(eye, (0, 0, 0), Intrinsics(width=W, height=H))
+    cam = look_at(wl.eye, (0, 0, 0), Intrinsics(width=W, height=H))
     composite = None
     pr = None
     if world > 1:
         from paper_2407_19097_b200.parallel import PeerShardedRenderer, ShardedRenderer
 
-        if args.composite == "peer" and len(cloud.segments) == 1:
+        if peer_wanted:
             try:  # fused composite + resolve over symmetric (NVLink peer) memory
-                pr = PeerShardedRenderer(W, H, cloud)
+                pr = PeerShardedRenderer(W, H, cloud, shard_is_symmetric=alloc is not None)
                 composite = "fused peer-memory composite+resolve (nar_resolve_peers)"
             except Exception as e:  # no symmetric memory here: NCCL path
                 log(f"[rank {rank}] peer path unavailable ({e}); using NCCL")
@@ -441,7 +657,7 @@ def main_ours(args):
             ok.zero_()
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)
         if ok.item() == 1.0:
-            cloud = pr.local  # render the symmetric-memory copy of the shard
+            cloud = pr.local  # the symmetric-memory shard (the same tensors when allocated there)
             composite += " (validated against the NCCL path)"
         else:
             log(f"[rank {rank}] fused composite mismatch; timing the NCCL path")
@@ -451,20 +667,22 @@ def main_ours(args):
         del chk
 
     unet = None
-    if args.workload == "c4":
+    if wl.unet:
         from paper_2407_19097_b200.neural import UNet, UNetConfig, init_params
 
         cfg = UNetConfig(input_channels=len(names))
         unet = UNet(cfg, init_params(cfg), device=dev)
         ph, pw = out["data"].shape[:2]
         unet_out = torch.empty((ph, pw, 3), dtype=torch.float32, device=dev)
+    root_data = pr_out[0]["data"] if pr is not None else out["data"]
 
-    def frame(ev_r0=None, ev_r1=None):
-        if ev_r0 is not None:
-            ev_r0.record(main)
+    def frame(evs=None):
+        """evs: 4 events -> render | composite + resolve | U-Net boundaries."""
+        if evs is not None:
+            evs[0].record(main)
         r.render(cloud, cam)
-        if ev_r1 is not None:
-            ev_r1.record(main)
+        if evs is not None:
+            evs[1].record(main)
         if world > 1 and pr is not None:
             from paper_2407_19097_b200.parallel import row_slice
 
@@ -481,8 +699,12 @@ def main_ours(args):
             reduce_planes(out["data"], dst=0)
         else:
             r.resolve(cloud, cam, sel, out=out)
+        if evs is not None:
+            evs[2].record(main)
         if unet is not None and rank == 0:
-            unet.forward_into(out["data"], unet_out)
+            unet.forward_into(root_data, unet_out)
+        if evs is not None:
+            evs[3].record(main)
 
     for _ in range(args.warmup):  # synchronised: the renderer's pass statistics land
         frame()
@@ -491,24 +713,22 @@ def main_ours(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    from paper_2407_19097_b200 import _lib as nar_lib
-
-    n_launch0 = nar_lib.launch_count()
+    n_launch0 = _lib.launch_count()
     t0 = time.time()
     e0.record(main)
     for k in range(args.steps):
-        frame(*evs[k])
+        frame(evs[k])
     e1.record(main)
-    n_launches = nar_lib.launch_count() - n_launch0
+    n_launches = _lib.launch_count() - n_launch0
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     t1 = time.time()
     total_ms = e0.elapsed_time(e1)
-    render_ms = [a.elapsed_time(b) for a, b in evs]
+    stage = [[a.elapsed_time(b) for a, b in zip(ev[:-1], ev[1:])] for ev in evs]
+    render_ms = [st[0] for st in stage]
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -517,47 +737,69 @@ def main_ours(args):
     if sampler:
         sampler.stop()
     ms_step = total_ms / args.steps
-    pts_total = cloud.count * world
+    pts_total = cloud.count * world if wl.scaling == "weak" else n_arg
     value = pts_total / (ms_step * 1e-3) / 1e9
     render_avg = sum(render_ms) / len(render_ms)
     peaks, peak_kind = measured_peaks()
     achieved = cloud.count * BYTES_PER_POINT / (render_avg * 1e-3) / 1e9
+    med = lambda xs: sorted(xs)[len(xs) // 2]
+    stages = {"render": med([st[0] for st in stage]),
+              ("composite_resolve" if world > 1 else "resolve"): med([st[1] for st in stage])}
+    if unet is not None:
+        stages["unet"] = med([st[2] for st in stage])
+    breakdown = {"stage_ms_median_rank0": stages,
+                 "composite_share": (stages.get("composite_resolve", 0.0) / ms_step
+                                     if world > 1 else None)}
+
+    # ---- parity of the timed frame against the CPU oracle (N=1) -------------------
+    parity = None
+    if world == 1 and not args.no_parity:
+        try:
+            parity = _parity_check(cloud, cam, sel, r, names, os.cpu_count() or 4)
+        except MemoryError as e:
+            parity = {"checked": False, "why": f"host memory ({e})"}
+        torch.cuda.empty_cache()
 
     # ---- e2e through the reference-facing API (host buffers) -----------------
     e2e = None
-    if not args.no_e2e and world == 1 and args.workload in ("c1", "c2"):
-        host_pos = torch.empty((cloud.count, 3), dtype=torch.float32, pin_memory=True)
-        host_rgb = torch.empty((cloud.count, 3), dtype=torch.uint8, pin_memory=True)
-        host_pos.copy_(cloud.segments[0]["positions"])
-        host_rgb.copy_(cloud.segments[0]["streams"]["rgb"])
-        pc = PointCloud.__new__(PointCloud)
-        pc.positions, pc.pinned = host_pos.numpy(), True
-        pc.streams = [Stream.__new__(Stream)]
-        pc.streams[0].name, pc.streams[0].format, pc.streams[0].data = "rgb", "u8", host_rgb.numpy()
+    if not args.no_e2e and world == 1 and len(cloud.segments) == 1 and not wl.unet:
+        seg = cloud.segments[0]
+        host_pos = seg["positions"].cpu().numpy()  # pageable: a stock caller's arrays
+        host_rgb = seg["streams"]["rgb"].cpu().numpy()
         k_e2e = max(2, min(args.steps, 5))
-        rasterize(pc, cam, sel)  # warm
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(main)
-        for _ in range(k_e2e):
-            fi = rasterize(pc, cam, sel)
-        b.record(main)
-        torch.cuda.synchronize()
-        e2e_ms = a.elapsed_time(b) / k_e2e
+
+        def timed_rasterize(pc):
+            rasterize(pc, cam, sel)  # warm (staging buffers, pinned output pool)
+            torch.cuda.synchronize()
+            a = time.perf_counter()
+            for _ in range(k_e2e):
+                fi = rasterize(pc, cam, sel)  # returns after the D2H has landed
+            return (time.perf_counter() - a) / k_e2e * 1e3, fi
+
+        # the stock drop-in caller: pageable numpy arrays in a plain PointCloud
+        pg_ms, fi = timed_rasterize(PointCloud(host_pos, [Stream("rgb", "u8", host_rgb)]))
         d2h = fi.data.nbytes + fi.coverage.nbytes + fi.index_plane.nbytes + fi.depth.nbytes
-        # points are DMA-copied; rgb stays in pinned host memory and the resolve
-        # reads the winners' 3 bytes in place (zero-copy), one per covered pixel
+        del fi
+        # PointCloud(..., pinned=True): points DMA'd, rgb gathered in place (zero-copy)
+        pc_pin = PointCloud(host_pos, [Stream("rgb", "u8", host_rgb)], pinned=True)
+        pin_ms, fi = timed_rasterize(pc_pin)
         gathered = int(fi.coverage.astype(bool).sum()) * 3
-        e2e = {"value": cloud.count / (e2e_ms * 1e-3) / 1e9, "unit": "Gpts/s",
-               "h2d_bytes_per_step": int(host_pos.numel() * 4 + gathered),
+        e2e = {"value": cloud.count / (pin_ms * 1e-3) / 1e9, "unit": "Gpts/s",
+               "h2d_bytes_per_step": int(host_pos.nbytes + gathered),
                "h2d_note": "positions DMA (12 B/pt) + zero-copy gather of winners' rgb",
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms,
-               "api": "paper_2407_19097_b200.msr.rasterize(pinned host PointCloud)"}
-        del host_pos, host_rgb, pc
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": pin_ms,
+               "api": "paper_2407_19097_b200.msr.rasterize(PointCloud(..., pinned=True))",
+               "pageable": {"value": cloud.count / (pg_ms * 1e-3) / 1e9, "unit": "Gpts/s",
+                            "ms_per_step": pg_ms,
+                            "h2d_bytes_per_step": int(host_pos.nbytes + host_rgb.nbytes),
+                            "d2h_bytes_per_step": int(d2h),
+                            "api": "paper_2407_19097_b200.msr.rasterize(PointCloud(numpy arrays)) "
+                                   "-- the stock drop-in caller (staged H2D of points + rgb)"}}
+        del host_pos, host_rgb, pc_pin, fi
 
     # ---- full NAR frame on the same cloud: render + resolve + U-Net ----------
     pipeline = None
-    if world == 1 and args.workload in ("c2", "c3") and not args.no_pipeline:
+    if world == 1 and not wl.unet and args.workload in ("c2", "c3") and not args.no_pipeline:
         from paper_2407_19097_b200.neural import UNetConfig, init_params
         from paper_2407_19097_b200.pipeline import NeuralRenderer
 
@@ -568,7 +810,6 @@ def main_ours(args):
             nr.frame(cloud, cam, stream=main)
         kp = max(3, min(args.steps, 20))
         ts = [nr.frame(cloud, cam, stream=main)[1] for _ in range(kp)]
-        med = lambda xs: sorted(xs)[len(xs) // 2]
         tot = med([t.total_ms for t in ts])
         un = med([t.unet_ms for t in ts])
         ph, pw = nr._out["data"].shape[:2]
@@ -584,7 +825,7 @@ def main_ours(args):
 
     # ---- the same frame on the Morton-ordered cloud ------------
     morton = None
-    if world == 1 and len(cloud.segments) == 1 and not args.no_morton:
+    if world == 1 and len(cloud.segments) == 1 and not args.no_morton and not wl.unet:
         from paper_2407_19097_b200.preprocess import morton_reorder
 
         ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -618,12 +859,12 @@ def main_ours(args):
 
     # ---- Gaussian-splat ground-truth renderer (§8f): GPU blend vs the reference's
     gsplat = None
-    if world == 1 and not args.no_gsplat:
+    if world == 1 and not args.no_gsplat and args.workload in ("c1", "c2"):
         gsplat = run_gsplat(dev, W, H, cpu=not args.no_cpu)
 
     cpu = None
-    if not args.no_cpu and world == 1 and rank == 0:
-        cpu = run_cpu_baseline(W, H, min(n_pts, 35_000_000))
+    if not args.no_cpu and world == 1 and rank == 0 and wl.cloud == "uniform":
+        cpu = run_cpu_baseline(W, H, min(cloud.count, 35_000_000))
 
     traffic = None
     tp = ROOT / "profiles" / "render_traffic.json"
@@ -639,21 +880,26 @@ def main_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": "Gpts/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": wl.scaling, "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": desc, "points_per_gpu": cloud.count, "width": W, "height": H,
+            "config": {"workload": desc, "name": args.workload, "points_total": pts_total,
+                       "points_per_gpu": cloud.count, "width": W, "height": H,
                        "selection": list(names), "order": "storage (random)",
+                       "unet": ("UNetConfig(input_channels=4), random init, on rank 0"
+                                if wl.unet else None),
                        "l2": f"inputs {cloud.count * 12 / 1e9:.1f} GB per GPU > 126 MB L2 (no flush needed)",
                        "parallelism": f"points sharded over {world} GPU(s)" if world > 1 else "1 GPU",
                        "composite": composite},
             "fps": 1e3 / ms_step,
             "render_ms": render_avg,
+            "frame": breakdown,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
                          "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
                          "frac_nominal_8tbs": achieved / 8000.0,
                          "traffic": traffic, "peak_kind": peak_kind,
                          "kernel": "render passes (render_pre_kernel + seed render_tma_kernel + hiz_kernel)",
                          "bytes_per_point": BYTES_PER_POINT},
+            "parity": parity,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "pipeline": pipeline,
@@ -670,11 +916,12 @@ def main_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
-    ap.add_argument("--points", type=int, default=0, help="override points per GPU")
+    ap.add_argument("--points", type=int, default=0,
+                    help="override the workload's points (per GPU, or total for strong scaling)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-morton", action="store_true")
     ap.add_argument("--no-gsplat", action="store_true")
@@ -682,6 +929,8 @@ def main():
                     help="N>1: fused peer-memory composite+resolve or the NCCL path")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-pipeline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true",
+                    help="skip the post-timing keybuf/G-buffer check against the CPU oracle")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

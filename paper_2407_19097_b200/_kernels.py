@@ -2,10 +2,11 @@
 
 The reference picks an implementation module by name ("native" Cython loop or
 "python" numpy twin, ``_resolve`` at :45-53).  This build has exactly one
-backend, ``"cuda"``: the sm_100a kernels behind libnar_b200.so.  Asking for
-any other name raises ``ValueError`` (as the reference does for unknown
-names); a missing library raises ``RuntimeError("cuda kernels are not
-built")``.  There is no CPU fallback.
+backend, ``"cuda"``: the sm_100a kernels behind libnar_b200.so; the reference
+name ``"native"`` is an alias of it (a drop-in caller asking for the compiled
+backend gets this one), ``"python"`` raises ``RuntimeError`` (not built: there
+is no CPU fallback) and any other name ``ValueError``, as in the reference; a
+missing library raises ``RuntimeError("cuda kernels are not built")``.
 
 ``zbuffer_render`` keeps the reference signature (``threads`` is accepted
 for compatibility; the GPU render has no thread-count knob and its result is
@@ -29,11 +30,20 @@ def available_backends() -> list[str]:
 
 
 def _resolve(backend: str | None) -> str:
+    """Backend names (reference _kernels/__init__.py:45-53): ``"cuda"`` and the
+    reference's ``"native"`` (this build *is* the compiled backend a caller
+    asks for by that name) select the sm_100a kernels; ``"python"`` -- the
+    reference's numpy twin -- raises RuntimeError, as the reference does for a
+    backend that is not built (there is no CPU path here); anything else
+    raises ValueError."""
     name = backend or BACKEND
-    if name != "cuda":
+    if name == "python":
+        raise RuntimeError("python kernels are not part of this build (no CPU fallback); "
+                           "use backend='cuda'")
+    if name not in ("cuda", "native"):
         raise ValueError(f"unknown kernel backend {name!r}")
     _lib.load()
-    return name
+    return "cuda"
 
 
 def _as_f64_3x3(R) -> np.ndarray:

@@ -228,6 +228,32 @@ def stream_handle(stream, device_index: int | None = None) -> int:
     return int(stream.cuda_stream)
 
 
+class on_device:
+    """Makes CUDA device ``index`` current for the enclosed library calls (the
+    library keys its per-device state and launches on the current device);
+    a no-op when it already is."""
+
+    __slots__ = ("index", "prev")
+
+    def __init__(self, index: int | None):
+        self.index = index
+
+    def __enter__(self):
+        import torch
+
+        self.prev = torch.cuda.current_device()
+        if self.index is not None and self.index != self.prev:
+            torch.cuda.set_device(self.index)
+        return self
+
+    def __exit__(self, *exc):
+        import torch
+
+        if self.index is not None and self.index != self.prev:
+            torch.cuda.set_device(self.prev)
+        return False
+
+
 def mapped_pointer(host_ptr: int):
     """Device address of mapped pinned host memory, or None (pageable memory)."""
     out = C.c_void_p()

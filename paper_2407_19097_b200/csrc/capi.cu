@@ -35,8 +35,8 @@ uint64_t launch_total() { return g_launches.load(std::memory_order_relaxed); }
 // release threshold is 0 by default, so every synchronisation would hand the
 // memory back and the next call would map it again).
 void keep_pool_memory() {
-  static std::once_flag once;
-  std::call_once(once, [] {
+  static std::once_flag once[kMaxDevices];
+  std::call_once(once[current_device()], [] {
     int dev = 0;
     cudaMemPool_t pool;
     if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {

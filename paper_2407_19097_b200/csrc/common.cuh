@@ -18,6 +18,17 @@ uint64_t launch_total();
 // keeps cudaMallocAsync scratch mapped across calls (default pool threshold)
 void keep_pool_memory();
 
+// Per-device state (kernel attributes, SM counts, staging buffers) is indexed
+// by the calling thread's current device: the library works on whichever
+// device the caller made current (the Python shim makes the tensors' device
+// current around every call).
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDevices) d = 0;
+  return d;
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

@@ -927,11 +927,20 @@ __global__ void __launch_bounds__(256)
                          (idx - P.seg[s].begin) * sel.rgb_arity;
       // the 3 bytes through one aligned 8-byte load (two when they straddle):
       // attributes in mapped host memory cost one PCIe read per load
+      // -- only where the aligned words lie inside the stream's own bytes
+      // [base, base + count * arity); at its first / last bytes, byte loads
       const uintptr_t ca = reinterpret_cast<uintptr_t>(c);
       const uint32_t off = (uint32_t)(ca & 7u);
-      const unsigned long long* w8 = reinterpret_cast<const unsigned long long*>(ca - off);
-      uint64_t w = __ldg(w8) >> (8u * off);
-      if (off > 5u) w |= __ldg(w8 + 1) << (8u * (8u - off));
+      const uintptr_t lo = reinterpret_cast<uintptr_t>(P.seg[s].rgb);
+      const uintptr_t hi = lo + (uintptr_t)P.seg[s].count * (uintptr_t)sel.rgb_arity;
+      uint64_t w;
+      if (ca - off >= lo && ca - off + (off > 5u ? 16u : 8u) <= hi) {
+        const unsigned long long* w8 = reinterpret_cast<const unsigned long long*>(ca - off);
+        w = __ldg(w8) >> (8u * off);
+        if (off > 5u) w |= __ldg(w8 + 1) << (8u * (8u - off));
+      } else {
+        w = (uint64_t)__ldg(c) | ((uint64_t)__ldg(c + 1) << 8) | ((uint64_t)__ldg(c + 2) << 16);
+      }
       v.x = __fdiv_rn((float)(uint32_t)(w & 0xFFu), 255.0f);
       v.y = __fdiv_rn((float)(uint32_t)((w >> 8) & 0xFFu), 255.0f);
       v.z = __fdiv_rn((float)(uint32_t)((w >> 16) & 0xFFu), 255.0f);
@@ -1010,12 +1019,13 @@ __global__ void __launch_bounds__(256)
 // host side
 // ----------------------------------------------------------------------------
 static int g_num_sms = 0;
-static std::once_flag g_init_once;
+static std::once_flag g_init_once[kMaxDevices];  // kernel attributes are per device
 static bool g_no_pre = false;  // NAR_RENDER_NO_PRETEST=1: exact-path-only Hi-Z passes
 
 static int device_init() {
   int err = 0;
-  std::call_once(g_init_once, [&]() {
+  const int cur = current_device();
+  std::call_once(g_init_once[cur], [&]() {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) { err = 1; return; }
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1287,7 +1297,7 @@ struct HostPath {
   cudaStream_t cp = nullptr;
   cudaEvent_t copied[2] = {nullptr, nullptr}, done[2] = {nullptr, nullptr};
 };
-static HostPath g_host;
+static HostPath g_host[kMaxDevices];  // staging + Hi-Z scratch of each device
 
 static int host_path_reserve(HostPath& h, int64_t chunk) {
   if (!h.cp) {
@@ -1321,7 +1331,7 @@ static int render_host_impl(uint64_t* keybuf_dev, const float* pos_host, int64_t
   if (n <= 0) return NAR_OK;
   const int64_t kChunk = (int64_t)1 << 23;  // 8 Mi points = 96 MiB per buffer
   const int64_t chunk = n < kChunk ? ((n + kTilePts - 1) / kTilePts) * kTilePts : kChunk;
-  HostPath& h = g_host;
+  HostPath& h = g_host[current_device()];
   std::lock_guard<std::mutex> lock(h.mu);
   int rc = host_path_reserve(h, chunk);
   if (rc) return rc;

@@ -425,8 +425,26 @@ static Plan make_plan(const nar_unet& n, int H, int W) {
   return p;
 }
 
+// Device copies of the parameters; re-run after any nar_unet_set_param.  The
+// previous copies are released first (cudaFree waits for in-flight work that
+// may still read them); set_param must not race a forward on another thread.
 static int upload(nar_unet* n) {
   if (n->uploaded) return NAR_OK;
+  auto release = [](auto*& p) {
+    if (p) cudaFree(p);
+    p = nullptr;
+  };
+  release(n->d_head_w);
+  release(n->d_head_b);
+  release(n->d_out_w);
+  release(n->d_out_b);
+  for (auto& l : n->layers) {
+    release(l.wf32);
+    release(l.wg32);
+    release(l.bf);
+    release(l.bg);
+    release(l.wtc);
+  }
   auto dup = [](const std::vector<float>& v, float** d) -> int {
     if (cudaMalloc(d, v.size() * 4 + 4) != cudaSuccess) return 1;
     cudaMemcpy(*d, v.data(), v.size() * 4, cudaMemcpyHostToDevice);

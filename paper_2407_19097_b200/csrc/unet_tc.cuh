@@ -124,12 +124,19 @@ __host__ __device__ constexpr int tc_smem(int N, int NB) {
   return tc_stages(N, NB) * tc_stage_bytes(N, NB) + tc_fixed_smem(N);
 }
 
+// Padded output width of the f (and g) half: the kernel is instantiated for
+// N = 2 * {8, 16, 24, 32, 48, 64, 96, 128}; other widths round up to the next
+// one (the extra columns carry zero weights and bias, so they gate to 0).
+__host__ __device__ constexpr int tc_coutp(int cout) {
+  return cout <= 32 ? (cout + 7) / 8 * 8 : cout <= 48 ? 48 : cout <= 64 ? 64 : cout <= 96 ? 96 : 128;
+}
+
 // Host: pack HWIO f32 weights into bf16 [chunk q][tap][k8][n][8] where
 // n < Coutp indexes f outputs and n >= Coutp g outputs (zero padded).
 // Sliding layers (tc_slide(N)): [chunk q][kx][k8][n' = (2 - ky) * N + n][8].
 inline void tc_pack_weights(const std::vector<float>& wf, const std::vector<float>& wg, int ca,
                             int cb, int cout, std::vector<uint16_t>& packed) {
-  const int coutp = (cout + 7) / 8 * 8, N = 2 * coutp;
+  const int coutp = tc_coutp(cout), N = 2 * coutp;
   const bool slide = tc_slide(N);
   const int nqa = (ca + 15) / 16, nqb = (cb + 15) / 16, nq = nqa + nqb, cin = ca + cb;
   packed.assign((size_t)nq * 9 * 2 * N * 8, 0);
@@ -662,13 +669,11 @@ static int tc_make_map(CUtensorMap* m, const void* base, int cs, int w, int h, i
 // Single TMEM buffer (twice the rows) only for weight-heavy layers where the
 // bigger tile costs no extra wave; the rest keep double buffering's overlap.
 inline int tc_sm_count() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = 148;
-  }
-  return sms;
+  static int sms[kMaxDevices] = {};
+  const int dev = current_device();
+  if (!sms[dev] && cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    sms[dev] = 148;
+  return sms[dev];
 }
 inline int tc_bufs_for(int N, int H, int W, int nq) {
   // weight-heavy: N = 256 always; N = 128 from 8 chunks (decoder concat layers)
@@ -679,14 +684,16 @@ inline int tc_bufs_for(int N, int H, int W, int nq) {
   return w1 * R1 <= w2 * R2 ? 1 : 2;  // no more row-waves with the bigger tile
 }
 inline int tc_rows_for(int cout, int H, int W, int nq) {
-  const int N = 2 * ((cout + 7) / 8 * 8);
+  const int N = 2 * tc_coutp(cout);
   return tc_rows(N, tc_bufs_for(N, H, W, nq));
 }
 
 template <int N, bool kHead, int NB>
 static int tc_launch_nhb(const ConvArgs& a, cudaStream_t st) {
-  static bool attr_done = false;
-  if (!attr_done) {
+  // kernel attributes are per device: set once on each device used
+  static bool attr_done[kMaxDevices] = {};
+  const int dev = current_device();
+  if (!attr_done[dev]) {
     const cudaError_t e =
         cudaFuncSetAttribute(gated_conv_tc<N, kHead, NB>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem(N, NB));
@@ -696,7 +703,7 @@ static int tc_launch_nhb(const ConvArgs& a, cudaStream_t st) {
                cudaGetErrorString(e));
       return set_error(NAR_ERR_CUDA, msg);
     }
-    attr_done = true;
+    attr_done[dev] = true;
   }
   constexpr int R = tc_rows(N, NB);
   if (a.pool_out && (R & 1)) return set_error(NAR_ERR_CONFIG, "fused pool needs an even row tile");
@@ -745,9 +752,10 @@ static int tc_launch_n(const ConvArgs& a, cudaStream_t st) {
 }
 
 inline int tc_launch_gated_conv(const ConvArgs& a, cudaStream_t st) {
-  const int coutp = (a.cout + 7) / 8 * 8;
-  if (a.cout_stride % 8 || a.cout_stride < coutp)
-    return set_error(NAR_ERR_CONFIG, "conv output stride must be a multiple of 8 >= Coutp");
+  if (a.cout < 1 || a.cout > 128) return set_error(NAR_ERR_CONFIG, "conv width must be 1..128");
+  const int coutp = tc_coutp(a.cout);
+  if (a.cout_stride % 8 || a.cout_stride < (a.cout + 7) / 8 * 8)
+    return set_error(NAR_ERR_CONFIG, "conv output stride must be a multiple of 8 >= Cout");
   if (a.ca_stride % 16 || (a.cb && a.cb_stride % 16))
     return set_error(NAR_ERR_CONFIG, "conv input strides must be multiples of 16");
   if (a.head_out && (a.head_n < 1 || a.head_n > 4))

@@ -316,8 +316,9 @@ class Renderer:
         return self.width * self.height
 
     def clear(self, stream=None) -> None:
-        _lib.call("nar_keybuf_fill", self.keybuf.data_ptr(), self.npix,
-                  C.c_uint64(self.empty), _lib.stream_handle(stream, self.device.index))
+        with _lib.on_device(self.device.index):
+            _lib.call("nar_keybuf_fill", self.keybuf.data_ptr(), self.npix,
+                      C.c_uint64(self.empty), _lib.stream_handle(stream, self.device.index))
 
     def _check_cam(self, cam: CameraPose):
         i = cam.intrinsics
@@ -329,6 +330,10 @@ class Renderer:
                multi_stream: bool = True) -> None:
         """Fold every point buffer of ``cloud`` into the keybuf; with several
         buffers and ``multi_stream`` each renders on its own CUDA stream."""
+        with _lib.on_device(self.device.index):
+            self._render(cloud, cam, stream, multi_stream)
+
+    def _render(self, cloud, cam, stream, multi_stream) -> None:
         import torch
 
         kc = self._check_cam(cam)
@@ -400,18 +405,21 @@ class Renderer:
         ro.owner_only, ro.clear_keybuf = int(owner_only), int(clear)
         s = _selection_struct(sel, cloud)
         segs = _segments_struct(cloud, sel)
+        with _lib.on_device(self.device.index):
+            self._resolve_call(kc, s, segs, len(cloud.segments), ro, stream, peers, rows)
+        return DeviceFeatureImage(self.width, self.height, names, out["data"], out["coverage"],
+                                  out["index_plane"], out["depth"])
+
+    def _resolve_call(self, kc, s, segs, nseg, ro, stream, peers, rows) -> None:
         if peers is None:
             _lib.call("nar_resolve", self.keybuf.data_ptr(), C.byref(kc), self.domain, C.byref(s),
-                      segs, len(cloud.segments), C.byref(ro),
-                      _lib.stream_handle(stream, self.device.index))
+                      segs, nseg, C.byref(ro), _lib.stream_handle(stream, self.device.index))
         else:
             arr = (C.c_void_p * len(peers))(*[int(p) for p in peers])
             r0, r1 = rows if rows is not None else (0, -1)
             _lib.call("nar_resolve_peers", arr, len(peers), int(r0), int(r1), C.byref(kc),
-                      self.domain, C.byref(s), segs, len(cloud.segments), C.byref(ro),
+                      self.domain, C.byref(s), segs, nseg, C.byref(ro),
                       _lib.stream_handle(stream, self.device.index))
-        return DeviceFeatureImage(self.width, self.height, names, out["data"], out["coverage"],
-                                  out["index_plane"], out["depth"])
 
     def rasterize(self, cloud: DeviceCloud, cam: CameraPose, sel: StreamSelection, out=None,
                   stream=None) -> DeviceFeatureImage:

@@ -239,22 +239,9 @@ class UNet:
             raise ConfigurationError(f"missing parameters: {sorted(missing)[:4]}")
         with torch.cuda.device(self.device):
             for name in sorted(expected):
-                v = params[name]
-                if hasattr(v, "detach"):
-                    v = v.detach().cpu().numpy()
-                elif hasattr(v, "data") and not isinstance(v, np.ndarray):
-                    v = v.data  # reference autodiff Tensor
-                a = np.ascontiguousarray(v, dtype=np.float32)
+                a = _host_param(params[name])
                 _lib.check(lib.nar_unet_set_param(self._h, name.encode(), a.ctypes.data, a.size))
         self._ws = {}
-
-    def launches_per_forward(self) -> int:
-        """Kernels per forward on the tensor-core path: head+pyramid, the gated
-        convs, plus one standalone pool for levels whose row tile is odd."""
-        L = self.config.levels
-        odd_pool = sum(1 for k in range(L - 1)
-                       if 2 * (-(-self.config.width(k) // 8) * 8) >= 256)
-        return 1 + 2 * L + 2 * (L - 1) + odd_pool
 
     def _workspace(self, H: int, W: int):
         import torch
@@ -287,9 +274,10 @@ class UNet:
         if x.numel() != H * W * int(x.shape[-1]):
             raise ValueError("forward_into takes one image (H, W, C) or (1, H, W, C)")
         ws = self._workspace(H, W)
-        _lib.check(_lib.load().nar_unet_forward(self._h, x.data_ptr(), H, W, out.data_ptr(),
-                                                ws.data_ptr(), ws.numel(),
-                                                _lib.stream_handle(stream)))
+        with _lib.on_device(self.device.index):  # weights upload + launches on self.device
+            _lib.check(_lib.load().nar_unet_forward(
+                self._h, x.data_ptr(), H, W, out.data_ptr(), ws.data_ptr(), ws.numel(),
+                _lib.stream_handle(stream, self.device.index)))
 
     def __call__(self, x):
         import torch
@@ -318,24 +306,37 @@ class UNet:
 _nets: dict = {}
 
 
-def _params_digest(params: dict) -> bytes:
-    import hashlib
+def _host_param(v) -> np.ndarray:
+    """A parameter value as a host f32 array: numpy arrays, reference autodiff
+    Tensors (``.data``) and torch tensors (any device) alike."""
+    if hasattr(v, "detach"):
+        v = v.detach().cpu().numpy()
+    elif hasattr(v, "data") and not isinstance(v, np.ndarray):
+        v = v.data
+    return np.ascontiguousarray(v, dtype=np.float32)
 
-    h = hashlib.blake2b(digest_size=16)
+
+def _params_digest(params: dict) -> tuple:
+    """Content key of a parameter dict: (name, shape, crc32 of the bytes) per
+    entry.  crc32 runs over the buffers in place at several GB/s (~2 ms for the
+    default 10 MB network), so a dict updated in place still repacks."""
+    import zlib
+
+    key = []
     for name in sorted(params):
-        a = np.ascontiguousarray(getattr(params[name], "data", params[name]), np.float32)
-        h.update(name.encode())
-        h.update(str(a.shape).encode())
-        h.update(a.tobytes())
-    return h.digest()
+        a = _host_param(params[name])
+        key.append((name, a.shape, zlib.crc32(memoryview(a).cast("B"))))
+    return tuple(key)
 
 
 def forward(features, params: dict, config: UNetConfig):
     """Full inference path (model.py:194-204): descriptor head, pyramid, U-Net.
 
-    ``features``: (N, H, W, C) f32 numpy array / reference Tensor (returns
-    numpy) or CUDA tensor (returns a CUDA tensor).  H and W must be multiples
-    of 2^(levels-1); use ``pad_to_multiple`` first, as the reference does.
+    ``features``: (N, H, W, C) f32 -- a torch tensor (returns a tensor on the
+    network's device), a reference autodiff ``Tensor`` (returns the same type
+    wrapping the numpy result, so ``.data`` is an ndarray as in model.py:194),
+    or a numpy array (returns numpy).  H and W must be multiples of
+    2^(levels-1); use ``pad_to_multiple`` first, as the reference does.
     """
     import torch
 
@@ -359,5 +360,7 @@ def forward(features, params: dict, config: UNetConfig):
     if isinstance(data, torch.Tensor):
         return net(data)
     x = torch.from_numpy(np.ascontiguousarray(data, dtype=np.float32))
-    y = net(x.to(net.device))
-    return y.cpu().numpy()
+    y = net(x.to(net.device)).cpu().numpy()
+    if data is not features:  # a reference Tensor in -> the same Tensor type out
+        return type(features)(y)
+    return y

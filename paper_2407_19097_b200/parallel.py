@@ -106,7 +106,7 @@ class PeerShardedRenderer:
     """
 
     def __init__(self, width: int, height: int, shard, group=None, pad_multiple: int = 16,
-                 root: int = 0):
+                 root: int = 0, shard_is_symmetric: bool = False):
         import torch
         import torch.distributed as dist
         import torch.distributed._symmetric_memory as symm
@@ -132,9 +132,20 @@ class PeerShardedRenderer:
         nmax = max(c for _, c in counts)
         self._hold = []
 
+        # A shard the caller allocated in symmetric memory (whole symm.empty
+        # buffers, equal counts on all ranks -- ``shard_is_symmetric``) is mapped
+        # as is; otherwise it is copied into symmetric buffers once.
+        in_place = bool(shard_is_symmetric) and len({c for _, c in counts}) == 1
+        flags = [None] * self.world
+        dist.all_gather_object(flags, in_place, group=self.group)
+        in_place = all(flags)
+
         def share(t):
-            buf = symm.empty((nmax,) + tuple(t.shape[1:]), dtype=t.dtype, device=dev)
-            buf[: t.shape[0]].copy_(t)
+            if in_place:
+                buf = t
+            else:
+                buf = symm.empty((nmax,) + tuple(t.shape[1:]), dtype=t.dtype, device=dev)
+                buf[: t.shape[0]].copy_(t)
             h = symm.rendezvous(buf, self.group)
             self._hold.append((buf, h))
             return buf, [int(p) for p in h.buffer_ptrs]

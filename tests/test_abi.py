@@ -54,11 +54,17 @@ def test_no_device_means_clean_status():
 
 
 def test_backend_names():
+    """_kernels/__init__.py:45-53 names: "native" is an alias of the CUDA build
+    (the compiled backend a drop-in caller asks for), "python" is not built
+    (RuntimeError, like the reference's missing native module), others are
+    unknown (ValueError)."""
     assert _kernels.BACKEND == "cuda"
-    with pytest.raises(ValueError):
-        _kernels._resolve("native")
-    with pytest.raises(ValueError):
+    assert _kernels._resolve(None) == "cuda"
+    assert _kernels._resolve("native") == "cuda"
+    with pytest.raises(RuntimeError, match="not part of this build"):
         _kernels._resolve("python")
+    with pytest.raises(ValueError):
+        _kernels._resolve("opencl")
     assert _kernels.EMPTY_KEY == np.uint64(2 ** 64 - 1)
 
 

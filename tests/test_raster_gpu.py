@@ -312,7 +312,9 @@ def test_hiz_pretest_multipass_vs_oracle(cuda, seed, monkeypatch):
 def test_host_path_chunked_hiz(cuda):
     """nar_render_host over 20M host points (three 8 Mi-point staging chunks;
     chunks 2 and 3 are tested against the Hi-Z of the earlier ones) gives the
-    same keybuf as the plain single-pass device render."""
+    same keybuf as the CPU oracle and as the plain single-pass device render."""
+    import os
+
     import torch
 
     from paper_2407_19097_b200 import _kernels
@@ -326,6 +328,9 @@ def test_host_path_chunked_hiz(cuda):
     i = cam.intrinsics
     kb = _kernels.zbuffer_render(pos, cam.orientation, cam.position, i.focal_px, i.cx, i.cy,
                                  i.near, i.far, 1280, 720)
+    ref = oracle.zbuffer_render(pos, cam.orientation, cam.position, i.focal_px, i.cx, i.cy,
+                                i.near, i.far, 1280, 720, threads=os.cpu_count() or 4)
+    assert np.array_equal(kb, ref)  # the host path vs the CPU oracle
     plain = Renderer(1280, 720, device=cuda)
     plain.use_hiz = False
     plain.render(DeviceCloud.from_tensors(torch.from_numpy(pos).to(cuda)), cam)

@@ -259,3 +259,53 @@ def test_gated_conv_single_tmem_buffer(cuda, H, W, cin, cout):
     assert y.shape == ref.shape
     assert np.max(np.abs(y - ref)) <= 2e-2
     assert oracle.psnr(y, ref) >= PSNR_MIN
+
+
+@pytest.mark.parametrize("base", [10, 20, 40])
+def test_forward_other_widths(cuda, base):
+    """Widths without their own kernel instance (20/40/80, 40/80/128, ...) round
+    up to the next one with zero-padded weights (UNetConfig(base_channels=b))."""
+    from paper_2407_19097_b200.neural import forward, init_params
+
+    cfg = _cfg(4, base, 5)
+    params = init_params(cfg)
+    x = np.random.default_rng(base).uniform(0, 1, (1, 64, 96, 4)).astype(np.float32)
+    y = forward(x, params, cfg)
+    ref = oracle.forward(x, params, cfg)
+    assert oracle.psnr(y, ref) >= PSNR_MIN
+    assert np.max(np.abs(y - ref)) <= MAX_ABS
+
+
+def test_forward_returns_reference_tensor_type(cuda):
+    """model.py:194 returns an autodiff Tensor: a Tensor-typed input gets the
+    same type back, with an ndarray in .data."""
+    from paper_2407_19097_b200.neural import forward, init_params
+
+    class Tensor:  # the reference's autodiff.Tensor surface: Tensor(data), .data
+        def __init__(self, data):
+            self.data = np.asarray(data)
+
+    cfg = _cfg(4, 16, 0)
+    params = init_params(cfg)
+    x = np.random.default_rng(9).uniform(0, 1, (1, 32, 48, 4)).astype(np.float32)
+    y = forward(Tensor(x), {k: Tensor(v) for k, v in params.items()}, cfg)
+    assert isinstance(y, Tensor) and isinstance(y.data, np.ndarray)
+    assert y.data.shape == (1, 32, 48, 3)
+    assert oracle.psnr(y.data, oracle.forward(x, params, cfg)) >= PSNR_MIN
+
+
+def test_unet_on_non_current_device_index(cuda):
+    """UNet / Renderer calls make their own device current (the library keys its
+    per-device state on it); with one GPU this checks the guard is a no-op and
+    the raw stream handle of the network's device is used."""
+    import torch
+
+    from paper_2407_19097_b200 import _lib
+    from paper_2407_19097_b200.neural import UNet, init_params
+
+    cfg = _cfg(4, 16, 0)
+    net = UNet(cfg, init_params(cfg), device=cuda)
+    x = torch.rand((64, 96, 4), device=cuda)
+    with _lib.on_device(cuda.index):
+        y = net(x)
+    assert torch.isfinite(y).all()
