@@ -548,6 +548,11 @@ static int run_conv(nar_unet* n, Layer& l, const __nv_bfloat16* src_a, int ca_st
       if (!a.out) a.out = scratch;
     }
   }
+  static const int dbg = [] {
+    const char* e = getenv("NAR_TC_DEBUG");
+    return e ? atoi(e) : 0;
+  }();
+  a.debug = dbg;
   int rc = tc_launch_gated_conv(a, st);
   if (rc) return rc;
   if (pool_out && !fuse_pool) pool_kernel(a.out);

@@ -71,6 +71,9 @@ struct ConvArgs {
   // zero padded, so the fused head's FMAs take constant operands (cout <= 32)
   float head_wv[32 * 4];
   float head_bv[4];
+  // timing experiments only (NAR_TC_DEBUG, wrong results): bit 0 = epilogue
+  // skips the gate math and stores, bit 1 = no MMAs are issued
+  int debug;
 };
 
 constexpr int kProdWarps = 1;   // TMA issue (one lane)
@@ -421,7 +424,10 @@ __global__ void __maxnreg__(96)
         const int s = it % S;
         mbar_wait(&full[s], (uint32_t)(it / S) & 1u);
         tc_fence_after();
-        if (lane == 0) {
+        if (lane == 0 && (a.debug & 2)) {
+          umma_commit(&empty[s]);
+          if (q == nq - 1) umma_commit(&tfull[b]);
+        } else if (lane == 0) {
           const uint32_t sa = smem_u32(smem + s * STAGE);
           const uint32_t sb = sa + A_BYTES;
           if constexpr (SLIDE) {
@@ -494,6 +500,12 @@ __global__ void __maxnreg__(96)
       const int y0 = (tile / tiles_x) * R, x0 = (tile % tiles_x) * 128;
       mbar_wait(&tfull[b], ((uint32_t)(tl / NB)) & 1u);
       tc_fence_after();
+      if (a.debug & 1) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[b]);
+        continue;
+      }
       const int x = x0 + m;
       const bool xok = x < a.W;
       float logit[kHead ? RPW : 1][4];

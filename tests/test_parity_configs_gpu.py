@@ -52,7 +52,8 @@ def test_unet_c4_frame_vs_f32_oracle(cuda):
     x = _terrain_gbuffer(cuda)
     assert tuple(x.shape) == (1088, 1920, 4)
     cov = float((x[..., 3] > 0).float().mean())
-    assert cov > 0.5, f"terrain G-buffer covers only {cov:.2f} of the frame"
+    # the oblique C4 view: terrain fills the lower ~40 % of the frame, sky above
+    assert cov > 0.3, f"terrain G-buffer covers only {cov:.2f} of the frame"
     cfg = UNetConfig(input_channels=4)  # C4: random init, init_seed=0
     params = init_params(cfg)
     net = UNet(cfg, params, device=cuda)
