@@ -769,20 +769,23 @@ def main_ours(args):
         k_e2e = max(2, min(args.steps, 5))
 
         def timed_rasterize(pc):
+            a = time.perf_counter()
             rasterize(pc, cam, sel)  # warm (staging buffers, pinned output pool)
             torch.cuda.synchronize()
+            first = (time.perf_counter() - a) * 1e3
             a = time.perf_counter()
             for _ in range(k_e2e):
                 fi = rasterize(pc, cam, sel)  # returns after the D2H has landed
-            return (time.perf_counter() - a) / k_e2e * 1e3, fi
+            return (time.perf_counter() - a) / k_e2e * 1e3, fi, first
 
         # the stock drop-in caller: pageable numpy arrays in a plain PointCloud
-        pg_ms, fi = timed_rasterize(PointCloud(host_pos, [Stream("rgb", "u8", host_rgb)]))
+        # (page-locked in place by the first call, then DMA + zero-copy)
+        pg_ms, fi, pg_first = timed_rasterize(PointCloud(host_pos, [Stream("rgb", "u8", host_rgb)]))
         d2h = fi.data.nbytes + fi.coverage.nbytes + fi.index_plane.nbytes + fi.depth.nbytes
         del fi
         # PointCloud(..., pinned=True): points DMA'd, rgb gathered in place (zero-copy)
         pc_pin = PointCloud(host_pos, [Stream("rgb", "u8", host_rgb)], pinned=True)
-        pin_ms, fi = timed_rasterize(pc_pin)
+        pin_ms, fi, _ = timed_rasterize(pc_pin)
         gathered = int(fi.coverage.astype(bool).sum()) * 3
         e2e = {"value": cloud.count / (pin_ms * 1e-3) / 1e9, "unit": "Gpts/s",
                "h2d_bytes_per_step": int(host_pos.nbytes + gathered),
@@ -790,11 +793,13 @@ def main_ours(args):
                "d2h_bytes_per_step": int(d2h), "ms_per_step": pin_ms,
                "api": "paper_2407_19097_b200.msr.rasterize(PointCloud(..., pinned=True))",
                "pageable": {"value": cloud.count / (pg_ms * 1e-3) / 1e9, "unit": "Gpts/s",
-                            "ms_per_step": pg_ms,
-                            "h2d_bytes_per_step": int(host_pos.nbytes + host_rgb.nbytes),
+                            "ms_per_step": pg_ms, "first_call_ms": pg_first,
+                            "first_call_note": "includes cudaHostRegister of the caller's "
+                                               "arrays (kept while they live)",
+                            "h2d_bytes_per_step": int(host_pos.nbytes + gathered),
                             "d2h_bytes_per_step": int(d2h),
                             "api": "paper_2407_19097_b200.msr.rasterize(PointCloud(numpy arrays)) "
-                                   "-- the stock drop-in caller (staged H2D of points + rgb)"}}
+                                   "-- the stock drop-in caller"}}
         del host_pos, host_rgb, pc_pin, fi
 
     # ---- full NAR frame on the same cloud: render + resolve + U-Net ----------

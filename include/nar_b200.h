@@ -81,6 +81,14 @@ int nar_host_free(void* ptr);
  * device memory).  Kernels read through it over PCIe ("zero-copy"): the
  * resolve gathers only the winners' attributes instead of uploading streams. */
 int nar_host_mapped_pointer(const void* host, void** dev);
+/* Page-lock (and map) an existing pageable host range in place, so later
+ * copies from it are async DMA and kernels can read it zero-copy; undone by
+ * nar_host_unregister.  NAR_ERR_INVALID if (part of) the range is already
+ * registered or the pages cannot be locked.  The Python shim registers the
+ * numpy arrays of a host PointCloud on first use (msr.rasterize) and
+ * unregisters them when the arrays are released. */
+int nar_host_register(void* host, size_t bytes);
+int nar_host_unregister(void* host);
 
 /* ---- host-parity twin of the reference FFI --------------------------------------
  * Same arguments and semantics as `_native.zbuffer_accumulate` (_native.pyx:32):

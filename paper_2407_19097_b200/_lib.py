@@ -110,6 +110,8 @@ SIGNATURES = {
     "nar_launch_count": (C.c_uint64, []),
     "nar_splat_blend": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp]),
     "nar_host_mapped_pointer": (C.c_int, [_vp, C.POINTER(C.c_void_p)]),
+    "nar_host_register": (C.c_int, [_vp, C.c_size_t]),
+    "nar_host_unregister": (C.c_int, [_vp]),
     "nar_zbuffer_accumulate": (
         C.c_int,
         [_vp, _vp, _i64, _u64, _vp, _vp, _d, _d, _d, _d, _d, _i32, _i32],
@@ -252,6 +254,44 @@ class on_device:
         if self.index is not None and self.index != self.prev:
             torch.cuda.set_device(self.prev)
         return False
+
+
+# ---- in-place page locking of caller arrays (msr.rasterize's pageable path) ----
+REGISTER_MIN_BYTES = 64 << 20
+_registered: dict = {}  # data pointer -> (nbytes, weakref.finalize)
+_reg_lock = threading.Lock()
+
+
+def _unregister(ptr: int) -> None:
+    with _reg_lock:
+        if _registered.pop(ptr, None) is not None and _lib is not None:
+            _lib.nar_host_unregister(C.c_void_p(ptr))
+
+
+def ensure_registered(arr) -> bool:
+    """Page-lock a large pageable numpy array in place (cudaHostRegister, mapped)
+    so it behaves like pinned memory: async DMA and zero-copy kernel reads.  The
+    registration lives as long as the array object (a weakref finalizer undoes
+    it before numpy frees the buffer).  Returns False (array left pageable) for
+    small arrays, when NAR_HOST_REGISTER=0, or when the driver refuses."""
+    import weakref
+
+    if arr.nbytes < REGISTER_MIN_BYTES or os.environ.get("NAR_HOST_REGISTER", "1") == "0":
+        return False
+    ptr = int(arr.ctypes.data)
+    with _reg_lock:
+        if ptr in _registered:
+            return _registered[ptr][0] >= arr.nbytes
+        if load().nar_host_register(C.c_void_p(ptr), arr.nbytes) != NAR_OK:
+            return False
+        try:
+            fin = weakref.finalize(arr, _unregister, ptr)
+        except TypeError:  # no weakref support: undo, stay pageable
+            _lib.nar_host_unregister(C.c_void_p(ptr))
+            return False
+        fin.atexit = False
+        _registered[ptr] = (arr.nbytes, fin)
+    return True
 
 
 def mapped_pointer(host_ptr: int):

@@ -99,4 +99,25 @@ int nar_host_mapped_pointer(const void* host, void** dev) {
   return NAR_OK;
 }
 
+int nar_host_register(void* host, size_t bytes) {
+  if (!host || !bytes) return nar::set_error(NAR_ERR_INVALID, "NULL or empty range");
+  const cudaError_t e =
+      cudaHostRegister(host, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    std::string m = std::string("cudaHostRegister failed: ") + cudaGetErrorString(e);
+    return nar::set_error(NAR_ERR_INVALID, m.c_str());
+  }
+  return NAR_OK;
+}
+
+int nar_host_unregister(void* host) {
+  if (!host) return nar::set_error(NAR_ERR_INVALID, "NULL pointer");
+  if (cudaHostUnregister(host) != cudaSuccess) {
+    cudaGetLastError();
+    return nar::set_error(NAR_ERR_INVALID, "range was not registered");
+  }
+  return NAR_OK;
+}
+
 }  // extern "C"

@@ -103,16 +103,22 @@ __host__ __device__ constexpr int tc_b_bytes(int N) { return 9 * N * 32; }
 __host__ __device__ constexpr int tc_stage_bytes(int N, int NB) {
   return tc_r1024(tc_a_bytes(N, NB) + tc_b_bytes(N));
 }
-constexpr int kTcParamFloats = 3 * 144 + 128 * 4 + 4;  // bias_f, bias_f*log2e, bias_g/2, head_w, head_b
+constexpr int kTcParamFloats = 128 * 4 + 4;  // head_w, head_b
 // Narrow layers (N <= 48) use "sliding" MMAs: one MMA per (halo row, kx) with
 // the three ky weight blocks stacked along N (N' = 3N) accumulates into three
 // consecutive output rows at once -- (R+2)*3 MMAs per chunk instead of 9*R,
 // which matters because an M=128, K=16 MMA costs ~55 cycles for any N <= 64.
-// Accumulators are zeroed first by one MMA with zero operands (kTcZeroBytes).
 __host__ __device__ constexpr bool tc_slide(int N) { return N <= 64; }
-constexpr int kTcZeroBytes = 256 * 32;  // B: 256 rows x K16 bf16 (A uses its first 4 KB)
+// Bias in the accumulator: every tile starts with one MMA (two for 512-column
+// tiles) of a "ones" A operand (k = 0, 1 -> 1.0) against a bias B operand
+// (row n: k = 0 -> hi, k = 1 -> lo bf16 halves of the packed bias of column
+// n % N), so the accumulators begin at the bias (to ~2^-16 relative) and the
+// epilogue reads conv + bias directly.  No-swizzle K-major, 8-row core
+// matrices: A = 128 rows (LBO 2048), B = 256 rows (LBO 4096).
+constexpr int kTcOnesBytes = 128 * 32;
+constexpr int kTcBiasBytes = 256 * 32;
 __host__ __device__ constexpr int tc_fixed_smem(int N) {
-  return 512 + kTcParamFloats * 4 + (tc_slide(N) ? kTcZeroBytes : 0);
+  return 512 + kTcOnesBytes + kTcBiasBytes + kTcParamFloats * 4;
 }
 // stages: as many (<= NAR_TC_MAX_STAGES) as fit the 227 KB opt-in shared memory
 #ifndef NAR_TC_MAX_STAGES
@@ -135,7 +141,10 @@ __host__ __device__ constexpr int tc_coutp(int cout) {
 }
 
 // Host: pack HWIO f32 weights into bf16 [chunk q][tap][k8][n][8] where
-// n < Coutp indexes f outputs and n >= Coutp g outputs (zero padded).
+// n < Coutp indexes f outputs and n >= Coutp g outputs (zero padded).  All
+// weights (and, in the kernel, biases) are scaled by 1/2 -- exact in bf16 --
+// so the accumulators hold f/2 and g/2, the operands of the epilogue's
+// elu(f)/2 and tanh(g/2) (see gate_h).
 // Sliding layers (tc_slide(N)): [chunk q][kx][k8][n' = (2 - ky) * N + n][8].
 inline void tc_pack_weights(const std::vector<float>& wf, const std::vector<float>& wg, int ca,
                             int cb, int cout, std::vector<uint16_t>& packed) {
@@ -162,7 +171,7 @@ inline void tc_pack_weights(const std::vector<float>& wf, const std::vector<floa
             const bool is_g = n >= coutp;
             const int j = is_g ? n - coutp : n;
             if (j >= cout) continue;
-            const float v = (is_g ? wg : wf)[((size_t)tap * cin + ci) * cout + j];
+            const float v = 0.5f * (is_g ? wg : wf)[((size_t)tap * cin + ci) * cout + j];
             if (slide) {
               const int ky = tap / 3, kx = tap % 3;
               const size_t np = (size_t)(2 - ky) * N + n;
@@ -287,15 +296,15 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
-// elu(f + bf) * sigmoid(g + bg) on raw accumulators, with bfl = bf*log2(e) and
-// bgh = bg/2 precomputed: elu via ex2 (autodiff.py:186-194), sigmoid via
-// tanh (autodiff.py:197-203) -- 2 MUFU + 7 FMA-pipe ops per output.
-__device__ __forceinline__ float gate_b(float f, float g, float bf, float bfl, float bgh) {
-  const float fb = f + bf;
-  const float ex = ex2_approx(fmaf(f, 1.44269504088896341f, bfl));
-  const float e = fb > 0.0f ? fb : ex - 1.0f;
-  const float sg = fmaf(0.5f, tanh_approx(fmaf(0.5f, g, bgh)), 0.5f);
-  return e * sg;
+// elu(f) * sigmoid(g) (autodiff.py:186-203) from the accumulators fh = f/2,
+// gh = g/2 (bias included): with e = elu(f)/2 (fh, or (e^f - 1)/2 via ex2) and
+// sigmoid(g) = (1 + tanh(g/2))/2, the gate is e + e*tanh(gh) -- 2 MUFU + 4
+// FMA-pipe ops per output.
+__device__ __forceinline__ float gate_h(float fh, float gh) {
+  const float ex = ex2_approx(fh * 2.88539008177792681f);  // 2^(2 fh log2 e) = e^f
+  const float e = fh > 0.0f ? fh : fmaf(0.5f, ex, -0.5f);
+  const float t = tanh_approx(gh);
+  return fmaf(e, t, e);
 }
 
 // ---------------------------------------------------------------------------
@@ -326,13 +335,11 @@ __global__ void __maxnreg__(96)
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
   uint32_t* tbase_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  float* sbias_f = reinterpret_cast<float*>(fixed + 512);
-  float* sbias_fl = sbias_f + 144;
-  float* sbias_gh = sbias_fl + 144;
-  float* shead_w = sbias_gh + 144;
+  uint8_t* sones = fixed + 512;                 // bias MMA operands (kTcOnesBytes)
+  uint8_t* sbiasm = sones + kTcOnesBytes;       // (kTcBiasBytes)
+  float* shead_w = reinterpret_cast<float*>(sbiasm + kTcBiasBytes);
   float* shead_b = shead_w + 512;
   constexpr bool SLIDE = tc_slide(N);
-  uint8_t* szero = reinterpret_cast<uint8_t*>(sbias_f + kTcParamFloats);  // SLIDE only
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles_x = (a.W + 127) / 128;
@@ -353,19 +360,23 @@ __global__ void __maxnreg__(96)
     prefetch_tmap(&tma_a);
     if (nqb) prefetch_tmap(&tma_b);
   }
-  for (int i = threadIdx.x; i < 144; i += kTcThreads) {
-    // zero beyond cout: padded accumulators are 0, so gate(0, 0 | 0) = elu(0) * 0.5 = 0
-    const float bf = i < a.cout ? a.bias_f[i] : 0.0f;
-    const float bg = i < a.cout ? a.bias_g[i] : 0.0f;
-    sbias_f[i] = bf;
-    sbias_fl[i] = bf * 1.44269504088896341f;
-    sbias_gh[i] = 0.5f * bg;
+  // bias MMA operands; columns beyond cout get bias 0, so their gate is
+  // elu(0) * sigmoid(0) = 0 (padded output channels stay exact zeros)
+  for (int i = threadIdx.x; i < (kTcOnesBytes + kTcBiasBytes) / 16; i += kTcThreads) {
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (i < 128) {
+      v.x = 0x3F803F80u;  // A row i, k = 0, 1: 1.0
+    } else if (i >= kTcOnesBytes / 16 && i < kTcOnesBytes / 16 + 256) {
+      const int n = (i - kTcOnesBytes / 16) % N;  // B row -> accumulator column
+      const int j = n < COUTP ? n : n - COUTP;
+      const float b = j < a.cout ? 0.5f * (n < COUTP ? a.bias_f[j] : a.bias_g[j]) : 0.0f;
+      const __nv_bfloat16 hi = __float2bfloat16_rn(b);
+      const __nv_bfloat16 lo = __float2bfloat16_rn(b - __bfloat162float(hi));
+      v.x = (uint32_t)__bfloat16_as_ushort(hi) | ((uint32_t)__bfloat16_as_ushort(lo) << 16);
+    }
+    reinterpret_cast<uint4*>(sones)[i] = v;
   }
-  if (SLIDE) {
-    for (int i = threadIdx.x; i < kTcZeroBytes / 16; i += kTcThreads)
-      reinterpret_cast<uint4*>(szero)[i] = make_uint4(0u, 0u, 0u, 0u);
-    fence_proxy_async_smem();  // generic-proxy zeros, read by the tensor core
-  }
+  fence_proxy_async_smem();  // generic-proxy writes, read by the tensor core
   if (a.head_out)
     for (int i = threadIdx.x; i < a.cout * a.head_n; i += kTcThreads) shead_w[i] = a.head_w[i];
   if (a.head_out && threadIdx.x < a.head_n) shead_b[threadIdx.x] = a.head_b[threadIdx.x];
@@ -430,12 +441,14 @@ __global__ void __maxnreg__(96)
         } else if (lane == 0) {
           const uint32_t sa = smem_u32(smem + s * STAGE);
           const uint32_t sb = sa + A_BYTES;
+          if (q == 0) {  // this tile's R*N accumulator columns start at the bias
+            const uint64_t ad = umma_desc(smem_u32(sones), 2048, 128);
+            const uint64_t bd = umma_desc(smem_u32(sbiasm), 4096, 128);
+#pragma unroll
+            for (int c = 0; c < R * N; c += 256)
+              umma_bf16(dcol + c, ad, bd, umma_idesc_bf16(128, R * N - c < 256 ? R * N - c : 256), 0u);
+          }
           if constexpr (SLIDE) {
-            if (q == 0) {  // zero this tile's R*N accumulator columns
-              const uint32_t z = smem_u32(szero);
-              umma_bf16(dcol, umma_desc(z, 2048, 128), umma_desc(z, R * N * 16, 128),
-                        umma_idesc_bf16(128, R * N), 0u);
-            }
 #pragma unroll 1
             for (int kx = 0; kx < 3; ++kx) {
               const uint32_t bk = sb + kx * (3 * N * 32);  // [k8][3N][8]: LBO = 3N*16
@@ -460,7 +473,7 @@ __global__ void __maxnreg__(96)
               for (int r = 0; r < R; ++r) {
                 const uint64_t adesc =
                     umma_desc_sw32(sa + ((r + ky + par) >> sh) * kHaloRowBytes + kx * 32);
-                umma_bf16(dcol + r * N, adesc, bdesc, IDESC, (q > 0 || tap > 0) ? 1u : 0u);
+                umma_bf16(dcol + r * N, adesc, bdesc, IDESC, 1u);
               }
             }
           }
@@ -524,13 +537,6 @@ __global__ void __maxnreg__(96)
         if (c8 >= nc8) break;
         const int c0 = c8 * 8;
         const bool have = c0 < COUTP;
-        float bfv[8], bflv[8], bghv[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          bfv[e] = sbias_f[c0 + e];
-          bflv[e] = sbias_fl[c0 + e];
-          bghv[e] = sbias_gh[c0 + e];
-        }
         // rows of this warp: r = grp*rstep + i*4*rstep; unrolled so `slot`
         // (the logit row) is a compile-time index (registers, not local memory)
 #pragma unroll
@@ -557,7 +563,7 @@ __global__ void __maxnreg__(96)
           for (int h = 0; h < 2; ++h) {
             if (h == 1 && !do_pool) break;
 #pragma unroll
-            for (int e = 0; e < 8; ++e) o[h][e] = gate_b(f[h][e], g[h][e], bfv[e], bflv[e], bghv[e]);
+            for (int e = 0; e < 8; ++e) o[h][e] = gate_h(f[h][e], g[h][e]);
             const int y = y0 + r + h;
             const bool ok = y < a.H && xok;
             if (a.out != nullptr && ok) {

@@ -517,6 +517,14 @@ def _rasterize(pc: PointCloud, cam: CameraPose, sel: StreamSelection, r: "Render
     main = torch.cuda.current_stream(dev)
     kc = cam.kernel_camera()
     names = sel.needed_streams()
+    # Large pageable arrays (a stock caller's numpy PointCloud) are page-locked
+    # in place on first use and stay registered while the arrays live, so the
+    # points go up by async DMA and the attributes are read zero-copy, exactly
+    # as for PointCloud(..., pinned=True) (NAR_HOST_REGISTER=0 disables this).
+    if not getattr(pc, "pinned", False):
+        _lib.ensure_registered(pc.positions)
+        for n in names:
+            _lib.ensure_registered(pc.stream(n).data)
     # Attribute streams in mapped pinned memory are not uploaded: the resolve
     # gathers just the winners' attributes through their device address
     # (zero-copy over PCIe).  Pageable streams go up on a side stream while the
