@@ -72,7 +72,8 @@ struct ConvArgs {
   float head_wv[32 * 4];
   float head_bv[4];
   // timing experiments only (NAR_TC_DEBUG, wrong results): bit 0 = epilogue
-  // skips the gate math and stores, bit 1 = no MMAs are issued
+  // skips the gate math and stores, bit 1 = no MMAs are issued, bit 2 = no
+  // operand loads
   int debug;
 };
 
@@ -307,6 +308,7 @@ __device__ __forceinline__ float gate_h(float fh, float gh) {
   return fmaf(e, t, e);
 }
 
+
 // ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
@@ -413,6 +415,10 @@ __global__ void __maxnreg__(96)
         const CUtensorMap* map = in_a ? &tma_a : &tma_b;
         const int yr = up ? (y0 - 1) >> 1 : y0 - 1;  // arithmetic shift: row -1 stays OOB
         mbar_wait(&empty[s], ((uint32_t)(it / S) & 1u) ^ 1u);
+        if (a.debug & 4) {  // timing experiment: no loads
+          mbar_arrive(&full[s]);
+          continue;
+        }
         mbar_expect_tx(&full[s], (up ? UP_TX : A_TX) + B_BYTES);
         tma_load_3d(stA, map, cbase, x0 - 1, yr, &full[s]);
         bulk_g2s(stA + A_BYTES, a.wtc + (size_t)q * (B_BYTES / 2), B_BYTES, &full[s]);
