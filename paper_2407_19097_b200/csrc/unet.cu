@@ -180,6 +180,8 @@ __global__ void __launch_bounds__(256)
                              const float* __restrict__ hw, const float* __restrict__ hb,
                              int use_head, int levels, PyrOut out) {
   __shared__ float tile[16 * 16 * 4];  // level-1 values of the CTA (16 x 16 x 4)
+  // let the first conv (a programmatic dependent) get scheduled early
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int t = threadIdx.x;
   const int qy = t >> 4, qx = t & 15;  // quad = level-1 pixel of the 32 x 32 tile
   const int y0 = blockIdx.y * 32 + 2 * qy, x0 = blockIdx.x * 32 + 2 * qx;

@@ -36,6 +36,7 @@
 #include <cudaTypedefs.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <vector>
@@ -330,6 +331,10 @@ __global__ void __maxnreg__(96)
   static_assert(NB * R * N <= 512, "TMEM budget");
   static_assert(S >= 2, "pipeline depth");
 
+  // Programmatic dependent launch: the next layer's CTAs may be scheduled as soon
+  // as every CTA of this one is running (they take an SM once ours leaves it, run
+  // their prologue and wait in griddepcontrol.wait below for this grid to finish).
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* fixed = smem + S * STAGE;
   uint64_t* full = reinterpret_cast<uint64_t*>(fixed);
@@ -392,6 +397,10 @@ __global__ void __maxnreg__(96)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tbase_slot;
+  // Everything above touches only this launch's constant parameters; the
+  // activations are the previous layer's output (and our output may still be
+  // read by an earlier layer): wait for the prerequisite grid to complete.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp < kProdWarps) {
     // ------------------------------ producer ------------------------------
@@ -751,7 +760,24 @@ static int tc_launch_nhb(const ConvArgs& a, cudaStream_t st) {
   const int tiles = ((a.W + 127) / 128) * ((a.H + R - 1) / R);
   const int grid = tiles < sms ? tiles : sms;
   nar::count_launch();
-  gated_conv_tc<N, kHead, NB><<<grid, kTcThreads, tc_smem(N, NB), st>>>(a, ma, mb);
+  // launched as a programmatic dependent of the previous kernel on the stream
+  // (NAR_TC_PDL=0 turns it off for timing comparisons)
+  static const bool pdl = [] {
+    const char* e = getenv("NAR_TC_PDL");
+    return !(e && e[0] == '0');
+  }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kTcThreads);
+  cfg.dynamicSmemBytes = tc_smem(N, NB);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, gated_conv_tc<N, kHead, NB>, a, ma, mb);
+  if (e != cudaSuccess) return set_error(NAR_ERR_CUDA, cudaGetErrorString(e));
   return check_launch("gated_conv_tc");
 }
 
