@@ -555,6 +555,12 @@ static int run_conv(nar_unet* n, Layer& l, const __nv_bfloat16* src_a, int ca_st
     return e ? atoi(e) : 0;
   }();
   a.debug = dbg;
+  static const int sblk = [] {
+    const char* e = getenv("NAR_TC_SLIDE_BLOCKS");
+    const int v = e ? atoi(e) : 2;
+    return v < 1 ? 1 : (v > 4 ? 4 : v);
+  }();
+  a.slide_blocks = sblk;
   int rc = tc_launch_gated_conv(a, st);
   if (rc) return rc;
   if (pool_out && !fuse_pool) pool_kernel(a.out);

@@ -28,7 +28,10 @@
 //              (model.py:189-191) in f32 instead of the bf16 activation.
 // Accumulators are double buffered in TMEM (2 x R x N <= 512 columns) so the
 // epilogue of tile i overlaps the MMAs of tile i+1 -- except for wide layers,
-// which take a single buffer of twice the rows (see tc_bufs_for).
+// which take a single buffer of twice the rows (see tc_bufs_for).  Within a
+// tile the MMAs run row by row in the last channel chunk and each epilogue row
+// slot is signalled as soon as its rows are complete (tc_epi_*), so the
+// epilogue of the first rows also overlaps the MMAs of the last ones.
 #pragma once
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -39,6 +42,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -76,6 +80,9 @@ struct ConvArgs {
   // skips the gate math and stores, bit 1 = no MMAs are issued, bit 2 = no
   // operand loads
   int debug;
+  // sliding layers: halo-row blocks of the last chunk, each followed by the
+  // signal of the epilogue row slots it completes (1 = signal at the tile end)
+  int slide_blocks;
 };
 
 constexpr int kProdWarps = 1;   // TMA issue (one lane)
@@ -119,6 +126,19 @@ __host__ __device__ constexpr bool tc_slide(int N) { return N <= 64; }
 // matrices: A = 128 rows (LBO 2048), B = 256 rows (LBO 4096).
 constexpr int kTcOnesBytes = 128 * 32;
 constexpr int kTcBiasBytes = 256 * 32;
+// Epilogue row slots: the kEpiGroups warp groups split a tile's rows into
+// contiguous slots of whole units (a unit = one row, or a row pair when the
+// output is 2x2-pooled); with fewer units than groups the groups also split
+// the channel chunks.  Slot s ends at row tc_epi_last_row(s, ...).
+__host__ __device__ constexpr int tc_epi_rgroups(int units) {
+  return units < kEpiGroups ? (units > 0 ? units : 1) : kEpiGroups;
+}
+__host__ __device__ constexpr int tc_epi_first_unit(int s, int units, int rg) {
+  return s * units / rg;
+}
+__host__ __device__ constexpr int tc_epi_last_row(int s, int units, int rg, int rstep) {
+  return tc_epi_first_unit(s + 1, units, rg) * rstep - 1;
+}
 __host__ __device__ constexpr int tc_fixed_smem(int N) {
   return 512 + kTcOnesBytes + kTcBiasBytes + kTcParamFloats * 4;
 }
@@ -339,8 +359,8 @@ __global__ void __maxnreg__(96)
   uint8_t* fixed = smem + S * STAGE;
   uint64_t* full = reinterpret_cast<uint64_t*>(fixed);
   uint64_t* empty = full + S;
-  uint64_t* tfull = empty + S;
-  uint64_t* tempty = tfull + 2;
+  uint64_t* tfull = empty + S;       // [buffer][row slot]
+  uint64_t* tempty = tfull + 2 * kEpiGroups;
   uint32_t* tbase_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   uint8_t* sones = fixed + 512;                 // bias MMA operands (kTcOnesBytes)
   uint8_t* sbiasm = sones + kTcOnesBytes;       // (kTcBiasBytes)
@@ -360,7 +380,7 @@ __global__ void __maxnreg__(96)
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&tfull[b], 1);
+      for (int g = 0; g < kEpiGroups; ++g) mbar_init(&tfull[b * kEpiGroups + g], 1);
       mbar_init(&tempty[b], 4 * kEpiGroups);
     }
     fence_mbar_init();
@@ -435,9 +455,13 @@ __global__ void __maxnreg__(96)
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------ MMA issuer -----------------------------
+    // epilogue row slots (see tc_epi_rgroups): signalled one by one in the last chunk
+    const int rstep = (!kHead && a.pool_out != nullptr) ? 2 : 1;
+    const int units = R / rstep, rg = tc_epi_rgroups(units);
     int it = 0, tl = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tl) {
       const int b = tl % NB;
+      uint64_t* tf = tfull + b * kEpiGroups;
       mbar_wait(&tempty[b], (((uint32_t)(tl / NB)) & 1u) ^ 1u);
       tc_fence_after();
       const uint32_t dcol = tbase + (uint32_t)(b * R * N);
@@ -448,11 +472,13 @@ __global__ void __maxnreg__(96)
         const bool up = a.a_up2 && q < nqa;
         const int sh = up ? 1 : 0, par = up ? ((y0 - 1) & 1) : 0;
         const int s = it % S;
+        const bool last = q == nq - 1;
         mbar_wait(&full[s], (uint32_t)(it / S) & 1u);
         tc_fence_after();
         if (lane == 0 && (a.debug & 2)) {
           umma_commit(&empty[s]);
-          if (q == nq - 1) umma_commit(&tfull[b]);
+          if (last)
+            for (int g = 0; g < rg; ++g) umma_commit(&tf[g]);
         } else if (lane == 0) {
           const uint32_t sa = smem_u32(smem + s * STAGE);
           const uint32_t sb = sa + A_BYTES;
@@ -463,37 +489,57 @@ __global__ void __maxnreg__(96)
             for (int c = 0; c < R * N; c += 256)
               umma_bf16(dcol + c, ad, bd, umma_idesc_bf16(128, R * N - c < 256 ? R * N - c : 256), 0u);
           }
+          int slot = 0;  // next row slot to signal (last chunk)
           if constexpr (SLIDE) {
+            // halo row h feeds output rows h-2..h (ky = 2, 1, 0): after h, rows <= h-2 are
+            // complete.  kx outer, h inner and unrolled (compile-time descriptors: the
+            // single issuing thread must keep up with ~57-cycle MMAs).  The last chunk
+            // (a.slide_blocks > 1) runs its halo rows in two blocks and signals the row
+            // slots the first block completes before starting the second.
+            auto rows = [&](auto h0c, auto h1c) {
+              constexpr int H0 = decltype(h0c)::value, H1 = decltype(h1c)::value;
 #pragma unroll 1
-            for (int kx = 0; kx < 3; ++kx) {
-              const uint32_t bk = sb + kx * (3 * N * 32);  // [k8][3N][8]: LBO = 3N*16
+              for (int kx = 0; kx < 3; ++kx) {
+                const uint32_t bk = sb + kx * (3 * N * 32);  // [k8][3N][8]: LBO = 3N*16
 #pragma unroll
-              for (int h = 0; h < R + 2; ++h) {
-                // output rows r = h - ky for ky in [kymin, kymax]; blocks ordered ky = 2, 1, 0
-                const int kymax = h < 2 ? h : 2;
-                const int kymin = h - (R - 1) > 0 ? h - (R - 1) : 0;
-                const int nb = kymax - kymin + 1;
-                const uint64_t bdesc = umma_desc(bk + (2 - kymax) * N * 16, 3 * N * 16, 128);
-                const uint64_t adesc =
-                    umma_desc_sw32(sa + ((h + par) >> sh) * kHaloRowBytes + kx * 32);
-                umma_bf16(dcol + (h - kymax) * N, adesc, bdesc, umma_idesc_bf16(128, nb * N), 1u);
+                for (int h = H0; h < H1; ++h) {
+                  const int kymax = h < 2 ? h : 2;
+                  const int kymin = h - (R - 1) > 0 ? h - (R - 1) : 0;
+                  const int nb = kymax - kymin + 1;
+                  const uint64_t bdesc = umma_desc(bk + (2 - kymax) * N * 16, 3 * N * 16, 128);
+                  const uint64_t adesc =
+                      umma_desc_sw32(sa + ((h + par) >> sh) * kHaloRowBytes + kx * 32);
+                  umma_bf16(dcol + (h - kymax) * N, adesc, bdesc, umma_idesc_bf16(128, nb * N), 1u);
+                }
               }
+              if (last)
+                while (slot < rg && H1 - 1 >= tc_epi_last_row(slot, units, rg, rstep) + 2)
+                  umma_commit(&tf[slot++]);
+            };
+            constexpr int HM = R / 2 + 2;  // rows < R/2 are complete after halo row HM-1
+            if (last && a.slide_blocks > 1 && R >= 2) {
+              rows(std::integral_constant<int, 0>{}, std::integral_constant<int, HM>{});
+              rows(std::integral_constant<int, HM>{}, std::integral_constant<int, R + 2>{});
+            } else {
+              rows(std::integral_constant<int, 0>{}, std::integral_constant<int, R + 2>{});
             }
           } else {
 #pragma unroll 1
-            for (int tap = 0; tap < 9; ++tap) {
-              const int ky = tap / 3, kx = tap % 3;
-              const uint64_t bdesc = umma_desc(sb + tap * (N * 32), N * 16, 128);
+            for (int r = 0; r < R; ++r) {
 #pragma unroll
-              for (int r = 0; r < R; ++r) {
+              for (int tap = 0; tap < 9; ++tap) {
+                const int ky = tap / 3, kx = tap % 3;
+                const uint64_t bdesc = umma_desc(sb + tap * (N * 32), N * 16, 128);
                 const uint64_t adesc =
                     umma_desc_sw32(sa + ((r + ky + par) >> sh) * kHaloRowBytes + kx * 32);
                 umma_bf16(dcol + r * N, adesc, bdesc, IDESC, 1u);
               }
+              if (last)
+                while (slot < rg && r >= tc_epi_last_row(slot, units, rg, rstep))
+                  umma_commit(&tf[slot++]);
             }
           }
           umma_commit(&empty[s]);
-          if (q == nq - 1) umma_commit(&tfull[b]);
         }
         __syncwarp();
       }
@@ -515,18 +561,19 @@ __global__ void __maxnreg__(96)
     // With fewer row slots than groups (small R, or pooled row pairs) the
     // groups also split the channel chunks, so all 16 warps stay busy; the
     // head layer keeps whole channel ranges per warp (its logits sum them).
-    const int rgroups = kHead ? kEpiGroups
-                              : (R / rstep < kEpiGroups ? (R / rstep > 0 ? R / rstep : 1)
-                                                        : kEpiGroups);
+    const int units = R / rstep, rgroups = tc_epi_rgroups(units);
     const int cgroups = kEpiGroups / rgroups;
     const int rslot = grp % rgroups, cslot = grp / rgroups;
+    // this warp's rows: units [u0, u1) of the tile (contiguous, see tc_epi_rgroups)
+    const int u0 = tc_epi_first_unit(rslot, units, rgroups);
+    const int u1 = tc_epi_first_unit(rslot + 1, units, rgroups);
     const int nc8 = a.cout_stride / 8;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     int tl = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tl) {
       const int b = tl % NB;
       const int y0 = (tile / tiles_x) * R, x0 = (tile % tiles_x) * 128;
-      mbar_wait(&tfull[b], ((uint32_t)(tl / NB)) & 1u);
+      mbar_wait(&tfull[b * kEpiGroups + rslot], ((uint32_t)(tl / NB)) & 1u);
       tc_fence_after();
       if (a.debug & 1) {
         tc_fence_before();
@@ -556,9 +603,8 @@ __global__ void __maxnreg__(96)
         // (the logit row) is a compile-time index (registers, not local memory)
 #pragma unroll
         for (int i = 0; i < RPW; ++i) {
-          const int r = rslot * rstep + i * rgroups * rstep;
-          const int slot = i * rstep;
-          if (r >= R || slot >= RPW) break;
+          if (u0 + i >= u1) break;
+          const int r = (u0 + i) * rstep;
           float o[2][8];
           float f[2][8], g[2][8];
 #pragma unroll
@@ -634,9 +680,8 @@ __global__ void __maxnreg__(96)
       if (do_head) {
 #pragma unroll
         for (int i = 0; i < RPW; ++i) {
-          const int r = rslot * rstep + i * rgroups * rstep;
-          const int slot = i * rstep;
-          if (r >= R || slot >= RPW) break;
+          if (u0 + i >= u1) break;
+          const int r = (u0 + i) * rstep;
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             if (h == 1 && !do_pool) break;

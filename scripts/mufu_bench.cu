@@ -27,6 +27,13 @@ __global__ void k(float* out, int iters, long long* cyc) {
       if (OP == 3) asm volatile("tanh.approx.f16x2 %0, %0;" : "+r"(h[i]));
       if (OP == 4) asm volatile("tanh.approx.bf16x2 %0, %0;" : "+r"(h[i]));
       if (OP == 5) asm volatile("rcp.approx.ftz.f32 %0, %0;" : "+f"(x[i]));
+      if (OP == 6) asm volatile("cvt.rn.bf16x2.f32 %0, %1, %0;" : "+r"(h[i]) : "f"(x[i]));
+      if (OP == 7) asm volatile("cvt.rn.f16x2.f32 %0, %1, %0;" : "+r"(h[i]) : "f"(x[i]));
+      if (OP == 8) {  // MUFU and the bf16 pack interleaved: one pipe or two?
+        asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(x[i]));
+        asm volatile("cvt.rn.bf16x2.f32 %0, %1, %0;" : "+r"(h[i]) : "f"(x[i ^ 1]));
+      }
+      if (OP == 9) asm volatile("fma.rn.f32 %0, %0, %0, %0;" : "+f"(x[i]));
     }
   }
   __syncthreads();
@@ -45,17 +52,19 @@ int main() {
   long long* cyc;
   cudaMalloc(&out, sms * 512 * 4);
   cudaMalloc(&cyc, sms * 8);
-  const char* names[] = {"ex2.f32", "tanh.f32", "ex2.f16x2", "tanh.f16x2", "tanh.bf16x2", "rcp.f32"};
+  const char* names[] = {"ex2.f32", "tanh.f32", "ex2.f16x2", "tanh.f16x2", "tanh.bf16x2", "rcp.f32",
+                         "cvt.bf16x2", "cvt.f16x2", "ex2+cvt.bf16x2", "ffma"};
   const int iters = 4096;
-  for (int op = 0; op < 6; ++op) {
-    auto f = op == 0 ? k<0> : op == 1 ? k<1> : op == 2 ? k<2> : op == 3 ? k<3> : op == 4 ? k<4> : k<5>;
+  for (int op = 0; op < 10; ++op) {
+    void (*ks[])(float*, int, long long*) = {k<0>, k<1>, k<2>, k<3>, k<4>, k<5>, k<6>, k<7>, k<8>, k<9>};
+    auto f = ks[op];
     f<<<sms, 512>>>(out, iters, cyc);
     f<<<sms, 512>>>(out, iters, cyc);
     cudaDeviceSynchronize();
     long long c;
     cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
     const double ops = 512.0 * iters * 8;  // instructions' lanes per SM
-    const double elems = ops * (op >= 2 && op <= 4 ? 2 : 1);
+    const double elems = ops * (op >= 2 && op <= 4 ? 2 : op == 8 ? 2 : 1);
     printf("%-12s %6.2f lane-ops/clk/SM  %6.2f elements/clk/SM  (%lld cycles)\n", names[op], ops / c,
            elems / c, c);
   }
