@@ -175,55 +175,65 @@ __device__ __forceinline__ uint4 pack8_bf16(const float* v4, int cin) {
   return pk;
 }
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(128)
     head_pyramid_quad_kernel(const float* __restrict__ x, int H, int W, int cin, int cp,
                              const float* __restrict__ hw, const float* __restrict__ hb,
                              int use_head, int levels, PyrOut out) {
   __shared__ float tile[16 * 16 * 4];  // level-1 values of the CTA (16 x 16 x 4)
   // let the first conv (a programmatic dependent) get scheduled early
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // 128 threads, two 2x2 quads each (quad rows qy and qy + 8 of the 32 x 32 tile):
+  // all eight float4 loads are issued before any is used
   const int t = threadIdx.x;
-  const int qy = t >> 4, qx = t & 15;  // quad = level-1 pixel of the 32 x 32 tile
-  const int y0 = blockIdx.y * 32 + 2 * qy, x0 = blockIdx.x * 32 + 2 * qx;
+  const int qx = t & 15, qy0 = t >> 4;
   float wgt[16], bias[4];
 #pragma unroll
   for (int i = 0; i < 16; ++i) wgt[i] = (use_head && i / 4 < cin && i % 4 < cin) ? __ldg(hw + (i / 4) * cin + (i % 4)) : 0.f;
 #pragma unroll
   for (int j = 0; j < 4; ++j) bias[j] = (use_head && j < cin) ? __ldg(hb + j) : 0.f;
-  float4 in[4];
+  float4 in[2][4];
 #pragma unroll
-  for (int d = 0; d < 4; ++d)
-    in[d] = __ldg(reinterpret_cast<const float4*>(x + ((size_t)(y0 + (d >> 1)) * W + x0 + (d & 1)) * 4));
-  float hq[4][4];  // head outputs of the quad: TL, TR, BL, BR
+  for (int u = 0; u < 2; ++u) {
+    const int y0 = blockIdx.y * 32 + 2 * (qy0 + 8 * u), x0 = blockIdx.x * 32 + 2 * qx;
 #pragma unroll
-  for (int d = 0; d < 4; ++d) {
-    const float v[4] = {in[d].x, in[d].y, in[d].z, in[d].w};
+    for (int d = 0; d < 4; ++d)
+      in[u][d] = __ldg(reinterpret_cast<const float4*>(x + ((size_t)(y0 + (d >> 1)) * W + x0 + (d & 1)) * 4));
+  }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float acc = v[j];
-      if (use_head) {
-        acc = bias[j];
+  for (int u = 0; u < 2; ++u) {
+    const int qy = qy0 + 8 * u;
+    const int y0 = blockIdx.y * 32 + 2 * qy, x0 = blockIdx.x * 32 + 2 * qx;
+    float hq[4][4];  // head outputs of the quad: TL, TR, BL, BR
 #pragma unroll
-        for (int c = 0; c < 4; ++c) acc = fmaf(v[c], wgt[c * 4 + j], acc);
+    for (int d = 0; d < 4; ++d) {
+      const float v[4] = {in[u][d].x, in[u][d].y, in[u][d].z, in[u][d].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float acc = v[j];
+        if (use_head) {
+          acc = bias[j];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc = fmaf(v[c], wgt[c * 4 + j], acc);
+        }
+        hq[d][j] = j < cin ? acc : 0.f;
       }
-      hq[d][j] = j < cin ? acc : 0.f;
+      __nv_bfloat16* o = out.lvl[0] + ((size_t)(y0 + (d >> 1)) * W + x0 + (d & 1)) * cp;
+      *reinterpret_cast<uint4*>(o) = pack8_bf16(hq[d], cin);
+      if (cp > 8) *reinterpret_cast<uint4*>(o + 8) = make_uint4(0u, 0u, 0u, 0u);
     }
-    __nv_bfloat16* o = out.lvl[0] + ((size_t)(y0 + (d >> 1)) * W + x0 + (d & 1)) * cp;
-    *reinterpret_cast<uint4*>(o) = pack8_bf16(hq[d], cin);
-    if (cp > 8) *reinterpret_cast<uint4*>(o + 8) = make_uint4(0u, 0u, 0u, 0u);
-  }
-  float sum[4];  // the reference's 2x2 mean: ((TL + TR) + (BL + BR)) * 0.25
+    float sum[4];  // the reference's 2x2 mean: ((TL + TR) + (BL + BR)) * 0.25
 #pragma unroll
-  for (int j = 0; j < 4; ++j) sum[j] = ((hq[0][j] + hq[1][j]) + (hq[2][j] + hq[3][j])) * 0.25f;
-  // level 1 from registers
-  if (levels > 1) {
-    const int W1 = W >> 1;
-    __nv_bfloat16* o = out.lvl[1] + ((size_t)(blockIdx.y * 16 + qy) * W1 + blockIdx.x * 16 + qx) * cp;
-    *reinterpret_cast<uint4*>(o) = pack8_bf16(sum, cin);
-    if (cp > 8) *reinterpret_cast<uint4*>(o + 8) = make_uint4(0u, 0u, 0u, 0u);
-  }
+    for (int j = 0; j < 4; ++j) sum[j] = ((hq[0][j] + hq[1][j]) + (hq[2][j] + hq[3][j])) * 0.25f;
+    // level 1 from registers
+    if (levels > 1) {
+      const int W1 = W >> 1;
+      __nv_bfloat16* o = out.lvl[1] + ((size_t)(blockIdx.y * 16 + qy) * W1 + blockIdx.x * 16 + qx) * cp;
+      *reinterpret_cast<uint4*>(o) = pack8_bf16(sum, cin);
+      if (cp > 8) *reinterpret_cast<uint4*>(o + 8) = make_uint4(0u, 0u, 0u, 0u);
+    }
 #pragma unroll
-  for (int j = 0; j < 4; ++j) tile[t * 4 + j] = sum[j];
+    for (int j = 0; j < 4; ++j) tile[(qy * 16 + qx) * 4 + j] = sum[j];
+  }
   __syncthreads();
   int side = 16;
 #pragma unroll
@@ -403,7 +413,11 @@ struct Plan {
 static Plan make_plan(const nar_unet& n, int H, int W) {
   Plan p;
   p.L = n.cfg.levels;
-  p.cinp = rup(n.cfg.input_channels, 16);
+  // pyramid levels at an 8-channel stride when the input has <= 8 channels: 16-byte
+  // pixels, written with full-sector stores and no zero padding; the conv reads them
+  // through an overlapping tensor map (tc_make_map) whose channels 8..15 are the
+  // next pixel's (their weights are zero)
+  p.cinp = rup(n.cfg.input_channels, 8);
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
@@ -415,7 +429,7 @@ static Plan make_plan(const nar_unet& n, int H, int W) {
     p.W[k] = W >> k;
     const size_t px = (size_t)p.H[k] * p.W[k];
     const int w = stride_of(n.cfg, k);
-    p.off_pyr16[k] = take(px * p.cinp * 2);
+    p.off_pyr16[k] = take(px * p.cinp * 2 + 32);  // + the overlap read past the last pixel
     // off_x[k] (k >= 1) and the bottleneck off_skip[L-1] feed an up2 and are
     // written wide (H, 2W) on the tensor-core path
     p.off_skip[k] = take(px * w * 2 * (k + 1 == p.L ? 2 : 1));
@@ -745,7 +759,7 @@ int nar_unet_forward(nar_unet* n, const float* in, int32_t H, int32_t W, float* 
     if (cin == 4 && !aligned) kern = head_pyramid_kernel<8>;  // no float4 loads
     nar::count_launch();
     if (cin == 4 && aligned && L <= 5 && W % 32 == 0 && H % 32 == 0)
-      head_pyramid_quad_kernel<<<dim3(W / 32, H / 32), 256, 0, st>>>(
+      head_pyramid_quad_kernel<<<dim3(W / 32, H / 32), 128, 0, st>>>(
           in, H, W, cin, p.cinp, n->d_head_w, n->d_head_b, n->cfg.use_descriptor_head, L, po);
     else
       kern<<<dim3(W / T, H / T), T * T, sm, st>>>(in, H, W, cin, p.cinp, n->d_head_w,

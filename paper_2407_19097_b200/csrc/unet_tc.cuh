@@ -50,7 +50,7 @@
 namespace nar {
 
 struct ConvArgs {
-  const __nv_bfloat16* src_a;  // NHWC, channel stride ca_stride (multiple of 16)
+  const __nv_bfloat16* src_a;  // NHWC, channel stride ca_stride (multiple of 8)
   const __nv_bfloat16* src_b;  // NHWC, channel stride cb_stride, or NULL
   int ca, cb, ca_stride, cb_stride;
   // a_up2: srcA is nearest-upsampled 2x.  1 = srcA is (H/2, W/2) (SIMT path);
@@ -733,7 +733,11 @@ static int tc_make_map(CUtensorMap* m, const void* base, int cs, int w, int h, i
                        int bh) {
   auto fn = tc_encode_fn();
   if (!fn) return set_error(NAR_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  cuuint64_t dims[3] = {(cuuint64_t)cs, (cuuint64_t)w, (cuuint64_t)h};
+  // cs = 8 (a pyramid level): the 16-channel box still reads 32 bytes per pixel --
+  // channels 8..15 overlap the next pixel (their weights are zero; the buffer has
+  // slack for the last pixel), so every box row is in bounds (an out-of-bounds
+  // channel half makes TMA ~20 % slower)
+  cuuint64_t dims[3] = {(cuuint64_t)(cs < bc ? bc : cs), (cuuint64_t)w, (cuuint64_t)h};
   cuuint64_t strides[2] = {(cuuint64_t)cs * 2, (cuuint64_t)cs * 2 * (cuuint64_t)w};
   cuuint32_t box[3] = {(cuuint32_t)bc, (cuuint32_t)bw, (cuuint32_t)bh};
   cuuint32_t es[3] = {1, 1, 1};
@@ -851,8 +855,9 @@ inline int tc_launch_gated_conv(const ConvArgs& a, cudaStream_t st) {
   const int coutp = tc_coutp(a.cout);
   if (a.cout_stride % 8 || a.cout_stride < (a.cout + 7) / 8 * 8)
     return set_error(NAR_ERR_CONFIG, "conv output stride must be a multiple of 8 >= Cout");
-  if (a.ca_stride % 16 || (a.cb && a.cb_stride % 16))
-    return set_error(NAR_ERR_CONFIG, "conv input strides must be multiples of 16");
+  // (stride 8: see tc_make_map -- the source must have 16 readable bytes past its end)
+  if (a.ca_stride % 8 || (a.cb && a.cb_stride % 8))
+    return set_error(NAR_ERR_CONFIG, "conv input strides must be multiples of 8");
   if (a.head_out && (a.head_n < 1 || a.head_n > 4))
     return set_error(NAR_ERR_CONFIG, "fused out head supports 1..4 outputs");
   switch (2 * coutp) {
