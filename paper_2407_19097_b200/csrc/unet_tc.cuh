@@ -288,6 +288,13 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 32-byte global store (sm_100 STG.256): one full sector per lane
+__device__ __forceinline__ void st_global_v8(void* p, const uint32_t* w) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(w[0]),
+               "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+               : "memory");
+}
+
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -590,6 +597,72 @@ __global__ void __maxnreg__(96)
 #pragma unroll
           for (int k = 0; k < 4; ++k) logit[i][k] = 0.0f;
       }
+      if constexpr (!kHead && COUTP % 16 == 0) {
+        // 16 channels at a time: one x16 TMEM load per branch, one 32-byte store
+        // per lane (a full sector: 16-byte stores at the 32-byte pixel pitch of a
+        // 16-channel layer left every sector half written); rows one at a time
+        const int nc16 = a.cout_stride / 16;
+        for (int c16 = cslot; c16 < nc16; c16 += cgroups) {
+          const int c0 = c16 * 16;
+          const bool have = c0 < COUTP;
+#pragma unroll
+          for (int i = 0; i < RPW; ++i) {
+            if (u0 + i >= u1) break;
+            const int r = (u0 + i) * rstep;
+            float pacc[16];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              if (h == 1 && !do_pool) break;
+              float o[16];
+              if (have) {
+                float f[16], g[16];
+                const uint32_t col = tbase + (uint32_t)(b * R * N + (r + h) * N + c0) + lane_off;
+                tmem_ld16(col, f);
+                tmem_ld16(col + COUTP, g);
+                tmem_wait_ld();
+#pragma unroll
+                for (int e = 0; e < 16; ++e) o[e] = gate_h(f[e], g[e]);
+              } else {
+#pragma unroll
+                for (int e = 0; e < 16; ++e) o[e] = 0.0f;
+              }
+              const int y = y0 + r + h;
+              if (a.out != nullptr && y < a.H && xok) {
+                uint32_t pw[8];
+#pragma unroll
+                for (int e = 0; e < 16; e += 2) {
+                  __nv_bfloat162 hh = __floats2bfloat162_rn(o[e], o[e + 1]);
+                  pw[e / 2] = *reinterpret_cast<uint32_t*>(&hh);
+                }
+                const int wsh = a.out_wide;  // wide (H, 2W) output: each pixel twice
+                __nv_bfloat16* d = a.out + (((size_t)y * a.W + x) << wsh) * a.cout_stride + c0;
+                st_global_v8(d, pw);
+                if (wsh) st_global_v8(d + a.cout_stride, pw);
+              }
+              if (do_pool) {
+#pragma unroll
+                for (int e = 0; e < 16; ++e) pacc[e] = h == 0 ? o[e] : pacc[e] + o[e];
+              }
+            }
+            if (do_pool) {
+              // 2x2 average of the f32 outputs: rows r, r+1 here, columns m, m+1 via shuffle
+#pragma unroll
+              for (int e = 0; e < 16; ++e) pacc[e] += __shfl_xor_sync(0xffffffffu, pacc[e], 1);
+              const int y = y0 + r;
+              if ((m & 1) == 0 && y < a.H && xok) {
+                uint32_t pw[8];
+#pragma unroll
+                for (int e = 0; e < 16; e += 2) {
+                  __nv_bfloat162 hh = __floats2bfloat162_rn(0.25f * pacc[e], 0.25f * pacc[e + 1]);
+                  pw[e / 2] = *reinterpret_cast<uint32_t*>(&hh);
+                }
+                st_global_v8(a.pool_out + ((size_t)(y >> 1) * (a.W >> 1) + (x >> 1)) * a.cout_stride + c0,
+                             pw);
+              }
+            }
+          }
+        }
+      } else {
       // kHead: channel chunks unrolled (<= 4) so head weights index the
       // parameter bank with compile-time offsets
       constexpr int NC8_HEAD = 2 * ((COUTP + 15) / 16);
@@ -677,6 +750,7 @@ __global__ void __maxnreg__(96)
           }
         }
       }
+      }  // 8-channel chunks
       if (do_head) {
 #pragma unroll
         for (int i = 0; i < RPW; ++i) {
