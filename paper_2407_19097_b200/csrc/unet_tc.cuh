@@ -597,7 +597,49 @@ __global__ void __maxnreg__(96)
 #pragma unroll
           for (int k = 0; k < 4; ++k) logit[i][k] = 0.0f;
       }
-      if constexpr (!kHead && COUTP % 16 == 0) {
+      if constexpr (kHead && COUTP % 16 == 0) {
+        // fused out head (the last layer, <= 32 channels): rows one at a time, 16
+        // channels per x16 TMEM load; the logits take the head weights from the
+        // parameter bank (zero beyond cout / head_n, so no per-channel guards)
+#pragma unroll
+        for (int i = 0; i < RPW; ++i) {
+          if (u0 + i >= u1) break;
+          const int y = y0 + u0 + i;
+          const bool ok = y < a.H && xok;
+          float lg[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+          for (int c16 = 0; c16 < COUTP / 16; ++c16) {
+            const int c0 = c16 * 16;
+            float f[16], g[16], o[16];
+            const uint32_t col = tbase + (uint32_t)(b * R * N + (u0 + i) * N + c0) + lane_off;
+            tmem_ld16(col, f);
+            tmem_ld16(col + COUTP, g);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) o[e] = gate_h(f[e], g[e]);
+            if (a.out != nullptr && ok) {
+              uint32_t pw[8];
+#pragma unroll
+              for (int e = 0; e < 16; e += 2) {
+                __nv_bfloat162 hh = __floats2bfloat162_rn(o[e], o[e + 1]);
+                pw[e / 2] = *reinterpret_cast<uint32_t*>(&hh);
+              }
+              st_global_v8(a.out + ((size_t)y * a.W + x) * a.cout_stride + c0, pw);
+            }
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+#pragma unroll
+              for (int k = 0; k < 4; ++k) lg[k] = fmaf(o[e], a.head_wv[(c0 + e) * 4 + k], lg[k]);
+          }
+          if (ok) {
+            float* dst = a.head_out + ((size_t)y * a.W + x) * a.head_n;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              if (k < a.head_n)
+                dst[k] = fmaf(0.5f, tanh_approx(0.5f * (lg[k] + a.head_bv[k])), 0.5f);  // sigmoid
+          }
+        }
+      } else if constexpr (!kHead && COUTP % 16 == 0) {
         // 16 channels at a time: one x16 TMEM load per branch, one 32-byte store
         // per lane (a full sector: 16-byte stores at the 32-byte pixel pitch of a
         // 16-channel layer left every sector half written); rows one at a time
@@ -751,7 +793,7 @@ __global__ void __maxnreg__(96)
         }
       }
       }  // 8-channel chunks
-      if (do_head) {
+      if (do_head && COUTP % 16 != 0) {  // (the 16-channel head path stored its own)
 #pragma unroll
         for (int i = 0; i < RPW; ++i) {
           if (u0 + i >= u1) break;
