@@ -51,7 +51,11 @@ def _compile(src: Path, verbose: bool) -> Path:
     obj = BUILD / (src.stem + ".o")
     if obj.exists() and obj.stat().st_mtime >= _deps_mtime():
         return obj
-    cmd = [_nvcc(), *ARCH, *COMMON, *PER_FILE.get(src.name, []), "-c", str(src), "-o", str(obj)]
+    # NAR_NVCC_EXTRA: extra flags for experiment builds (e.g. -DNAR_TC_TRACE); such a
+    # build goes to another directory via NAR_BUILD_DIR so the product objects stay
+    extra = os.environ.get("NAR_NVCC_EXTRA", "").split()
+    cmd = [_nvcc(), *ARCH, *COMMON, *PER_FILE.get(src.name, []), *extra, "-c", str(src), "-o",
+           str(obj)]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     res = subprocess.run(cmd, capture_output=True, text=True)

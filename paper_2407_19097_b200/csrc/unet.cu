@@ -571,7 +571,7 @@ static int run_conv(nar_unet* n, Layer& l, const __nv_bfloat16* src_a, int ca_st
   a.debug = dbg;
   static const int sblk = [] {
     const char* e = getenv("NAR_TC_SLIDE_BLOCKS");
-    const int v = e ? atoi(e) : 2;
+    const int v = e ? atoi(e) : 1;
     return v < 1 ? 1 : (v > 4 ? 4 : v);
   }();
   a.slide_blocks = sblk;
@@ -720,6 +720,16 @@ int nar_unet_set_param(nar_unet* n, const char* name, const float* host, int64_t
     return set_error(NAR_ERR_CONFIG, m.c_str());
   }
   return NAR_OK;
+}
+
+// timing experiments: the clock64() stamps of the last conv launched with
+// NAR_TC_DEBUG bit 3 (see TC_TRACE in unet_tc.cuh); not part of the public header
+int nar_debug_tc_trace(unsigned long long* out, int n) {
+  if (!out || n > kTraceTiles * kTraceSlots) return set_error(NAR_ERR_INVALID, "trace");
+  cudaDeviceSynchronize();
+  return cudaMemcpyFromSymbol(out, g_tc_trace, n * sizeof(unsigned long long)) == cudaSuccess
+             ? NAR_OK
+             : set_error(NAR_ERR_CUDA, "trace copy");
 }
 
 int nar_unet_workspace_bytes(const nar_unet* n, int32_t height, int32_t width, size_t* bytes) {
@@ -888,6 +898,8 @@ int nar_gated_conv(const float* in, int32_t H, int32_t W, int32_t cin, const flo
     a.bias_g = bg;
     a.wtc = w;
     a.out = y;
+    const char* dbg = getenv("NAR_TC_DEBUG");  // timing experiments only
+    a.debug = dbg ? atoi(dbg) : 0;
     rc = tc_launch_gated_conv(a, st);
     if (!rc) {
       nar::count_launch();

@@ -139,6 +139,19 @@ __host__ __device__ constexpr int tc_epi_first_unit(int s, int units, int rg) {
 __host__ __device__ constexpr int tc_epi_last_row(int s, int units, int rg, int rstep) {
   return tc_epi_first_unit(s + 1, units, rg) * rstep - 1;
 }
+// Every tcgen05.commit is a bubble in the tensor pipe (~60 cycles, scripts/
+// mma_slide_bench.cu), so slots completing together share one signal: the barrier
+// of the first slot of their group.  Sliding layers complete all slots at the tile
+// end, or (two blocks) the slots ending by row R/2-1 after the first block and
+// the rest at the end; plain layers signal each slot as its last row completes.
+__host__ __device__ constexpr int tc_epi_signal(int s, bool slide, int nblk, int units, int rg,
+                                                int rstep, int R) {
+  if (!slide) return s;
+  if (nblk < 2) return 0;
+  int s1 = 0;  // slots complete after the first block (rows < R/2)
+  while (s1 < rg && tc_epi_last_row(s1, units, rg, rstep) <= R / 2 - 1) ++s1;
+  return s < s1 ? 0 : s1;
+}
 __host__ __device__ constexpr int tc_fixed_smem(int N) {
   return 512 + kTcOnesBytes + kTcBiasBytes + kTcParamFloats * 4;
 }
@@ -337,6 +350,26 @@ __device__ __forceinline__ float gate_h(float fh, float gh) {
 }
 
 
+// timing experiments (build with -DNAR_TC_TRACE, run with NAR_TC_DEBUG bit 3): CTA 0 records clock64() stamps of its
+// first kTraceTiles tiles -- [tile][0] MMA before the TMEM-empty wait, [1] after
+// it, [2+2q]/[3+2q] after chunk q's full wait / after its MMAs are issued,
+// [10]/[11] epilogue warp 1 after the TMEM-full wait / at the end of the tile,
+// [12]/[13] producer before / after the empty wait of the tile's first chunk
+constexpr int kTraceTiles = 16, kTraceSlots = 16;
+__device__ unsigned long long g_tc_trace[kTraceTiles * kTraceSlots];
+// (compiled in only with -DNAR_TC_TRACE: even dead, the checks cost the hot loops)
+#ifdef NAR_TC_TRACE
+#define TC_TRACE(tl, slot)                                                          \
+  do {                                                                              \
+    if ((a.debug & 8) && blockIdx.x == 0 && (tl) < kTraceTiles)                     \
+      g_tc_trace[(tl) * kTraceSlots + (slot)] = clock64();                          \
+  } while (0)
+#else
+#define TC_TRACE(tl, slot) \
+  do {                     \
+  } while (0)
+#endif
+
 // ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
@@ -450,7 +483,9 @@ __global__ void __maxnreg__(96)
         const int cbase = 16 * (in_a ? q : q - nqa);
         const CUtensorMap* map = in_a ? &tma_a : &tma_b;
         const int yr = up ? (y0 - 1) >> 1 : y0 - 1;  // arithmetic shift: row -1 stays OOB
+        if (q == 0) TC_TRACE(it / nq, 12);
         mbar_wait(&empty[s], ((uint32_t)(it / S) & 1u) ^ 1u);
+        if (q == 0) TC_TRACE(it / nq, 13);
         if (a.debug & 4) {  // timing experiment: no loads
           mbar_arrive(&full[s]);
           continue;
@@ -469,8 +504,10 @@ __global__ void __maxnreg__(96)
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tl) {
       const int b = tl % NB;
       uint64_t* tf = tfull + b * kEpiGroups;
+      if (lane == 0) TC_TRACE(tl, 0);
       mbar_wait(&tempty[b], (((uint32_t)(tl / NB)) & 1u) ^ 1u);
       tc_fence_after();
+      if (lane == 0) TC_TRACE(tl, 1);
       const uint32_t dcol = tbase + (uint32_t)(b * R * N);
       const int y0 = (tile / tiles_x) * R;
       for (int q = 0; q < nq; ++q, ++it) {
@@ -482,10 +519,11 @@ __global__ void __maxnreg__(96)
         const bool last = q == nq - 1;
         mbar_wait(&full[s], (uint32_t)(it / S) & 1u);
         tc_fence_after();
+        if (lane == 0 && q < 4) TC_TRACE(tl, 2 + 2 * q);
         if (lane == 0 && (a.debug & 2)) {
           umma_commit(&empty[s]);
           if (last)
-            for (int g = 0; g < rg; ++g) umma_commit(&tf[g]);
+            for (int g = 0; g < rg; ++g) umma_commit(&tf[g]);  // (all barriers: timing mode)
         } else if (lane == 0) {
           const uint32_t sa = smem_u32(smem + s * STAGE);
           const uint32_t sb = sa + A_BYTES;
@@ -499,10 +537,11 @@ __global__ void __maxnreg__(96)
           int slot = 0;  // next row slot to signal (last chunk)
           if constexpr (SLIDE) {
             // halo row h feeds output rows h-2..h (ky = 2, 1, 0): after h, rows <= h-2 are
-            // complete.  kx outer, h inner and unrolled (compile-time descriptors: the
-            // single issuing thread must keep up with ~57-cycle MMAs).  The last chunk
-            // (a.slide_blocks > 1) runs its halo rows in two blocks and signals the row
-            // slots the first block completes before starting the second.
+            // complete.  kx outer, h inner and unrolled: consecutive MMAs share the B
+            // block (h outer costs 75 vs 57 cycles per MMA, scripts/mma_slide_bench.cu).
+            // With a.slide_blocks > 1 the last chunk runs its halo rows in two blocks and
+            // signals the slots the first completes (default 1: one signal at the end --
+            // every commit is a ~60-cycle bubble in the tensor pipe).
             auto rows = [&](auto h0c, auto h1c) {
               constexpr int H0 = decltype(h0c)::value, H1 = decltype(h1c)::value;
 #pragma unroll 1
@@ -519,9 +558,11 @@ __global__ void __maxnreg__(96)
                   umma_bf16(dcol + (h - kymax) * N, adesc, bdesc, umma_idesc_bf16(128, nb * N), 1u);
                 }
               }
-              if (last)
-                while (slot < rg && H1 - 1 >= tc_epi_last_row(slot, units, rg, rstep) + 2)
-                  umma_commit(&tf[slot++]);
+              if (last) {  // one signal for all slots this block completed
+                const int s0 = slot;
+                while (slot < rg && H1 - 1 >= tc_epi_last_row(slot, units, rg, rstep) + 2) ++slot;
+                if (slot > s0) umma_commit(&tf[s0]);
+              }
             };
             constexpr int HM = R / 2 + 2;  // rows < R/2 are complete after halo row HM-1
             if (last && a.slide_blocks > 1 && R >= 2) {
@@ -547,6 +588,7 @@ __global__ void __maxnreg__(96)
             }
           }
           umma_commit(&empty[s]);
+          if (q < 4) TC_TRACE(tl, 3 + 2 * q);
         }
         __syncwarp();
       }
@@ -574,14 +616,17 @@ __global__ void __maxnreg__(96)
     // this warp's rows: units [u0, u1) of the tile (contiguous, see tc_epi_rgroups)
     const int u0 = tc_epi_first_unit(rslot, units, rgroups);
     const int u1 = tc_epi_first_unit(rslot + 1, units, rgroups);
+    const int sig = tc_epi_signal(rslot, SLIDE, (a.slide_blocks > 1 && R >= 2) ? 2 : 1, units,
+                                  rgroups, rstep, R);
     const int nc8 = a.cout_stride / 8;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     int tl = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++tl) {
       const int b = tl % NB;
       const int y0 = (tile / tiles_x) * R, x0 = (tile % tiles_x) * 128;
-      mbar_wait(&tfull[b * kEpiGroups + rslot], ((uint32_t)(tl / NB)) & 1u);
+      mbar_wait(&tfull[b * kEpiGroups + sig], ((uint32_t)(tl / NB)) & 1u);
       tc_fence_after();
+      if (warp == 1 && lane == 0) TC_TRACE(tl, 10);
       if (a.debug & 1) {
         tc_fence_before();
         __syncwarp();
@@ -813,6 +858,7 @@ __global__ void __maxnreg__(96)
           }
         }
       }
+      if (warp == 1 && lane == 0) TC_TRACE(tl, 11);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[b]);

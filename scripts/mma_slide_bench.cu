@@ -20,15 +20,17 @@ __device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t
   asm volatile("{.reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;}"
                :: "r"(d), "l"(a), "l"(b), "r"(id), "r"(acc));
 }
-// MODE 0: sliding (N<=64), 1: plain 9 taps x R rows, 2: sliding but A not shifted (kx ignored)
+// MODE 0: sliding (N<=64), 1: plain 9 taps x R rows, 2: sliding but A not shifted (kx ignored),
+// 3: sliding + 5 tcgen05.commit per 30 MMAs (the conv's per-slot signals), 4: sliding + one
+// no-swizzle N=256 bias MMA per tile, 5: 3 and 4, 6: sliding with h outer / kx inner
 template <int N, int MODE>
 __global__ void k(long long* out, int iters) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint32_t tb;
-  __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(8) uint64_t bar, bar2;
   const int w = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < 200 * 1024 / 4; i += blockDim.x) ((uint32_t*)sm)[i] = 0x3c003c00u;
-  if (threadIdx.x == 0) { asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(su(&bar))); asm volatile("fence.mbarrier_init.release.cluster;"); }
+  if (threadIdx.x == 0) { asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(su(&bar))); asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(su(&bar2))); asm volatile("fence.mbarrier_init.release.cluster;"); }
   if (w == 0) { asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" :: "r"(su(&tb))); asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;"); }
   asm volatile("fence.proxy.async.shared::cta;");
   asm volatile("tcgen05.fence::before_thread_sync;"); __syncthreads(); asm volatile("tcgen05.fence::after_thread_sync;");
@@ -39,7 +41,25 @@ __global__ void k(long long* out, int iters) {
     long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
       const uint32_t dcol = tb + (it & 1) * R * N;
-      if (MODE != 1) {
+      if (MODE == 4 || MODE == 5) {
+        mma(dcol, desc(a0, 2048, 128), desc(b0, 4096, 128), idesc(128, 256), 0u);
+        ++n_mma;
+      }
+      if (MODE == 6) {
+#pragma unroll 1
+        for (int h = 0; h < R + 2; ++h) {
+#pragma unroll
+          for (int kx = 0; kx < 3; ++kx) {
+            const int kymax = h < 2 ? h : 2;
+            const int kymin = h - (R - 1) > 0 ? h - (R - 1) : 0;
+            const int nb = kymax - kymin + 1;
+            const uint64_t bd = desc(b0 + kx * 3 * N * 32 + (2 - kymax) * N * 16, 3 * N * 16, 128);
+            const uint64_t ad = desc_sw32(a0 + h * 4352 + kx * 32);
+            mma(dcol + (h - kymax) * N, ad, bd, idesc(128, nb * N), 1u);
+            ++n_mma;
+          }
+        }
+      } else if (MODE != 1) {
 #pragma unroll 1
         for (int kx = 0; kx < 3; ++kx) {
 #pragma unroll
@@ -52,6 +72,9 @@ __global__ void k(long long* out, int iters) {
             mma(dcol + (h - kymax) * N, ad, bd, idesc(128, nb * N), 1u);
             ++n_mma;
           }
+          if ((MODE == 3 || MODE == 5) && kx == 2)
+            for (int c = 0; c < 5; ++c)
+              asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" :: "r"(su(&bar2)));
         }
       } else {
 #pragma unroll 1
@@ -89,6 +112,8 @@ template <int N, int MODE> void run(const char* what) {
 }
 int main() {
   run<32, 0>("slide (conv)"); run<32, 2>("slide, A unshifted"); run<32, 1>("plain 9 taps");
+  run<32, 3>("slide + 5 commits/tile"); run<32, 4>("slide + bias MMA"); run<32, 5>("slide + both");
+  run<32, 6>("slide, h outer"); run<64, 3>("slide + 5 commits/tile"); run<64, 5>("slide + both");
   run<64, 0>("slide (conv)"); run<64, 2>("slide, A unshifted"); run<64, 1>("plain 9 taps");
   run<128, 1>("plain 9 taps"); run<256, 1>("plain 9 taps");
   return 0;
