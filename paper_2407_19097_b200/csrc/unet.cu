@@ -43,8 +43,26 @@ static inline int rup(int x, int m) { return (x + m - 1) / m * m; }
 // bf16 NHWC padded to cp channels (zeros in the padding).
 struct PyrOut {
   __nv_bfloat16* lvl[8];
+  // bf16 levels: row pitch (W >> k) + pad pixels; the pad pixel(s) of every row are
+  // written as zeros (the conv's overlapping tensor map reads 16 bytes past a row's last
+  // pixel, which must not be the next row's first)
+  int pad;
   float* lvlf[8];  // standalone API (nar_head_pyramid): f32 (H>>k, W>>k, cin) levels instead
 };
+
+// Zero the pad pixels of the pyramid rows a CTA covers (level k: rows0 >> k rows from
+// ty * (rows0 >> k), rows0 = the CTA's level-0 rows); called by the last tile column.
+__device__ __forceinline__ void pyr_zero_pads(const PyrOut& out, int W, int ty, int rows0,
+                                              int levels, int cp, int t) {
+  for (int k = 0; k < levels; ++k) {
+    const int rows = rows0 >> k, Wk = W >> k;
+    for (int i = t; i < rows * out.pad; i += blockDim.x) {
+      __nv_bfloat16* o =
+          out.lvl[k] + ((size_t)(ty * rows + i / out.pad) * (Wk + out.pad) + Wk + i % out.pad) * cp;
+      for (int c8 = 0; c8 < cp; c8 += 8) *reinterpret_cast<uint4*>(o + c8) = make_uint4(0u, 0u, 0u, 0u);
+    }
+  }
+}
 
 // CIN: compile-time upper bound of cin (4, 8 or 16) so the per-pixel channel
 // arrays stay in registers at high occupancy.
@@ -92,7 +110,7 @@ __global__ void __launch_bounds__(256, 4)
       if (j < cin) f0[j] = hv[j];
   } else {
   // bf16 level 0, padded to cp channels, 16-byte stores
-  __nv_bfloat16* o0 = out.lvl[0] + ((size_t)y * W + xx) * cp;
+  __nv_bfloat16* o0 = out.lvl[0] + ((size_t)y * (W + out.pad) + xx) * cp;
 #pragma unroll
   for (int c8 = 0; c8 < 16; c8 += 8) {
     if (c8 >= cp) break;
@@ -138,7 +156,7 @@ __global__ void __launch_bounds__(256, 4)
         for (int c = 0; c < CIN; ++c)
           if (c < cin) fk[c] = m[c];
       } else {
-        __nv_bfloat16* ok = out.lvl[k] + ((size_t)(ty * ns + qy) * Wk + (tx * ns + qx)) * cp;
+        __nv_bfloat16* ok = out.lvl[k] + ((size_t)(ty * ns + qy) * (Wk + out.pad) + (tx * ns + qx)) * cp;
 #pragma unroll
         for (int c8 = 0; c8 < 16; c8 += 8) {
           if (c8 >= cp) break;
@@ -157,6 +175,7 @@ __global__ void __launch_bounds__(256, 4)
     __syncthreads();
     side = ns;
   }
+  if (out.pad && !out.lvlf[0] && tx == gridDim.x - 1) pyr_zero_pads(out, W, ty, T, levels, cp, t);
 }
 
 // Same result for the common case -- 4 input channels (16-byte aligned), levels
@@ -217,7 +236,7 @@ __global__ void __launch_bounds__(128)
         }
         hq[d][j] = j < cin ? acc : 0.f;
       }
-      __nv_bfloat16* o = out.lvl[0] + ((size_t)(y0 + (d >> 1)) * W + x0 + (d & 1)) * cp;
+      __nv_bfloat16* o = out.lvl[0] + ((size_t)(y0 + (d >> 1)) * (W + out.pad) + x0 + (d & 1)) * cp;
       *reinterpret_cast<uint4*>(o) = pack8_bf16(hq[d], cin);
       if (cp > 8) *reinterpret_cast<uint4*>(o + 8) = make_uint4(0u, 0u, 0u, 0u);
     }
@@ -227,7 +246,7 @@ __global__ void __launch_bounds__(128)
     // level 1 from registers
     if (levels > 1) {
       const int W1 = W >> 1;
-      __nv_bfloat16* o = out.lvl[1] + ((size_t)(blockIdx.y * 16 + qy) * W1 + blockIdx.x * 16 + qx) * cp;
+      __nv_bfloat16* o = out.lvl[1] + ((size_t)(blockIdx.y * 16 + qy) * (W1 + out.pad) + blockIdx.x * 16 + qx) * cp;
       *reinterpret_cast<uint4*>(o) = pack8_bf16(sum, cin);
       if (cp > 8) *reinterpret_cast<uint4*>(o + 8) = make_uint4(0u, 0u, 0u, 0u);
     }
@@ -254,13 +273,14 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
       for (int c = 0; c < 4; ++c) tile[t * 4 + c] = m[c];
       const int Wk = W >> k;
-      __nv_bfloat16* o = out.lvl[k] + ((size_t)(blockIdx.y * ns + py) * Wk + blockIdx.x * ns + pxx) * cp;
+      __nv_bfloat16* o = out.lvl[k] + ((size_t)(blockIdx.y * ns + py) * (Wk + out.pad) + blockIdx.x * ns + pxx) * cp;
       *reinterpret_cast<uint4*>(o) = pack8_bf16(m, cin);
       if (cp > 8) *reinterpret_cast<uint4*>(o + 8) = make_uint4(0u, 0u, 0u, 0u);
     }
     __syncthreads();
     side = ns;
   }
+  if (out.pad && blockIdx.x == gridDim.x - 1) pyr_zero_pads(out, W, blockIdx.y, 32, levels, cp, t);
 }
 
 // 2x2 average of a bf16 (H,W,C) map into bf16 (H/2,W/2,C), 8 channels per thread.
@@ -335,7 +355,7 @@ __global__ void gated_conv_simt(ConvArgs a) {
       if (a.a_up2)
         pa = a.src_a + ((int64_t)(yy / 2) * (a.W / 2) + xx / 2) * a.ca_stride;
       else
-        pa = a.src_a + ((int64_t)yy * a.W + xx) * a.ca_stride;
+        pa = a.src_a + ((int64_t)yy * (a.a_pitch ? a.a_pitch : a.W) + xx) * a.ca_stride;
       const float* wf = a.wf32 + ((int64_t)tap * cin) * a.cout + j;
       const float* wg = a.wg32 + ((int64_t)tap * cin) * a.cout + j;
       for (int c = 0; c < a.ca; ++c) {
@@ -344,7 +364,7 @@ __global__ void gated_conv_simt(ConvArgs a) {
         g = fmaf(v, wg[(int64_t)c * a.cout], g);
       }
       if (a.cb) {
-        const __nv_bfloat16* pb = a.src_b + ((int64_t)yy * a.W + xx) * a.cb_stride;
+        const __nv_bfloat16* pb = a.src_b + ((int64_t)yy * (a.b_pitch ? a.b_pitch : a.W) + xx) * a.cb_stride;
         for (int c = 0; c < a.cb; ++c) {
           const float v = __bfloat162float(pb[c]);
           f = fmaf(v, wf[(int64_t)(a.ca + c) * a.cout], f);
@@ -429,7 +449,7 @@ static Plan make_plan(const nar_unet& n, int H, int W) {
     p.W[k] = W >> k;
     const size_t px = (size_t)p.H[k] * p.W[k];
     const int w = stride_of(n.cfg, k);
-    p.off_pyr16[k] = take(px * p.cinp * 2 + 32);  // + the overlap read past the last pixel
+    p.off_pyr16[k] = take((px + p.H[k]) * p.cinp * 2);  // rows of W + 1 pixels (PyrOut::pad)
     // off_x[k] (k >= 1) and the bottleneck off_skip[L-1] feed an up2 and are
     // written wide (H, 2W) on the tensor-core path
     p.off_skip[k] = take(px * w * 2 * (k + 1 == p.L ? 2 : 1));
@@ -504,9 +524,11 @@ static int run_conv(nar_unet* n, Layer& l, const __nv_bfloat16* src_a, int ca_st
                     const __nv_bfloat16* src_b, int cb_stride, int H, int W,
                     __nv_bfloat16* out, cudaStream_t st, __nv_bfloat16* pool_out = nullptr,
                     float* head_out = nullptr, __nv_bfloat16* scratch = nullptr,
-                    int out_wide = 0) {
+                    int out_wide = 0, int a_pitch = 0, int b_pitch = 0) {
   ConvArgs a;
   memset(&a, 0, sizeof(a));
+  a.a_pitch = a_pitch;
+  a.b_pitch = b_pitch;
   a.src_a = src_a;
   a.src_b = src_b;
   a.ca = l.ca;
@@ -761,6 +783,7 @@ int nar_unet_forward(nar_unet* n, const float* in, int32_t H, int32_t W, float* 
     PyrOut po;
     memset(&po, 0, sizeof(po));
     for (int k = 0; k < L; ++k) po.lvl[k] = bf(p.off_pyr16[k]);
+    po.pad = 1;
     const size_t sm = (size_t)T * T * cin * 4;
     if (T * T > 256) return set_error(NAR_ERR_CONFIG, "at most 5 pyramid levels supported");
     auto kern = cin <= 4 ? head_pyramid_kernel<4>
@@ -784,10 +807,11 @@ int nar_unet_forward(nar_unet* n, const float* in, int32_t H, int32_t W, float* 
     Layer& lb = n->layers[li++];
     if (k == 0) {
       rc = run_conv(n, la, bf(p.off_pyr16[0]), p.cinp, 0, nullptr, 0, p.H[0], p.W[0],
-                    bf(p.off_tmp[0]), st);
+                    bf(p.off_tmp[0]), st, nullptr, nullptr, nullptr, 0, p.W[0] + 1);
     } else {
       rc = run_conv(n, la, bf(p.off_pool[k - 1]), stride_of(n->cfg, k - 1), 0,
-                    bf(p.off_pyr16[k]), p.cinp, p.H[k], p.W[k], bf(p.off_tmp[k]), st);
+                    bf(p.off_pyr16[k]), p.cinp, p.H[k], p.W[k], bf(p.off_tmp[k]), st, nullptr,
+                    nullptr, nullptr, 0, 0, p.W[k] + 1);
     }
     if (rc) return rc;
     const bool last = L == 1;

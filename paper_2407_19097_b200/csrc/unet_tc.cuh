@@ -60,6 +60,8 @@ struct ConvArgs {
   int a_up2;
   int H, W;                    // output (and src_b) resolution
   int out_wide;                // tensor-core path: write out as (H, 2W), each pixel twice
+  int a_pitch, b_pitch;        // row pitch of src_a / src_b in pixels (0: W); pyramid
+                               // levels have W + 1 (a zero pad pixel per row)
   int cout, cout_stride;       // real output channels, output channel stride
   const float* wf32;           // SIMT path: HWIO f32
   const float* wg32;
@@ -892,15 +894,15 @@ static PFN_cuTensorMapEncodeTiled_v12000 tc_encode_fn() {
 
 // NHWC bf16 tensor (h, w, cs) -> 3-D map over (channel, x, y), box {bc, bw, bh}.
 static int tc_make_map(CUtensorMap* m, const void* base, int cs, int w, int h, int bc, int bw,
-                       int bh) {
+                       int bh, int pitch = 0) {
   auto fn = tc_encode_fn();
   if (!fn) return set_error(NAR_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   // cs = 8 (a pyramid level): the 16-channel box still reads 32 bytes per pixel --
-  // channels 8..15 overlap the next pixel (their weights are zero; the buffer has
-  // slack for the last pixel), so every box row is in bounds (an out-of-bounds
-  // channel half makes TMA ~20 % slower)
+  // channels 8..15 overlap the next pixel (their weights are zero), so every box row
+  // is in bounds (an out-of-bounds channel half makes TMA ~20 % slower); the last
+  // pixel of a row reads the row's zero pad pixel (pitch = W + 1), never the next row
   cuuint64_t dims[3] = {(cuuint64_t)(cs < bc ? bc : cs), (cuuint64_t)w, (cuuint64_t)h};
-  cuuint64_t strides[2] = {(cuuint64_t)cs * 2, (cuuint64_t)cs * 2 * (cuuint64_t)w};
+  cuuint64_t strides[2] = {(cuuint64_t)cs * 2, (cuuint64_t)cs * 2 * (cuuint64_t)(pitch ? pitch : w)};
   cuuint32_t box[3] = {(cuuint32_t)bc, (cuuint32_t)bw, (cuuint32_t)bh};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
@@ -959,10 +961,10 @@ static int tc_launch_nhb(const ConvArgs& a, cudaStream_t st) {
   if (a.a_up2)  // wide (H/2, W) source: LR low-res rows, 136 wide pixels
     rc = tc_make_map(&ma, a.src_a, a.ca_stride, a.W, a.H / 2, 16, kHaloPitch, tc_low_rows(N, NB));
   else
-    rc = tc_make_map(&ma, a.src_a, a.ca_stride, a.W, a.H, 16, kHaloPitch, R + 2);
+    rc = tc_make_map(&ma, a.src_a, a.ca_stride, a.W, a.H, 16, kHaloPitch, R + 2, a.a_pitch);
   if (rc) return rc;
   if (a.cb) {
-    rc = tc_make_map(&mb, a.src_b, a.cb_stride, a.W, a.H, 16, kHaloPitch, R + 2);
+    rc = tc_make_map(&mb, a.src_b, a.cb_stride, a.W, a.H, 16, kHaloPitch, R + 2, a.b_pitch);
     if (rc) return rc;
   } else {
     mb = ma;
@@ -1017,9 +1019,11 @@ inline int tc_launch_gated_conv(const ConvArgs& a, cudaStream_t st) {
   const int coutp = tc_coutp(a.cout);
   if (a.cout_stride % 8 || a.cout_stride < (a.cout + 7) / 8 * 8)
     return set_error(NAR_ERR_CONFIG, "conv output stride must be a multiple of 8 >= Cout");
-  // (stride 8: see tc_make_map -- the source must have 16 readable bytes past its end)
+  // (stride 8 < the 16-channel box: see tc_make_map -- rows need a zero pad pixel)
   if (a.ca_stride % 8 || (a.cb && a.cb_stride % 8))
     return set_error(NAR_ERR_CONFIG, "conv input strides must be multiples of 8");
+  if ((a.ca_stride < 16 && a.a_pitch <= a.W) || (a.cb && a.cb_stride < 16 && a.b_pitch <= a.W))
+    return set_error(NAR_ERR_CONFIG, "8-channel conv inputs need a zero pad pixel per row");
   if (a.head_out && (a.head_n < 1 || a.head_n > 4))
     return set_error(NAR_ERR_CONFIG, "fused out head supports 1..4 outputs");
   switch (2 * coutp) {

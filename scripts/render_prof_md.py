@@ -58,7 +58,7 @@ def main(tag):
                 tot_rd += rd
                 tot_red += red
                 tot_rds += rds
-            g = (lambda x: x / t * 1e3 / 1e3) if t else (lambda x: 0.0)
+            g = (lambda x: x / t * 1e3) if t else (lambda x: 0.0)  # M per us -> G/s
             out.append(f"| {i} | {nm} | {t:.1f} | {rd:.1f} | {rd / t * 1e3 if t else 0:.0f} | "
                        f"{red:.2f} | {g(red):.1f} | {req:.2f} | {rds:.2f} | {g(rds):.1f} | "
                        f"{k.get('lts__t_sector_hit_rate.pct', 0):.1f} | "
@@ -68,8 +68,8 @@ def main(tag):
         out += ["", f"Render (all passes + Hi-Z refreshes): {tot_t:.1f} us, DRAM read {tot_rd:.0f} MB vs "
                 f"{alg:.0f} MB algorithmic ({tot_rd / alg:.2f}x), {alg / tot_t:.2f} TB/s algorithmic "
                 f"= {alg / tot_t / 6.5533:.2f} of the measured 6553 GB/s; {tot_red:.1f}M RED sectors "
-                f"({tot_red / tot_t:.2f} G/s averaged over the render), {tot_rds:.1f}M SM-read sectors "
-                f"({tot_rds / tot_t:.2f} G/s).", ""]
+                f"({tot_red / tot_t * 1e3:.0f} G/s averaged over the render), {tot_rds:.1f}M SM-read sectors "
+                f"({tot_rds / tot_t * 1e3:.0f} G/s).", ""]
     (ROOT / "profiles" / f"{tag}_render_ncu.md").write_text("\n".join(out) + "\n")
     print("\n".join(out))
 

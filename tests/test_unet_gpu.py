@@ -311,3 +311,27 @@ def test_unet_on_non_current_device_index(cuda):
     with _lib.on_device(cuda.index):
         y = net(x)
     assert torch.isfinite(y).all()
+
+
+def test_forward_with_poisoned_workspace(cuda):
+    """Workspace memory starts as NaN bytes (0xFF): every buffer the network reads --
+    including the pyramid levels' per-row pad pixels that the 8-channel overlapping
+    tensor maps touch -- must be written before it is read, so the output equals the
+    oracle's (a stale NaN would spread through the 3x3 convs)."""
+    import torch
+
+    from paper_2407_19097_b200.neural import UNet, UNetConfig, init_params
+
+    cfg = UNetConfig(input_channels=4)
+    params = init_params(cfg)
+    net = UNet(cfg, params, device=cuda)
+    H, W = 128, 192
+    ws = net._workspace(H, W)
+    ws.fill_(255)
+    x = np.random.default_rng(3).uniform(0, 1, (H, W, 4)).astype(np.float32)
+    y = torch.empty((H, W, 3), device=cuda)
+    net.forward_into(torch.from_numpy(x).to(cuda), y)
+    y = y.cpu().numpy()
+    assert np.isfinite(y).all()
+    ref = oracle.forward(x[None], params, cfg)[0]
+    assert oracle.psnr(y, ref) >= PSNR_MIN
