@@ -391,6 +391,8 @@ struct Layer {
   float* bf = nullptr;
   float* bg = nullptr;
   uint16_t* wtc = nullptr;  // tcgen05-packed bf16 weights (unet_tc.cuh layout)
+  bool up2 = false;         // source A is the nearest-upsampled lower level (decoder "a")
+  bool pairs = false;       // packed with paired up2 chunks (tc_pack_weights)
   size_t wtc_bytes = 0;
   std::vector<float> hf, hg, hbf, hbg;  // host staging (HWIO)
   bool set_f = false, set_g = false, set_bf = false, set_bg = false;
@@ -505,7 +507,12 @@ static int upload(nar_unet* n) {
     if (dup(l.hf, &l.wf32) || dup(l.hg, &l.wg32) || dup(l.hbf, &l.bf) || dup(l.hbg, &l.bg))
       return set_error(NAR_ERR_NOMEM, "weight upload failed");
     std::vector<uint16_t> packed;
-    tc_pack_weights(l.hf, l.hg, l.ca, l.cb, l.cout, packed);
+    {
+      const int N = 2 * tc_coutp(l.cout);
+      l.pairs = !n->simt && l.up2 && tc_slide(N) && tc_rows(N, 2) % 2 == 0 &&
+                !(getenv("NAR_TC_UP2PAIR") && getenv("NAR_TC_UP2PAIR")[0] == '0');
+    }
+    tc_pack_weights(l.hf, l.hg, l.ca, l.cb, l.cout, packed, l.pairs);
     l.wtc_bytes = packed.size() * 2;
     if (cudaMalloc(&l.wtc, l.wtc_bytes) != cudaSuccess)
       return set_error(NAR_ERR_NOMEM, "weight upload failed");
@@ -546,6 +553,7 @@ static int run_conv(nar_unet* n, Layer& l, const __nv_bfloat16* src_a, int ca_st
   a.bias_f = l.bf;
   a.bias_g = l.bg;
   a.wtc = reinterpret_cast<const __nv_bfloat16*>(l.wtc);
+  a.up2pair = l.pairs && a_up2 == 2;
   a.out = out;
   const int cst = a.cout_stride;
   auto pool_kernel = [&](const __nv_bfloat16* src) {
@@ -645,6 +653,7 @@ int nar_unet_create(const nar_unet_config* cfg, nar_unet** out) {
     const int w = width_of(*cfg, k);
     Layer a;
     a.name = "dec" + std::to_string(k) + "a";
+    a.up2 = true;
     a.ca = width_of(*cfg, k + 1);
     a.cb = w;
     a.cout = w;

@@ -85,6 +85,9 @@ struct ConvArgs {
   // sliding layers: halo-row blocks of the last chunk, each followed by the
   // signal of the epilogue row slots it completes (1 = signal at the tile end)
   int slide_blocks;
+  // paired up2 chunks (sliding layers with a wide up2 source, R even): the packed weights
+  // hold 4 stacked ky blocks per kx for source-A chunks (tc_pack_weights, pairs = true)
+  int up2pair;
 };
 
 constexpr int kProdWarps = 1;   // TMA issue (one lane)
@@ -110,7 +113,11 @@ __host__ __device__ constexpr int tc_r1024(int x) { return (x + 1023) / 1024 * 1
 __host__ __device__ constexpr int tc_a_bytes(int N, int NB) {
   return tc_r1024((tc_rows(N, NB) + 2) * kHaloRowBytes);
 }
-__host__ __device__ constexpr int tc_b_bytes(int N) { return 9 * N * 32; }
+// B slot of a stage: 9 taps x N rows x 32 B; sliding layers reserve 3 kx x 4N rows (the
+// paired up2 chunks, see tc_pack_weights) -- 4/3 of the plain size
+__host__ __device__ constexpr int tc_b_bytes(int N) { return N <= 64 ? 12 * N * 32 : 9 * N * 32; }
+__host__ __device__ constexpr int tc_b3_bytes(int N) { return 9 * N * 32; }   // a plain chunk
+__host__ __device__ constexpr int tc_b4_bytes(int N) { return 12 * N * 32; }  // a paired chunk
 __host__ __device__ constexpr int tc_stage_bytes(int N, int NB) {
   return tc_r1024(tc_a_bytes(N, NB) + tc_b_bytes(N));
 }
@@ -183,12 +190,23 @@ __host__ __device__ constexpr int tc_coutp(int cout) {
 // so the accumulators hold f/2 and g/2, the operands of the epilogue's
 // elu(f)/2 and tanh(g/2) (see gate_h).
 // Sliding layers (tc_slide(N)): [chunk q][kx][k8][n' = (2 - ky) * N + n][8].
+//
+// Paired up2 chunks (pairs = true: a sliding layer whose source A is nearest-upsampled
+// 2x): consecutive halo rows 2j-1, 2j read the same low-res row, so their two sliding
+// MMAs merge into one with 4 stacked blocks per kx, [W2; W1+W2; W0+W1; W0] (n' = b*N + n,
+// the sums in f32 before the bf16 rounding) feeding output rows 2j-3 .. 2j: source-A
+// chunks are [chunk q][kx][k8][4N][8] (tc_b4_bytes), source-B chunks as above.
 inline void tc_pack_weights(const std::vector<float>& wf, const std::vector<float>& wg, int ca,
-                            int cb, int cout, std::vector<uint16_t>& packed) {
+                            int cb, int cout, std::vector<uint16_t>& packed, bool pairs = false) {
   const int coutp = tc_coutp(cout), N = 2 * coutp;
   const bool slide = tc_slide(N);
+  pairs = pairs && slide;
   const int nqa = (ca + 15) / 16, nqb = (cb + 15) / 16, nq = nqa + nqb, cin = ca + cb;
-  packed.assign((size_t)nq * 9 * 2 * N * 8, 0);
+  const size_t e3 = (size_t)9 * 2 * N * 8;      // elements of a plain chunk
+  const size_t q4 = (size_t)3 * 2 * 4 * N * 8;  // ... of a paired chunk
+  packed.assign(pairs ? nqa * q4 + nqb * e3 : (size_t)nq * e3, 0);
+  // first element of chunk q
+  auto chunk0 = [&](int q) { return pairs ? (q < nqa ? q * q4 : nqa * q4 + (q - nqa) * e3) : q * e3; };
   auto bf16 = [](float v) -> uint16_t {
     uint32_t u;
     memcpy(&u, &v, 4);
@@ -209,13 +227,31 @@ inline void tc_pack_weights(const std::vector<float>& wf, const std::vector<floa
             const int j = is_g ? n - coutp : n;
             if (j >= cout) continue;
             const float v = 0.5f * (is_g ? wg : wf)[((size_t)tap * cin + ci) * cout + j];
+            if (pairs && in_a) continue;  // paired blocks: below
             if (slide) {
               const int ky = tap / 3, kx = tap % 3;
               const size_t np = (size_t)(2 - ky) * N + n;
-              packed[((((size_t)q * 3 + kx) * 2 + k8) * (3 * N) + np) * 8 + e] = bf16(v);
+              packed[chunk0(q) + (((size_t)kx * 2 + k8) * (3 * N) + np) * 8 + e] = bf16(v);
             } else {
-              packed[((((size_t)q * 9 + tap) * 2 + k8) * N + n) * 8 + e] = bf16(v);
+              packed[chunk0(q) + (((size_t)tap * 2 + k8) * N + n) * 8 + e] = bf16(v);
             }
+          }
+  if (!pairs) return;
+  for (int q = 0; q < nqa; ++q)
+    for (int kx = 0; kx < 3; ++kx)
+      for (int k8 = 0; k8 < 2; ++k8)
+        for (int n = 0; n < N; ++n)
+          for (int e = 0; e < 8; ++e) {
+            const int ci = 16 * q + 8 * k8 + e;
+            const bool is_g = n >= coutp;
+            const int j = is_g ? n - coutp : n;
+            if (ci >= ca || j >= cout) continue;
+            const float* w = is_g ? wg.data() : wf.data();
+            auto W = [&](int ky) { return w[((size_t)(ky * 3 + kx) * cin + ci) * cout + j]; };
+            const float blk[4] = {W(2), W(1) + W(2), W(0) + W(1), W(0)};
+            for (int b = 0; b < 4; ++b)
+              packed[((((size_t)q * 3 + kx) * 2 + k8) * (4 * N) + (size_t)b * N + n) * 8 + e] =
+                  bf16(0.5f * blk[b]);
           }
 }
 
@@ -492,9 +528,15 @@ __global__ void __maxnreg__(96)
           mbar_arrive(&full[s]);
           continue;
         }
-        mbar_expect_tx(&full[s], (up ? UP_TX : A_TX) + B_BYTES);
+        // chunk q's packed weights: paired up2 chunks (4 stacked blocks) first
+        constexpr uint32_t B3 = tc_b3_bytes(N), B4 = tc_b4_bytes(N);
+        const bool pq = SLIDE && a.up2pair && in_a;
+        const uint32_t bbytes = pq ? B4 : B3;
+        const size_t boff = a.up2pair ? (in_a ? (size_t)q * B4 : (size_t)nqa * B4 + (size_t)(q - nqa) * B3)
+                                      : (size_t)q * B3;
+        mbar_expect_tx(&full[s], (up ? UP_TX : A_TX) + bbytes);
         tma_load_3d(stA, map, cbase, x0 - 1, yr, &full[s]);
-        bulk_g2s(stA + A_BYTES, a.wtc + (size_t)q * (B_BYTES / 2), B_BYTES, &full[s]);
+        bulk_g2s(stA + A_BYTES, reinterpret_cast<const uint8_t*>(a.wtc) + boff, bbytes, &full[s]);
       }
     }
   } else if (warp == kMmaWarp) {
@@ -567,7 +609,32 @@ __global__ void __maxnreg__(96)
               }
             };
             constexpr int HM = R / 2 + 2;  // rows < R/2 are complete after halo row HM-1
-            if (last && a.slide_blocks > 1 && R >= 2) {
+            bool paired = false;
+            if constexpr (R % 2 == 0) paired = a.up2pair && up;
+            if (paired) {
+              // paired up2 chunk (tc_pack_weights): halo rows 2g-1, 2g read low-res row g, one
+              // MMA with blocks [W2; W1+W2; W0+W1; W0] covers output rows 2g-3 .. 2g (clipped
+              // to the tile); halo rows 0 and R+1 stay single (W0 -> row 0, W2 -> row R-1)
+#pragma unroll 1
+              for (int kx = 0; kx < 3; ++kx) {
+                const uint32_t bk = sb + kx * (4 * N * 32);  // [k8][4N][8]: LBO = 4N*16
+#pragma unroll
+                for (int g = 0; g < R / 2 + 2; ++g) {
+                  const int blk0 = g == 0 ? 3 : (3 - 2 * g > 0 ? 3 - 2 * g : 0);
+                  const int blk1 = g == R / 2 + 1 ? 0 : (R + 2 - 2 * g < 3 ? R + 2 - 2 * g : 3);
+                  const int drow = g == 0 ? 0 : (g == R / 2 + 1 ? R - 1 : 2 * g - 3 + blk0);
+                  const uint64_t bdesc = umma_desc(bk + blk0 * N * 16, 4 * N * 16, 128);
+                  const uint64_t adesc = umma_desc_sw32(sa + g * kHaloRowBytes + kx * 32);
+                  umma_bf16(dcol + drow * N, adesc, bdesc, umma_idesc_bf16(128, (blk1 - blk0 + 1) * N), 1u);
+                }
+              }
+              if (last) {  // (decoder layers end with the skip chunk; kept for completeness)
+                const int nb = (a.slide_blocks > 1 && R >= 2) ? 2 : 1;
+                for (int g = 0; g < rg; ++g)
+                  if (tc_epi_signal(g, true, nb, units, rg, rstep, R) == g) umma_commit(&tf[g]);
+                slot = rg;
+              }
+            } else if (last && a.slide_blocks > 1 && R >= 2) {
               rows(std::integral_constant<int, 0>{}, std::integral_constant<int, HM>{});
               rows(std::integral_constant<int, HM>{}, std::integral_constant<int, R + 2>{});
             } else {
