@@ -291,13 +291,16 @@ constexpr int kRenderThreads = kRenderWarps * 32;
 constexpr int kPtsPerThread = NAR_RENDER_PPT;
 constexpr int kChunkPts = 32 * kPtsPerThread;                // points per warp step
 constexpr int kChunkBytes = kChunkPts * 12;
-constexpr int kWarpStages = 6;
+// ring depth of the exact kernel: 6 x 64-point or 3 x 128-point chunks in flight per warp
+constexpr int kWarpStages = kPtsPerThread >= 4 ? 3 : 6;
 constexpr int kRingBytes = kRenderWarps * kWarpStages * kChunkBytes;
 constexpr int kQueueBytes = kRenderWarps * 32 * 16;
 constexpr int kHizMaxEntries = 34816;                        // 68 KB coarse depth (u16)
 constexpr int kRenderSmem =
     kRingBytes + kQueueBytes + kHizMaxEntries * 2 + kRenderWarps * kWarpStages * 8 + 128;
-constexpr int kUnitPts = 2 * kChunkPts;  // schedule granularity (tail -> simple kernel)
+constexpr int kUnitPts = 128;  // schedule granularity (tail -> simple kernel)
+constexpr int kChunksPerUnit = kUnitPts / kChunkPts;  // exact-kernel chunks per unit (1 or 2)
+static_assert(kChunksPerUnit * kChunkPts == kUnitPts, "chunk / unit sizes");
 constexpr int kUnitBytes = kUnitPts * 12;
 constexpr int kTilePts = kUnitPts;
 
@@ -328,7 +331,7 @@ struct ChunkMap {
   }
   // first point of 64-point chunk c (c counts halves of slots)
   __device__ __forceinline__ uint32_t off64(uint32_t c) const {
-    return unit(c >> 1) * kUnitPts + (c & 1u) * kChunkPts;
+    return unit(c / kChunksPerUnit) * kUnitPts + (c % kChunksPerUnit) * kChunkPts;
   }
 };
 
@@ -393,9 +396,9 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytes + kQueueBytes +
                                                kHizMaxEntries * 2) + warp * kWarpStages;
 
-  const int64_t c_first = 2 * cm.j0 + (int64_t)blockIdx.x * kRenderWarps + warp;
+  const int64_t c_first = kChunksPerUnit * cm.j0 + (int64_t)blockIdx.x * kRenderWarps + warp;
   const int64_t c_stride = (int64_t)gridDim.x * kRenderWarps;
-  const int64_t n_chunks = 2 * cm.j1;
+  const int64_t n_chunks = kChunksPerUnit * cm.j1;
   if (lane == 0) {
     for (int s = 0; s < kWarpStages; ++s) mbar_init(&full[s], 1);
     fence_mbar_init();
@@ -544,7 +547,7 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
 #endif
 constexpr int kPreStages = NAR_PRE_STAGES;
 constexpr int kPreRingBytes = kRenderWarps * kPreStages * kUnitBytes;
-constexpr int kCandCap = 32 + kChunkPts;  // queue entries per warp
+constexpr int kCandCap = 32 + 64;  // queue entries per warp (drained after every 64 points)
 constexpr int kCandBytes = kRenderWarps * kCandCap * 16;
 constexpr int kPreSmem =
     kPreRingBytes + kCandBytes + kHizMaxEntries * 2 + kRenderWarps * kPreStages * 8 + 128;
