@@ -35,6 +35,7 @@ namespace nar {
 struct DevCam {
   double r[9];
   double c[3];
+  double nc[3];  // -c: p - c evaluated as p + (-c) (bit-identical) with a constant-bank operand
   double f, cx, cy, nr, fr;
   double wd, hd;
   int32_t w, h;
@@ -55,6 +56,7 @@ static DevCam make_devcam(const nar_camera& cam) {
   DevCam k;
   for (int i = 0; i < 9; ++i) k.r[i] = cam.R[i];
   for (int i = 0; i < 3; ++i) k.c[i] = cam.campos[i];
+  for (int i = 0; i < 3; ++i) k.nc[i] = -cam.campos[i];
   k.f = cam.f;
   k.cx = cam.cx;
   k.cy = cam.cy;
@@ -154,9 +156,9 @@ __device__ __forceinline__ bool snap_certain(double t, uint32_t& i) {
 __device__ __forceinline__ void project_fast(float x, float y, float z, const DevCam& k,
                                              uint32_t& ix_out, uint32_t& iy_out, uint32_t& dbits,
                                              bool& hit, bool& uncertain) {
-  const double w0 = __dsub_rn((double)x, k.c[0]);
-  const double w1 = __dsub_rn((double)y, k.c[1]);
-  const double w2 = __dsub_rn((double)z, k.c[2]);
+  const double w0 = __dadd_rn((double)x, k.nc[0]);  // == __dsub_rn(x, c[0]) bit for bit
+  const double w1 = __dadd_rn((double)y, k.nc[1]);
+  const double w2 = __dadd_rn((double)z, k.nc[2]);
   const double uz =
       __dadd_rn(__dadd_rn(__dmul_rn(w0, k.r[6]), __dmul_rn(w1, k.r[7])), __dmul_rn(w2, k.r[8]));
   const bool in_depth = uz > k.nr && uz < k.fr;  // python_impl.py:43 (NaN culled)
@@ -296,8 +298,8 @@ constexpr int kWarpStages = kPtsPerThread >= 4 ? 3 : 6;
 constexpr int kRingBytes = kRenderWarps * kWarpStages * kChunkBytes;
 constexpr int kQueueBytes = kRenderWarps * 32 * 16;
 constexpr int kHizMaxEntries = 34816;                        // 68 KB coarse depth (u16)
-constexpr int kRenderSmem =
-    kRingBytes + kQueueBytes + kHizMaxEntries * 2 + kRenderWarps * kWarpStages * 8 + 128;
+constexpr int kRenderSmem = kRingBytes + kQueueBytes + kHizMaxEntries * 2 +
+                            kRenderWarps * kWarpStages * 8 + kRenderWarps * kWarpStages * 4 + 128;
 constexpr int kUnitPts = 128;  // schedule granularity (tail -> simple kernel)
 constexpr int kChunksPerUnit = kUnitPts / kChunkPts;  // exact-kernel chunks per unit (1 or 2)
 static_assert(kChunksPerUnit * kChunkPts == kUnitPts, "chunk / unit sizes");
@@ -395,6 +397,10 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
   uint16_t* zs = reinterpret_cast<uint16_t*>(smem + kRingBytes + kQueueBytes);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytes + kQueueBytes +
                                                kHizMaxEntries * 2) + warp * kWarpStages;
+  // first point of the chunk in each ring slot, written by the lane that issues its copy
+  // (the chunk -> unit map is computed once per chunk)
+  uint32_t* soff = reinterpret_cast<uint32_t*>(smem + kRingBytes + kQueueBytes + kHizMaxEntries * 2 +
+                                               kRenderWarps * kWarpStages * 8) + warp * kWarpStages;
 
   const int64_t c_first = kChunksPerUnit * cm.j0 + (int64_t)blockIdx.x * kRenderWarps + warp;
   const int64_t c_stride = (int64_t)gridDim.x * kRenderWarps;
@@ -405,9 +411,10 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
     for (int s = 0; s < kWarpStages; ++s) {
       const int64_t c = c_first + (int64_t)s * c_stride;
       if (c < n_chunks) {
+        const uint32_t off = cm.off64((uint32_t)c);
+        soff[s] = off;
         mbar_expect_tx(&full[s], kChunkBytes);
-        bulk_g2s_stream(ring + s * (kChunkPts * 3), pos + (size_t)cm.off64((uint32_t)c) * 3,
-                        kChunkBytes, &full[s], pol);
+        bulk_g2s_stream(ring + s * (kChunkPts * 3), pos + (size_t)off * 3, kChunkBytes, &full[s], pol);
       }
     }
   }
@@ -434,13 +441,18 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
     pcur[j] = 0;
   }
 
-  int k = 0;
+  int s = 0;          // ring slot of this chunk
+  uint32_t ph = 0u;    // its mbarrier phase parity
 #pragma unroll 2
-  for (int64_t c = c_first; c < n_chunks; c += c_stride, ++k) {
-    const int s = k % kWarpStages;
-    mbar_wait(&full[s], (uint32_t)(k / kWarpStages) & 1u);
-    const float* chunk = ring + s * (kChunkPts * 3);
-    const uint32_t cbase = (uint32_t)base_index + cm.off64((uint32_t)c);
+  for (int64_t c = c_first; c < n_chunks; c += c_stride) {
+    mbar_wait(&full[s], ph);
+    const int sc = s;  // this chunk's slot; advance (the kRed path continues early)
+    if (++s == kWarpStages) {
+      s = 0;
+      ph ^= 1u;
+    }
+    const float* chunk = ring + sc * (kChunkPts * 3);
+    const uint32_t cbase = (uint32_t)base_index + soff[sc];
 
     // (1) projections: straight-line, interleavable across the 4 points
     float px[kPtsPerThread], py[kPtsPerThread], pz[kPtsPerThread];
@@ -454,13 +466,14 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
       pz[j] = chunk[3 * p + 2];
     }
     __syncwarp();
-    {  // (3) slot s is consumed: refill it with chunk k + kWarpStages
+    {  // (3) slot sc is consumed: refill it with the chunk kWarpStages steps ahead
       const int64_t cn = c + (int64_t)kWarpStages * c_stride;
       if (lane == 0 && cn < n_chunks) {
+        const uint32_t off = cm.off64((uint32_t)cn);
+        soff[sc] = off;  // read by the lanes after this slot's next full wait
         fence_proxy_async_smem();
-        mbar_expect_tx(&full[s], kChunkBytes);
-        bulk_g2s_stream(ring + s * (kChunkPts * 3), pos + (size_t)cm.off64((uint32_t)cn) * 3,
-                        kChunkBytes, &full[s], pol);
+        mbar_expect_tx(&full[sc], kChunkBytes);
+        bulk_g2s_stream(ring + sc * (kChunkPts * 3), pos + (size_t)off * 3, kChunkBytes, &full[sc], pol);
       }
     }
 #pragma unroll
