@@ -610,6 +610,11 @@ __device__ __forceinline__ void exact_direct(float x, float y, float z, uint32_t
   }
 }
 
+// timing experiments (-DNAR_RENDER_TRACE): per-warp finish time (globaltimer, ns) of
+// the last pre-test launch, to size the tail imbalance of the static unit split
+#ifdef NAR_RENDER_TRACE
+__device__ unsigned long long g_render_trace[148 * kRenderWarps + 1];
+#endif
 template <bool kSigned, int kMode, bool kStats>
 __global__ void __launch_bounds__(kRenderThreads, 1)
     render_pre_kernel(uint64_t* __restrict__ keybuf, const float* __restrict__ pos,
@@ -748,7 +753,21 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
   // warp-uniform total: every candidate was drained in a batch or is in the tail
   if (kStats && lane == 0 && n_drained + qn)
     atomicAdd(hz.stats, (unsigned long long)(n_drained + qn));
+#ifdef NAR_RENDER_TRACE
+  if (lane == 0 && blockIdx.x < 148) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_render_trace[blockIdx.x * kRenderWarps + warp] = t;
+  }
+#endif
 }
+
+#ifdef NAR_RENDER_TRACE
+extern "C" int nar_debug_render_trace(unsigned long long* out, int n) {
+  cudaDeviceSynchronize();
+  return cudaMemcpyFromSymbol(out, g_render_trace, n * 8) == cudaSuccess ? 0 : 2;
+}
+#endif
 
 // Coarse max depth of the current keybuf on the shifted, dilated grid: block
 // (bu, bv) holds ceil(max depth bits / 2^16) over pixels x in
