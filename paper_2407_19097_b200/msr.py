@@ -236,12 +236,14 @@ class DeviceFeatureImage:
     height: int
     channel_names: tuple[str, ...]
     data: object          # torch (data_h, data_w, C) f32 (padded extent)
-    coverage: object      # torch (H, W) u8
-    index_plane: object   # torch (H, W) i64
-    depth: object         # torch (H, W) f32
+    coverage: object      # torch (H, W) u8, or None (not resolved)
+    index_plane: object   # torch (H, W) i64, or None
+    depth: object         # torch (H, W) f32, or None
 
     def to_host(self) -> FeatureImage:
         d = self.data[: self.height, : self.width].cpu().numpy()
+        if self.coverage is None or self.index_plane is None or self.depth is None:
+            raise ValueError("this frame was resolved without its coverage / index / depth planes")
         return FeatureImage(self.width, self.height, self.channel_names, np.ascontiguousarray(d),
                             self.coverage.cpu().numpy(), self.index_plane.cpu().numpy(),
                             self.depth.cpu().numpy())
@@ -367,17 +369,22 @@ class Renderer:
             ev.record(st)
             main.wait_event(ev)
 
-    def alloc_outputs(self, n_channels: int):
+    def alloc_outputs(self, n_channels: int, planes: bool = True):
+        """G-buffer tensors for resolve(out=...).  ``planes=False``: only the (padded)
+        channel data -- the coverage / index / depth planes are then not written
+        (the neural pipeline feeds the CNN from ``data`` alone)."""
         import torch
 
         H, W = self.height, self.width
         m = self.pad_multiple or 1
         ph, pw = H + (-H) % m, W + (-W) % m
         dev = self.device
-        return {"data": torch.empty((ph, pw, n_channels), dtype=torch.float32, device=dev),
-                "coverage": torch.empty((H, W), dtype=torch.uint8, device=dev),
-                "index_plane": torch.empty((H, W), dtype=torch.int64, device=dev),
-                "depth": torch.empty((H, W), dtype=torch.float32, device=dev)}
+        out = {"data": torch.empty((ph, pw, n_channels), dtype=torch.float32, device=dev)}
+        if planes:
+            out.update({"coverage": torch.empty((H, W), dtype=torch.uint8, device=dev),
+                        "index_plane": torch.empty((H, W), dtype=torch.int64, device=dev),
+                        "depth": torch.empty((H, W), dtype=torch.float32, device=dev)})
+        return out
 
     def resolve(self, cloud: DeviceCloud, cam: CameraPose, sel: StreamSelection, out=None,
                 stream=None, clear: bool = True, owner_only: bool = False,
@@ -399,16 +406,17 @@ class Renderer:
         ro = _lib.ResolveOut()
         ro.data = out["data"].data_ptr()
         ro.data_h, ro.data_w = int(out["data"].shape[0]), int(out["data"].shape[1])
-        ro.coverage = out["coverage"].data_ptr()
-        ro.index_plane = out["index_plane"].data_ptr()
-        ro.depth = out["depth"].data_ptr()
+        # planes are optional (nar_resolve_out: NULL = not written)
+        ro.coverage = out["coverage"].data_ptr() if "coverage" in out else None
+        ro.index_plane = out["index_plane"].data_ptr() if "index_plane" in out else None
+        ro.depth = out["depth"].data_ptr() if "depth" in out else None
         ro.owner_only, ro.clear_keybuf = int(owner_only), int(clear)
         s = _selection_struct(sel, cloud)
         segs = _segments_struct(cloud, sel)
         with _lib.on_device(self.device.index):
             self._resolve_call(kc, s, segs, len(cloud.segments), ro, stream, peers, rows)
-        return DeviceFeatureImage(self.width, self.height, names, out["data"], out["coverage"],
-                                  out["index_plane"], out["depth"])
+        return DeviceFeatureImage(self.width, self.height, names, out["data"], out.get("coverage"),
+                                  out.get("index_plane"), out.get("depth"))
 
     def _resolve_call(self, kc, s, segs, nseg, ro, stream, peers, rows) -> None:
         if peers is None:
@@ -470,6 +478,8 @@ def _check_outputs(out: dict, n_channels: int, H: int, W: int) -> None:
     want = {"data": torch.float32, "coverage": torch.uint8, "index_plane": torch.int64,
             "depth": torch.float32}
     for k, dt in want.items():
+        if k not in out and k != "data":  # optional planes (not written)
+            continue
         t = out[k]
         if k != "data" and tuple(t.shape) != (H, W):
             raise ValueError(f"out[{k!r}] must be ({H}, {W}), got {tuple(t.shape)}")

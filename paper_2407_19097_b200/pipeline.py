@@ -89,7 +89,8 @@ class NeuralRenderer:
             raise ValueError(f"selection gives {len(names)} channels, network expects "
                              f"{self.config.input_channels}")
         if self._out is None or self._out["data"].shape[-1] != len(names):
-            self._out = self.renderer.alloc_outputs(len(names))
+            # the CNN input only: the coverage / index / depth planes are not written
+            self._out = self.renderer.alloc_outputs(len(names), planes=False)
             ph, pw = self._out["data"].shape[:2]
             self._rgb = torch.empty((ph, pw, self.config.output_channels), dtype=torch.float32,
                                     device=self.device)

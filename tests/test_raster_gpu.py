@@ -505,3 +505,30 @@ def test_rasterize_output_pool_ownership(cuda):
     assert np.array_equal(view, refs[0]["depth"][:10])
     for img, ref in zip(again, refs[1:]):
         assert np.array_equal(img.data, ref["data"])
+
+
+def test_resolve_without_planes(cuda):
+    """resolve(out=alloc_outputs(C, planes=False)) writes only the CNN input (the neural
+    pipeline's path): the channel data equals a full resolve's, the planes are None and
+    to_host() refuses."""
+    import torch
+
+    from paper_2407_19097_b200.geometry import Intrinsics, PointCloud, Stream, look_at
+    from paper_2407_19097_b200.msr import DeviceCloud, Renderer, StreamSelection
+
+    rng = np.random.default_rng(11)
+    n = 300_000
+    pc = PointCloud(rng.uniform(-1, 1, (n, 3)).astype(np.float32),
+                    [Stream("rgb", "u8", rng.integers(0, 256, (n, 3), dtype=np.uint8))])
+    cloud = DeviceCloud.from_clouds([pc], device=cuda)
+    cam = look_at((0.0, -2.2, 1.0), (0, 0, 0), Intrinsics(width=200, height=136))
+    sel = StreamSelection(rgb=True, depth=True)
+    r = Renderer(200, 136, device=cuda, pad_multiple=16)
+    r.render(cloud, cam)
+    full = r.resolve(cloud, cam, sel, clear=False)
+    lean = r.resolve(cloud, cam, sel, out=r.alloc_outputs(4, planes=False))
+    torch.cuda.synchronize()
+    assert torch.equal(full.data, lean.data)
+    assert lean.coverage is None and lean.index_plane is None and lean.depth is None
+    with pytest.raises(ValueError):
+        lean.to_host()
