@@ -509,7 +509,8 @@ static int upload(nar_unet* n) {
     std::vector<uint16_t> packed;
     {
       const int N = 2 * tc_coutp(l.cout);
-      l.pairs = !n->simt && l.up2 && tc_slide(N) && tc_rows(N, 2) % 2 == 0 &&
+      // sliding layers with an even row tile, and plain layers up to N = 128 (R = 2 or 4)
+      l.pairs = !n->simt && l.up2 && N <= 128 && (!tc_slide(N) || tc_rows(N, 2) % 2 == 0) &&
                 !(getenv("NAR_TC_UP2PAIR") && getenv("NAR_TC_UP2PAIR")[0] == '0');
     }
     tc_pack_weights(l.hf, l.hg, l.ca, l.cb, l.cout, packed, l.pairs);

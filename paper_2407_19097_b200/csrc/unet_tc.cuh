@@ -113,9 +113,9 @@ __host__ __device__ constexpr int tc_r1024(int x) { return (x + 1023) / 1024 * 1
 __host__ __device__ constexpr int tc_a_bytes(int N, int NB) {
   return tc_r1024((tc_rows(N, NB) + 2) * kHaloRowBytes);
 }
-// B slot of a stage: 9 taps x N rows x 32 B; sliding layers reserve 3 kx x 4N rows (the
-// paired up2 chunks, see tc_pack_weights) -- 4/3 of the plain size
-__host__ __device__ constexpr int tc_b_bytes(int N) { return N <= 64 ? 12 * N * 32 : 9 * N * 32; }
+// B slot of a stage: 9 taps x N rows x 32 B; layers that can take paired up2 chunks
+// (N <= 128, see tc_pack_weights) reserve 3 kx x 4N rows -- 4/3 of the plain size
+__host__ __device__ constexpr int tc_b_bytes(int N) { return N <= 128 ? 12 * N * 32 : 9 * N * 32; }
 __host__ __device__ constexpr int tc_b3_bytes(int N) { return 9 * N * 32; }   // a plain chunk
 __host__ __device__ constexpr int tc_b4_bytes(int N) { return 12 * N * 32; }  // a paired chunk
 __host__ __device__ constexpr int tc_stage_bytes(int N, int NB) {
@@ -195,12 +195,15 @@ __host__ __device__ constexpr int tc_coutp(int cout) {
 // 2x): consecutive halo rows 2j-1, 2j read the same low-res row, so their two sliding
 // MMAs merge into one with 4 stacked blocks per kx, [W2; W1+W2; W0+W1; W0] (n' = b*N + n,
 // the sums in f32 before the bf16 rounding) feeding output rows 2j-3 .. 2j: source-A
-// chunks are [chunk q][kx][k8][4N][8] (tc_b4_bytes), source-B chunks as above.
+// chunks are [chunk q][kx][k8][4N][8] (tc_b4_bytes), source-B chunks as above.  Plain
+// layers (N = 96, 128) use the same blocks per output row pair (2p, 2p+1): blocks 1-2
+// [W1+W2 | W0+W1] on low-res row p+1 in one N' = 2N MMA, W0 (block 3) on row p for
+// row 2p and W2 (block 0) on row p+2 for row 2p+1 -- 3 MMAs per kx instead of 6.
 inline void tc_pack_weights(const std::vector<float>& wf, const std::vector<float>& wg, int ca,
                             int cb, int cout, std::vector<uint16_t>& packed, bool pairs = false) {
   const int coutp = tc_coutp(cout), N = 2 * coutp;
   const bool slide = tc_slide(N);
-  pairs = pairs && slide;
+  pairs = pairs && N <= 128;
   const int nqa = (ca + 15) / 16, nqb = (cb + 15) / 16, nq = nqa + nqb, cin = ca + cb;
   const size_t e3 = (size_t)9 * 2 * N * 8;      // elements of a plain chunk
   const size_t q4 = (size_t)3 * 2 * 4 * N * 8;  // ... of a paired chunk
@@ -530,7 +533,7 @@ __global__ void __maxnreg__(96)
         }
         // chunk q's packed weights: paired up2 chunks (4 stacked blocks) first
         constexpr uint32_t B3 = tc_b3_bytes(N), B4 = tc_b4_bytes(N);
-        const bool pq = SLIDE && a.up2pair && in_a;
+        const bool pq = a.up2pair && in_a;
         const uint32_t bbytes = pq ? B4 : B3;
         const size_t boff = a.up2pair ? (in_a ? (size_t)q * B4 : (size_t)nqa * B4 + (size_t)(q - nqa) * B3)
                                       : (size_t)q * B3;
@@ -639,6 +642,29 @@ __global__ void __maxnreg__(96)
               rows(std::integral_constant<int, HM>{}, std::integral_constant<int, R + 2>{});
             } else {
               rows(std::integral_constant<int, 0>{}, std::integral_constant<int, R + 2>{});
+            }
+          } else if (R % 2 == 0 && a.up2pair && up) {
+            // paired up2 chunk, plain layer (tc_pack_weights): per output row pair and kx
+            // one N' = 2N MMA on the shared low-res row and two N MMAs for the outer taps
+#pragma unroll 1
+            for (int kx = 0; kx < 3; ++kx) {
+              const uint32_t bk = sb + kx * (4 * N * 32);  // [k8][4N][8]: LBO = 4N*16
+              const uint64_t b12 = umma_desc(bk + 1 * N * 16, 4 * N * 16, 128);
+              const uint64_t b3 = umma_desc(bk + 3 * N * 16, 4 * N * 16, 128);
+              const uint64_t b0 = umma_desc(bk, 4 * N * 16, 128);
+              const uint32_t ax = sa + kx * 32;
+#pragma unroll
+              for (int pr = 0; pr < R / 2; ++pr) {
+                umma_bf16(dcol + 2 * pr * N, umma_desc_sw32(ax + (pr + 1) * kHaloRowBytes), b12,
+                          umma_idesc_bf16(128, 2 * N), 1u);
+                umma_bf16(dcol + 2 * pr * N, umma_desc_sw32(ax + pr * kHaloRowBytes), b3, IDESC, 1u);
+                umma_bf16(dcol + (2 * pr + 1) * N, umma_desc_sw32(ax + (pr + 2) * kHaloRowBytes), b0,
+                          IDESC, 1u);
+              }
+            }
+            if (last) {  // (decoder layers end with the skip chunk; kept for completeness)
+              for (int g = 0; g < rg; ++g) umma_commit(&tf[g]);
+              slot = rg;
             }
           } else {
 #pragma unroll 1
