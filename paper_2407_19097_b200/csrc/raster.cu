@@ -1050,6 +1050,83 @@ __global__ void __launch_bounds__(256)
   if (sel.coverage_channel && col < P.C) dst[col++] = 1.0f;
 }
 
+// The RGB+D resolve of a local keybuf (no peers), kPix pixels per thread: the keybuf
+// words of all its pixels are read first, then the winners' rgb words are gathered
+// together (kPix independent random reads in flight per thread -- the gathers are
+// what bounds the resolve), then the channels computed and stored.  Same results as
+// resolve_kernel<kSigned, true>.
+template <bool kSigned, int kPix>
+__global__ void __launch_bounds__(256)
+    resolve_rgbd_kernel(uint64_t* __restrict__ keybuf, const ResolveParams P) {
+  const int32_t W = P.cam.w, H = P.cam.h;
+  const int64_t npix_out = (int64_t)P.data_h * P.data_w;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t lid0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const uint64_t empty_raw = kSigned ? (NAR_EMPTY_KEY ^ NAR_SIGN_FLIP) : NAR_EMPTY_KEY;
+  int64_t pix[kPix];
+  uint64_t key[kPix];
+  bool img[kPix];
+#pragma unroll
+  for (int j = 0; j < kPix; ++j) {
+    const int64_t gid = lid0 + j * stride;
+    const int32_t y = (int32_t)(gid / P.data_w);
+    const int32_t x = (int32_t)(gid - (int64_t)y * P.data_w);
+    img[j] = gid < npix_out && y < H && x < W;
+    pix[j] = (int64_t)y * W + x;
+    key[j] = img[j] ? keybuf[pix[j]] : empty_raw;
+  }
+  uint64_t wd[kPix];
+  float dep[kPix];
+  bool hit[kPix];
+#pragma unroll
+  for (int j = 0; j < kPix; ++j) {
+    if (img[j] && P.clear) keybuf[pix[j]] = empty_raw;
+    const uint64_t k = kSigned ? key[j] ^ NAR_SIGN_FLIP : key[j];
+    const bool covered = img[j] && k != NAR_EMPTY_KEY;
+    const int64_t idx = covered ? (int64_t)(k & 0xFFFFFFFFull) : -1;
+    dep[j] = covered ? __uint_as_float((uint32_t)(k >> 32)) : 0.0f;
+    if (img[j]) {
+      if (P.coverage) P.coverage[pix[j]] = covered ? 1 : 0;
+      if (P.index_plane) P.index_plane[pix[j]] = idx;
+      if (P.depth) P.depth[pix[j]] = dep[j];
+    }
+    int s = -1;
+    if (covered)
+      for (int q = 0; q < P.nseg; ++q)
+        if (idx >= P.seg[q].begin && idx < P.seg[q].begin + P.seg[q].count) s = q;
+    hit[j] = s >= 0;
+    wd[j] = 0;
+    if (s >= 0) {  // see resolve_kernel: aligned 8-byte words inside the stream's bytes
+      const uint8_t* c = static_cast<const uint8_t*>(P.seg[s].rgb) + (idx - P.seg[s].begin) * P.sel.rgb_arity;
+      const uintptr_t ca = reinterpret_cast<uintptr_t>(c);
+      const uint32_t off = (uint32_t)(ca & 7u);
+      const uintptr_t lo = reinterpret_cast<uintptr_t>(P.seg[s].rgb);
+      const uintptr_t hi = lo + (uintptr_t)P.seg[s].count * (uintptr_t)P.sel.rgb_arity;
+      if (ca - off >= lo && ca - off + (off > 5u ? 16u : 8u) <= hi) {
+        const unsigned long long* w8 = reinterpret_cast<const unsigned long long*>(ca - off);
+        uint64_t w = __ldg(w8) >> (8u * off);
+        if (off > 5u) w |= __ldg(w8 + 1) << (8u * (8u - off));
+        wd[j] = w;
+      } else {
+        wd[j] = (uint64_t)__ldg(c) | ((uint64_t)__ldg(c + 1) << 8) | ((uint64_t)__ldg(c + 2) << 16);
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kPix; ++j) {
+    const int64_t gid = lid0 + j * stride;
+    if (gid >= npix_out) continue;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);  // padding and background: zeros
+    if (hit[j]) {
+      v.x = __fdiv_rn((float)(uint32_t)(wd[j] & 0xFFu), 255.0f);
+      v.y = __fdiv_rn((float)(uint32_t)((wd[j] >> 8) & 0xFFu), 255.0f);
+      v.z = __fdiv_rn((float)(uint32_t)((wd[j] >> 16) & 0xFFu), 255.0f);
+      v.w = fminf(fmaxf(__fdiv_rn(P.near_f, dep[j]), 0.0f), 1.0f);
+    }
+    *reinterpret_cast<float4*>(P.data + gid * 4) = v;
+  }
+}
+
 // ----------------------------------------------------------------------------
 // host side
 // ----------------------------------------------------------------------------
@@ -1573,6 +1650,22 @@ static int resolve_impl(uint64_t* keybuf_dev, const uint64_t* const* peers, int3
   const int64_t blocks = (n_out + 255) / 256;
   const bool rgbd = C == 4 && sel->rgb && sel->depth && sel->rgb_format == NAR_FMT_U8 &&
                     sel->rgb_arity >= 3 && (reinterpret_cast<uintptr_t>(out->data) & 15) == 0;
+  // RGB+D of a local keybuf: several pixels per thread (NAR_RESOLVE_PIX, default 4)
+  static const int kpix = [] {
+    const char* e = getenv("NAR_RESOLVE_PIX");
+    const int v = e ? atoi(e) : 4;
+    return v == 1 || v == 2 || v == 8 ? v : 4;
+  }();
+  if (rgbd && n_peers == 0 && P.row0 == 0 && P.row1 == P.data_h && P.data && kpix > 1) {
+    const bool sg = key_domain == NAR_KEYS_SIGNED;
+    auto k = kpix == 2 ? (sg ? resolve_rgbd_kernel<true, 2> : resolve_rgbd_kernel<false, 2>)
+           : kpix == 8 ? (sg ? resolve_rgbd_kernel<true, 8> : resolve_rgbd_kernel<false, 8>)
+                       : (sg ? resolve_rgbd_kernel<true, 4> : resolve_rgbd_kernel<false, 4>);
+    const int64_t b = (n_out + 256 * kpix - 1) / (256 * kpix);
+    nar::count_launch();
+    k<<<(unsigned)b, 256, 0, (cudaStream_t)stream>>>(keybuf_dev, P);
+    return check_launch("resolve");
+  }
   auto kern = key_domain == NAR_KEYS_SIGNED
                   ? (rgbd ? resolve_kernel<true, true> : resolve_kernel<true, false>)
                   : (rgbd ? resolve_kernel<false, true> : resolve_kernel<false, false>);
