@@ -903,6 +903,33 @@ __device__ __forceinline__ float stream_value(const void* base, int32_t fmt, int
   return __ldg(static_cast<const float*>(base) + row * arity + col);
 }
 
+// Vel2D channels of one point (velocity.py:26-48 + camera.py:154-166), f64 as the
+// reference (BLAS order: <= 1 f32 ulp): (vx, vy, theta, magnitude), scaled.
+__device__ __forceinline__ void vel2d_channels(const float* pos3, const double v[3],
+                                               const DevCam& k, double scale, float out[4]) {
+  const double w0 = (double)__ldg(pos3) - k.c[0];
+  const double w1 = (double)__ldg(pos3 + 1) - k.c[1];
+  const double w2 = (double)__ldg(pos3 + 2) - k.c[2];
+  const double ux = w0 * k.r[0] + w1 * k.r[1] + w2 * k.r[2];
+  const double uy = w0 * k.r[3] + w1 * k.r[4] + w2 * k.r[5];
+  const double uz = w0 * k.r[6] + w1 * k.r[7] + w2 * k.r[8];
+  const double sc = k.f / (uz * uz);
+  double vp0 = 0.0, vp1 = 0.0;
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const double j0 = (uz * k.r[j] - ux * k.r[6 + j]) * sc;
+    const double j1 = (uz * k.r[3 + j] - uy * k.r[6 + j]) * sc;
+    vp0 += j0 * v[j];
+    vp1 += j1 * v[j];
+  }
+  const double mag = hypot(vp0, vp1);
+  const double theta = mag < 1e-9 ? 0.0 : atan2(-vp1, vp0);
+  out[0] = (float)(vp0 / scale);
+  out[1] = (float)(vp1 / scale);
+  out[2] = (float)theta;
+  out[3] = (float)(mag / scale);
+}
+
 // kRgbd: the selection is exactly rgb (u8, arity >= 3) + depth -- one float4
 // store per pixel.  Otherwise channels are stored straight to global memory as
 // they are produced (no per-thread channel array: dynamic indexing would put
@@ -1009,29 +1036,10 @@ __global__ void __launch_bounds__(256)
       v[c] = (double)stream_value(sg.velocity, sel.vel_format, sel.vel_arity, row, c);
     const double scale = sel.velocity_scale;
     if (sel.vel2d) {
-      // velocity.py:26-48 + camera.py:154-166, f64 (BLAS order: <= 1 f32 ulp)
-      const DevCam& k = P.cam;
-      const double w0 = (double)__ldg(sg.positions + 3 * row) - k.c[0];
-      const double w1 = (double)__ldg(sg.positions + 3 * row + 1) - k.c[1];
-      const double w2 = (double)__ldg(sg.positions + 3 * row + 2) - k.c[2];
-      const double ux = w0 * k.r[0] + w1 * k.r[1] + w2 * k.r[2];
-      const double uy = w0 * k.r[3] + w1 * k.r[4] + w2 * k.r[5];
-      const double uz = w0 * k.r[6] + w1 * k.r[7] + w2 * k.r[8];
-      const double sc = k.f / (uz * uz);
-      double vp0 = 0.0, vp1 = 0.0;
+      float vc[4];
+      vel2d_channels(sg.positions + 3 * row, v, P.cam, scale, vc);
 #pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        const double j0 = (uz * k.r[j] - ux * k.r[6 + j]) * sc;
-        const double j1 = (uz * k.r[3 + j] - uy * k.r[6 + j]) * sc;
-        vp0 += j0 * v[j];
-        vp1 += j1 * v[j];
-      }
-      const double mag = hypot(vp0, vp1);
-      const double theta = mag < 1e-9 ? 0.0 : atan2(-vp1, vp0);
-      dst[col++] = (float)(vp0 / scale);
-      dst[col++] = (float)(vp1 / scale);
-      dst[col++] = (float)theta;
-      dst[col++] = (float)(mag / scale);
+      for (int c = 0; c < 4; ++c) dst[col++] = vc[c];
     }
     if (sel.vel3d) {
       // velocity.py:17-23
@@ -1054,8 +1062,10 @@ __global__ void __launch_bounds__(256)
 // words of all its pixels are read first, then the winners' rgb words are gathered
 // together (kPix independent random reads in flight per thread -- the gathers are
 // what bounds the resolve), then the channels computed and stored.  Same results as
-// resolve_kernel<kSigned, true>.
-template <bool kSigned, int kPix>
+// resolve_kernel<kSigned, true>.  kVel: RGB+D+Vel2D (C = 8, f32 velocity of arity >= 3,
+// C3's selection): the velocity and position of each winner are gathered in the same
+// phase and the channels come from the general kernel's vel2d_channels.
+template <bool kSigned, int kPix, bool kVel = false>
 __global__ void __launch_bounds__(256)
     resolve_rgbd_kernel(uint64_t* __restrict__ keybuf, const ResolveParams P) {
   const int32_t W = P.cam.w, H = P.cam.h;
@@ -1078,6 +1088,8 @@ __global__ void __launch_bounds__(256)
   uint64_t wd[kPix];
   float dep[kPix];
   bool hit[kPix];
+  float vel[kVel ? kPix : 1][3];
+  const float* ppos[kVel ? kPix : 1];
 #pragma unroll
   for (int j = 0; j < kPix; ++j) {
     if (img[j] && P.clear) keybuf[pix[j]] = empty_raw;
@@ -1110,6 +1122,13 @@ __global__ void __launch_bounds__(256)
       } else {
         wd[j] = (uint64_t)__ldg(c) | ((uint64_t)__ldg(c + 1) << 8) | ((uint64_t)__ldg(c + 2) << 16);
       }
+      if constexpr (kVel) {
+        const int64_t row = idx - P.seg[s].begin;
+        const float* vp = static_cast<const float*>(P.seg[s].velocity) + row * P.sel.vel_arity;
+#pragma unroll
+        for (int c2 = 0; c2 < 3; ++c2) vel[j][c2] = __ldg(vp + c2);
+        ppos[j] = P.seg[s].positions + 3 * row;
+      }
     }
   }
 #pragma unroll
@@ -1117,13 +1136,22 @@ __global__ void __launch_bounds__(256)
     const int64_t gid = lid0 + j * stride;
     if (gid >= npix_out) continue;
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);  // padding and background: zeros
+    float4 v2 = make_float4(0.f, 0.f, 0.f, 0.f);
     if (hit[j]) {
       v.x = __fdiv_rn((float)(uint32_t)(wd[j] & 0xFFu), 255.0f);
       v.y = __fdiv_rn((float)(uint32_t)((wd[j] >> 8) & 0xFFu), 255.0f);
       v.z = __fdiv_rn((float)(uint32_t)((wd[j] >> 16) & 0xFFu), 255.0f);
       v.w = fminf(fmaxf(__fdiv_rn(P.near_f, dep[j]), 0.0f), 1.0f);
+      if constexpr (kVel) {
+        const double vd[3] = {(double)vel[j][0], (double)vel[j][1], (double)vel[j][2]};
+        float vc[4];
+        vel2d_channels(ppos[j], vd, P.cam, P.sel.velocity_scale, vc);
+        v2 = make_float4(vc[0], vc[1], vc[2], vc[3]);
+      }
     }
-    *reinterpret_cast<float4*>(P.data + gid * 4) = v;
+    float4* d = reinterpret_cast<float4*>(P.data + gid * (kVel ? 8 : 4));
+    d[0] = v;
+    if constexpr (kVel) d[1] = v2;
   }
 }
 
@@ -1656,6 +1684,20 @@ static int resolve_impl(uint64_t* keybuf_dev, const uint64_t* const* peers, int3
     const int v = e ? atoi(e) : 4;
     return v == 1 || v == 2 || v == 8 ? v : 4;
   }();
+  // RGB+D+Vel2D (C3's selection): the same kernel with the velocity gathers (2 pixels)
+  const bool rgbdv = C == 8 && sel->rgb && sel->depth && sel->vel2d && !sel->vel3d &&
+                     !sel->coverage_channel && sel->n_scalars == 0 &&
+                     sel->rgb_format == NAR_FMT_U8 && sel->rgb_arity >= 3 &&
+                     sel->vel_format == NAR_FMT_F32 && sel->vel_arity >= 3 &&
+                     (reinterpret_cast<uintptr_t>(out->data) & 15) == 0;
+  if (rgbdv && out->data && n_peers == 0 && P.row0 == 0 && P.row1 == P.data_h && kpix > 1) {
+    auto k = key_domain == NAR_KEYS_SIGNED ? resolve_rgbd_kernel<true, 2, true>
+                                           : resolve_rgbd_kernel<false, 2, true>;
+    const int64_t b = (n_out + 511) / 512;
+    nar::count_launch();
+    k<<<(unsigned)b, 256, 0, (cudaStream_t)stream>>>(keybuf_dev, P);
+    return check_launch("resolve");
+  }
   if (rgbd && n_peers == 0 && P.row0 == 0 && P.row1 == P.data_h && P.data && kpix > 1) {
     const bool sg = key_domain == NAR_KEYS_SIGNED;
     auto k = kpix == 2 ? (sg ? resolve_rgbd_kernel<true, 2> : resolve_rgbd_kernel<false, 2>)
