@@ -1069,9 +1069,11 @@ template <bool kSigned, int kPix, bool kVel = false>
 __global__ void __launch_bounds__(256)
     resolve_rgbd_kernel(uint64_t* __restrict__ keybuf, const ResolveParams P) {
   const int32_t W = P.cam.w, H = P.cam.h;
-  const int64_t npix_out = (int64_t)P.data_h * P.data_w;
+  // output rows [row0, row1) (a rank's slice of the peer composite, else all)
+  const int64_t base = (int64_t)P.row0 * P.data_w;
+  const int64_t npix_out = base + (int64_t)(P.row1 - P.row0) * P.data_w;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t lid0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t lid0 = base + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const uint64_t empty_raw = kSigned ? (NAR_EMPTY_KEY ^ NAR_SIGN_FLIP) : NAR_EMPTY_KEY;
   int64_t pix[kPix];
   uint64_t key[kPix];
@@ -1083,7 +1085,18 @@ __global__ void __launch_bounds__(256)
     const int32_t x = (int32_t)(gid - (int64_t)y * P.data_w);
     img[j] = gid < npix_out && y < H && x < W;
     pix[j] = (int64_t)y * W + x;
-    key[j] = img[j] ? keybuf[pix[j]] : empty_raw;
+    if (P.nkeys > 0) {  // composite: min over the ranks' keybufs (unsigned order), raw domain
+      uint64_t m = NAR_EMPTY_KEY;
+      if (img[j])
+        for (int q = 0; q < P.nkeys; ++q) {
+          uint64_t v = __ldcg(reinterpret_cast<const unsigned long long*>(P.keys[q]) + pix[j]);
+          if (kSigned) v ^= NAR_SIGN_FLIP;
+          m = v < m ? v : m;
+        }
+      key[j] = kSigned ? m ^ NAR_SIGN_FLIP : m;
+    } else {
+      key[j] = img[j] ? keybuf[pix[j]] : empty_raw;
+    }
   }
   uint64_t wd[kPix];
   float dep[kPix];
@@ -1092,7 +1105,12 @@ __global__ void __launch_bounds__(256)
   const float* ppos[kVel ? kPix : 1];
 #pragma unroll
   for (int j = 0; j < kPix; ++j) {
-    if (img[j] && P.clear) keybuf[pix[j]] = empty_raw;
+    if (img[j] && P.clear) {
+      if (P.nkeys > 0)
+        for (int q = 0; q < P.nkeys; ++q) const_cast<uint64_t*>(P.keys[q])[pix[j]] = empty_raw;
+      else
+        keybuf[pix[j]] = empty_raw;
+    }
     const uint64_t k = kSigned ? key[j] ^ NAR_SIGN_FLIP : key[j];
     const bool covered = img[j] && k != NAR_EMPTY_KEY;
     const int64_t idx = covered ? (int64_t)(k & 0xFFFFFFFFull) : -1;
@@ -1690,7 +1708,7 @@ static int resolve_impl(uint64_t* keybuf_dev, const uint64_t* const* peers, int3
                      sel->rgb_format == NAR_FMT_U8 && sel->rgb_arity >= 3 &&
                      sel->vel_format == NAR_FMT_F32 && sel->vel_arity >= 3 &&
                      (reinterpret_cast<uintptr_t>(out->data) & 15) == 0;
-  if (rgbdv && out->data && n_peers == 0 && P.row0 == 0 && P.row1 == P.data_h && kpix > 1) {
+  if (rgbdv && out->data && kpix > 1) {
     auto k = key_domain == NAR_KEYS_SIGNED ? resolve_rgbd_kernel<true, 2, true>
                                            : resolve_rgbd_kernel<false, 2, true>;
     const int64_t b = (n_out + 511) / 512;
@@ -1698,7 +1716,7 @@ static int resolve_impl(uint64_t* keybuf_dev, const uint64_t* const* peers, int3
     k<<<(unsigned)b, 256, 0, (cudaStream_t)stream>>>(keybuf_dev, P);
     return check_launch("resolve");
   }
-  if (rgbd && n_peers == 0 && P.row0 == 0 && P.row1 == P.data_h && P.data && kpix > 1) {
+  if (rgbd && P.data && kpix > 1) {
     const bool sg = key_domain == NAR_KEYS_SIGNED;
     auto k = kpix == 2 ? (sg ? resolve_rgbd_kernel<true, 2> : resolve_rgbd_kernel<false, 2>)
            : kpix == 8 ? (sg ? resolve_rgbd_kernel<true, 8> : resolve_rgbd_kernel<false, 8>)
