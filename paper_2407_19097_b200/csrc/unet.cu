@@ -43,9 +43,9 @@ static inline int rup(int x, int m) { return (x + m - 1) / m * m; }
 // bf16 NHWC padded to cp channels (zeros in the padding).
 struct PyrOut {
   __nv_bfloat16* lvl[8];
-  // bf16 levels: row pitch (W >> k) + pad pixels; the pad pixel(s) of every row are
+  // bf16 levels: row pitch (W >> k) + pad pixels; the pad pixels of every row are
   // written as zeros (the conv's overlapping tensor map reads 16 bytes past a row's last
-  // pixel, which must not be the next row's first)
+  // pixel, which must not be the next row's first; 2 keep rows 32-byte aligned)
   int pad;
   float* lvlf[8];  // standalone API (nar_head_pyramid): f32 (H>>k, W>>k, cin) levels instead
 };
@@ -236,9 +236,23 @@ __global__ void __launch_bounds__(128)
         }
         hq[d][j] = j < cin ? acc : 0.f;
       }
-      __nv_bfloat16* o = out.lvl[0] + ((size_t)(y0 + (d >> 1)) * (W + out.pad) + x0 + (d & 1)) * cp;
-      *reinterpret_cast<uint4*>(o) = pack8_bf16(hq[d], cin);
-      if (cp > 8) *reinterpret_cast<uint4*>(o + 8) = make_uint4(0u, 0u, 0u, 0u);
+      if (cp > 8) {
+        __nv_bfloat16* o = out.lvl[0] + ((size_t)(y0 + (d >> 1)) * (W + out.pad) + x0 + (d & 1)) * cp;
+        *reinterpret_cast<uint4*>(o) = pack8_bf16(hq[d], cin);
+        *reinterpret_cast<uint4*>(o + 8) = make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+    if (cp == 8) {  // the quad's two pixels of each row in one 32-byte store (full sectors;
+                    // rows are 32-byte aligned: pitch W + 2)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint4 a = pack8_bf16(hq[2 * h], cin), b = pack8_bf16(hq[2 * h + 1], cin);
+        const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        __nv_bfloat16* o = out.lvl[0] + ((size_t)(y0 + h) * (W + out.pad) + x0) * 8;
+        asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(o), "r"(w[0]),
+                     "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+                     : "memory");
+      }
     }
     float sum[4];  // the reference's 2x2 mean: ((TL + TR) + (BL + BR)) * 0.25
 #pragma unroll
@@ -451,7 +465,7 @@ static Plan make_plan(const nar_unet& n, int H, int W) {
     p.W[k] = W >> k;
     const size_t px = (size_t)p.H[k] * p.W[k];
     const int w = stride_of(n.cfg, k);
-    p.off_pyr16[k] = take((px + p.H[k]) * p.cinp * 2);  // rows of W + 1 pixels (PyrOut::pad)
+    p.off_pyr16[k] = take((px + 2 * p.H[k]) * p.cinp * 2);  // rows of W + 2 pixels (PyrOut::pad)
     // off_x[k] (k >= 1) and the bottleneck off_skip[L-1] feed an up2 and are
     // written wide (H, 2W) on the tensor-core path
     p.off_skip[k] = take(px * w * 2 * (k + 1 == p.L ? 2 : 1));
@@ -793,7 +807,7 @@ int nar_unet_forward(nar_unet* n, const float* in, int32_t H, int32_t W, float* 
     PyrOut po;
     memset(&po, 0, sizeof(po));
     for (int k = 0; k < L; ++k) po.lvl[k] = bf(p.off_pyr16[k]);
-    po.pad = 1;
+    po.pad = 2;  // zero pixels per row: the overlap read needs one, the second keeps rows 32-B aligned
     const size_t sm = (size_t)T * T * cin * 4;
     if (T * T > 256) return set_error(NAR_ERR_CONFIG, "at most 5 pyramid levels supported");
     auto kern = cin <= 4 ? head_pyramid_kernel<4>
@@ -817,11 +831,11 @@ int nar_unet_forward(nar_unet* n, const float* in, int32_t H, int32_t W, float* 
     Layer& lb = n->layers[li++];
     if (k == 0) {
       rc = run_conv(n, la, bf(p.off_pyr16[0]), p.cinp, 0, nullptr, 0, p.H[0], p.W[0],
-                    bf(p.off_tmp[0]), st, nullptr, nullptr, nullptr, 0, p.W[0] + 1);
+                    bf(p.off_tmp[0]), st, nullptr, nullptr, nullptr, 0, p.W[0] + 2);
     } else {
       rc = run_conv(n, la, bf(p.off_pool[k - 1]), stride_of(n->cfg, k - 1), 0,
                     bf(p.off_pyr16[k]), p.cinp, p.H[k], p.W[k], bf(p.off_tmp[k]), st, nullptr,
-                    nullptr, nullptr, 0, 0, p.W[k] + 1);
+                    nullptr, nullptr, 0, 0, p.W[k] + 2);
     }
     if (rc) return rc;
     const bool last = L == 1;

@@ -61,7 +61,7 @@ struct ConvArgs {
   int H, W;                    // output (and src_b) resolution
   int out_wide;                // tensor-core path: write out as (H, 2W), each pixel twice
   int a_pitch, b_pitch;        // row pitch of src_a / src_b in pixels (0: W); pyramid
-                               // levels have W + 1 (a zero pad pixel per row)
+                               // levels have W + 2 (zero pad pixels per row)
   int cout, cout_stride;       // real output channels, output channel stride
   const float* wf32;           // SIMT path: HWIO f32
   const float* wg32;
@@ -993,7 +993,7 @@ static int tc_make_map(CUtensorMap* m, const void* base, int cs, int w, int h, i
   // cs = 8 (a pyramid level): the 16-channel box still reads 32 bytes per pixel --
   // channels 8..15 overlap the next pixel (their weights are zero), so every box row
   // is in bounds (an out-of-bounds channel half makes TMA ~20 % slower); the last
-  // pixel of a row reads the row's zero pad pixel (pitch = W + 1), never the next row
+  // pixel of a row reads the row's zero pad pixel (pitch = W + 2), never the next row
   cuuint64_t dims[3] = {(cuuint64_t)(cs < bc ? bc : cs), (cuuint64_t)w, (cuuint64_t)h};
   cuuint64_t strides[2] = {(cuuint64_t)cs * 2, (cuuint64_t)cs * 2 * (cuuint64_t)(pitch ? pitch : w)};
   cuuint32_t box[3] = {(cuuint32_t)bc, (cuuint32_t)bw, (cuuint32_t)bh};
