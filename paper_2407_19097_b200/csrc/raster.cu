@@ -833,6 +833,62 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// The same coarse table with coalesced reads (even W): a CTA takes one block row by and
+// 256 consecutive 2-pixel chunks of it -- every load instruction of a warp covers 512
+// contiguous bytes of one image row (hiz_kernel gives each thread a row of one block, so
+// its warp touches 32 rows per load).  Each thread keeps the max depth bits of its chunk
+// over the window rows [by S - 2, by S + S); the chunk maxima go through shared memory
+// and block bx takes chunks [bx S/2 - 1, bx S/2 + S/2 - 1] (its dilated window).  CTA x
+// covers kNb = 255 / (S/2) blocks; the edge column / row get 0 as in hiz_kernel.
+template <bool kSigned, int S>
+__global__ void __launch_bounds__(256)
+    hiz_rows_kernel(const uint64_t* __restrict__ keybuf, int W, int H, int zw, int zh,
+                    uint16_t* __restrict__ zmax) {
+  constexpr int kHalf = S / 2, kNb = 255 / kHalf;
+  __shared__ uint32_t cm[256];
+  const int by = blockIdx.y;
+  const int b0 = blockIdx.x * kNb;
+  const int t = threadIdx.x;
+  uint32_t m = 0;
+  if (by < zh - 1) {
+    const int c = b0 * kHalf - 1 + t;  // chunk: pixels 2c, 2c + 1
+    if (c >= 0 && 2 * c + 1 < W && t <= kNb * kHalf) {
+      const int ya = max(by * S - 2, 0), yb = min(by * S + S, H);
+      const ulonglong2* p = reinterpret_cast<const ulonglong2*>(keybuf) + c;
+      const int rs = W / 2;  // row stride in chunks
+      int y = ya;
+      for (; y + 4 <= yb; y += 4) {  // 4 rows in flight
+        ulonglong2 v[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[i] = __ldcg(p + (size_t)(y + i) * rs);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint64_t a = kSigned ? v[i].x ^ NAR_SIGN_FLIP : v[i].x;
+          const uint64_t b = kSigned ? v[i].y ^ NAR_SIGN_FLIP : v[i].y;
+          m = max(m, max((uint32_t)(a >> 32), (uint32_t)(b >> 32)));
+        }
+      }
+      for (; y < yb; ++y) {
+        const ulonglong2 v = __ldcg(p + (size_t)y * rs);
+        const uint64_t a = kSigned ? v.x ^ NAR_SIGN_FLIP : v.x;
+        const uint64_t b = kSigned ? v.y ^ NAR_SIGN_FLIP : v.y;
+        m = max(m, max((uint32_t)(a >> 32), (uint32_t)(b >> 32)));
+      }
+    }
+  }
+  cm[t] = m;
+  __syncthreads();
+  const int bx = b0 + t;
+  if (t < kNb && bx < zw) {
+    uint32_t mm = 0;
+#pragma unroll
+    for (int i = 0; i <= kHalf; ++i) mm = max(mm, cm[t * kHalf + i]);
+    const bool edge = bx == zw - 1 || by == zh - 1;
+    const uint32_t q = (mm >> 16) + ((mm & 0xFFFFu) != 0u);  // round up: conservative
+    zmax[(size_t)by * zw + bx] = edge ? (uint16_t)0 : (uint16_t)(q > 0xFFFFu ? 0xFFFFu : q);
+  }
+}
+
 static void hiz_geometry(int W, int H, int& shift, int& zw, int& zh) {
   shift = 3;  // <= 5 (one warp per coarse block row set) for any image < 2^32 pixels
   for (;;) {
@@ -1266,6 +1322,20 @@ static int launch_render(uint64_t* keybuf, const float* pos, int64_t n, uint64_t
                  : (shift == 3 ? hiz_kernel<false, 5> : shift == 4 ? hiz_kernel<false, 9>
                                                       : hiz_kernel<false, 17>);
     nar::count_launch();
+    static const bool rows = [] {  // NAR_HIZ_ROWS=0: the one-row-per-thread kernel
+      const char* e = getenv("NAR_HIZ_ROWS");
+      return !(e && e[0] == '0');
+    }();
+    if (rows && (cam.w & 1) == 0 && shift >= 3 && shift <= 5) {
+      const int half = 1 << (shift - 1), nb = 255 / half;
+      const dim3 grid((unsigned)((zw + nb - 1) / nb), (unsigned)zh);
+      auto kr = sgn ? (shift == 3 ? hiz_rows_kernel<true, 8> : shift == 4 ? hiz_rows_kernel<true, 16>
+                                                            : hiz_rows_kernel<true, 32>)
+                    : (shift == 3 ? hiz_rows_kernel<false, 8> : shift == 4 ? hiz_rows_kernel<false, 16>
+                                                             : hiz_rows_kernel<false, 32>);
+      kr<<<grid, 256, 0, st>>>(keybuf, cam.w, cam.h, zw, zh, zmax);
+      return;
+    }
     k<<<g, 256, 0, st>>>(keybuf, cam.w, cam.h, shift, zw, zh, zmax);
   };
   if ((reinterpret_cast<uintptr_t>(pos) & 15) == 0) {
