@@ -1322,10 +1322,8 @@ static int launch_render(uint64_t* keybuf, const float* pos, int64_t n, uint64_t
                  : (shift == 3 ? hiz_kernel<false, 5> : shift == 4 ? hiz_kernel<false, 9>
                                                       : hiz_kernel<false, 17>);
     nar::count_launch();
-    static const bool rows = [] {  // NAR_HIZ_ROWS=0: the one-row-per-thread kernel
-      const char* e = getenv("NAR_HIZ_ROWS");
-      return !(e && e[0] == '0');
-    }();
+    const char* hr = getenv("NAR_HIZ_ROWS");  // 0: the one-row-per-thread kernel (per render)
+    const bool rows = !(hr && hr[0] == '0');
     if (rows && (cam.w & 1) == 0 && shift >= 3 && shift <= 5) {
       const int half = 1 << (shift - 1), nb = 255 / half;
       const dim3 grid((unsigned)((zw + nb - 1) / nb), (unsigned)zh);

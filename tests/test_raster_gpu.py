@@ -532,3 +532,30 @@ def test_resolve_without_planes(cuda):
     assert lean.coverage is None and lean.index_plane is None and lean.depth is None
     with pytest.raises(ValueError):
         lean.to_host()
+
+
+@pytest.mark.parametrize("W,H", [(640, 360), (1920, 1080), (3840, 2160)])
+def test_hiz_refresh_kernels_agree(cuda, monkeypatch, W, H):
+    """The coalesced Hi-Z refresh (hiz_rows_kernel, default for even widths) writes the
+    same coarse table as the one-row-per-thread kernel (NAR_HIZ_ROWS=0) -- compared
+    after the same forced multi-pass render (the table then holds the last refresh)."""
+    import torch
+
+    from paper_2407_19097_b200.geometry import Intrinsics, look_at
+    from paper_2407_19097_b200.msr import DeviceCloud, Renderer
+
+    monkeypatch.setenv("NAR_RENDER_PASS_UNITS", "200")
+    rng = np.random.default_rng(W)
+    pos = torch.from_numpy(rng.uniform(-1, 1, (2_000_000, 3)).astype(np.float32)).to(cuda)
+    cam = look_at((0.0, -2.2, 1.0), (0, 0, 0), Intrinsics(width=W, height=H))
+    tables, keys = [], []
+    for mode in ("0", "1"):
+        monkeypatch.setenv("NAR_HIZ_ROWS", mode)
+        r = Renderer(W, H, device=cuda)
+        r.hiz.zero_()  # the scratch tail beyond the table stays untouched
+        r.render(DeviceCloud.from_tensors(pos), cam)
+        torch.cuda.synchronize()
+        tables.append(r.hiz.clone())
+        keys.append(r.keys())
+    assert np.array_equal(keys[0], keys[1])
+    assert torch.equal(tables[0], tables[1])
