@@ -544,7 +544,8 @@ __global__ void __maxnreg__(96)
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------ MMA issuer -----------------------------
-    // epilogue row slots (see tc_epi_rgroups): signalled one by one in the last chunk
+    // epilogue row slots (see tc_epi_rgroups): signalled in the last chunk -- sliding layers
+    // with one commit per completion group (tc_epi_signal), plain layers row by row
     const int rstep = (!kHead && a.pool_out != nullptr) ? 2 : 1;
     const int units = R / rstep, rg = tc_epi_rgroups(units);
     int it = 0, tl = 0;
