@@ -1786,10 +1786,12 @@ static int resolve_impl(uint64_t* keybuf_dev, const uint64_t* const* peers, int3
   }
   if (rgbd && P.data && kpix > 1) {
     const bool sg = key_domain == NAR_KEYS_SIGNED;
-    auto k = kpix == 2 ? (sg ? resolve_rgbd_kernel<true, 2> : resolve_rgbd_kernel<false, 2>)
-           : kpix == 8 ? (sg ? resolve_rgbd_kernel<true, 8> : resolve_rgbd_kernel<false, 8>)
-                       : (sg ? resolve_rgbd_kernel<true, 4> : resolve_rgbd_kernel<false, 4>);
-    const int64_t b = (n_out + 256 * kpix - 1) / (256 * kpix);
+    // small frames (< 1 Mpixel) have too few threads to fill the GPU at 4 pixels each
+    const int kp = n_out < (1 << 20) && kpix > 2 ? 2 : kpix;
+    auto k = kp == 2 ? (sg ? resolve_rgbd_kernel<true, 2> : resolve_rgbd_kernel<false, 2>)
+           : kp == 8 ? (sg ? resolve_rgbd_kernel<true, 8> : resolve_rgbd_kernel<false, 8>)
+                     : (sg ? resolve_rgbd_kernel<true, 4> : resolve_rgbd_kernel<false, 4>);
+    const int64_t b = (n_out + 256 * kp - 1) / (256 * kp);
     nar::count_launch();
     k<<<(unsigned)b, 256, 0, (cudaStream_t)stream>>>(keybuf_dev, P);
     return check_launch("resolve");
