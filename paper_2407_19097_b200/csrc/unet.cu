@@ -194,78 +194,100 @@ __device__ __forceinline__ uint4 pack8_bf16(const float* v4, int cin) {
   return pk;
 }
 
-__global__ void __launch_bounds__(128)
+// 8 bf16 of a pixel's 8 head outputs
+__device__ __forceinline__ uint4 pack8f_bf16(const float* v8) {
+  uint4 pk;
+#pragma unroll
+  for (int e = 0; e < 8; e += 2) {
+    __nv_bfloat162 h2 = __floats2bfloat162_rn(v8[e], v8[e + 1]);
+    (&pk.x)[e / 2] = *reinterpret_cast<uint32_t*>(&h2);
+  }
+  return pk;
+}
+
+// CIN = 4 or 8 input channels (the pyramid stride cp is 8): 32 x 32 pixels per CTA,
+// 2x2 quads per thread (two with 4 channels, 128 threads; one with 8, 256 threads),
+// all of a thread's float4 loads issued before any is used; level 0 written as one
+// 32-byte store per quad row (rows 32-byte aligned: pitch W + 2), level 1 from
+// registers, levels 2-4 through shared memory.
+template <int CIN>
+__global__ void __launch_bounds__(CIN == 4 ? 128 : 256)
     head_pyramid_quad_kernel(const float* __restrict__ x, int H, int W, int cin, int cp,
                              const float* __restrict__ hw, const float* __restrict__ hb,
                              int use_head, int levels, PyrOut out) {
-  __shared__ float tile[16 * 16 * 4];  // level-1 values of the CTA (16 x 16 x 4)
+  constexpr int QPT = CIN == 4 ? 2 : 1;   // quads per thread
+  constexpr int QROWS = 16 / QPT;         // quad rows per pass of the CTA's threads
+  constexpr int NV = CIN / 4;             // float4 per pixel
+  __shared__ float tile[16 * 16 * CIN];  // level-1 values of the CTA (16 x 16 x CIN)
   // let the first conv (a programmatic dependent) get scheduled early
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  // 128 threads, two 2x2 quads each (quad rows qy and qy + 8 of the 32 x 32 tile):
-  // all eight float4 loads are issued before any is used
   const int t = threadIdx.x;
   const int qx = t & 15, qy0 = t >> 4;
-  float wgt[16], bias[4];
+  float wgt[CIN * CIN], bias[CIN];
 #pragma unroll
-  for (int i = 0; i < 16; ++i) wgt[i] = (use_head && i / 4 < cin && i % 4 < cin) ? __ldg(hw + (i / 4) * cin + (i % 4)) : 0.f;
+  for (int i = 0; i < CIN * CIN; ++i)
+    wgt[i] = (use_head && i / CIN < cin && i % CIN < cin) ? __ldg(hw + (i / CIN) * cin + (i % CIN)) : 0.f;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) bias[j] = (use_head && j < cin) ? __ldg(hb + j) : 0.f;
-  float4 in[2][4];
+  for (int j = 0; j < CIN; ++j) bias[j] = (use_head && j < cin) ? __ldg(hb + j) : 0.f;
+  float4 in[QPT][4][NV];
 #pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    const int y0 = blockIdx.y * 32 + 2 * (qy0 + 8 * u), x0 = blockIdx.x * 32 + 2 * qx;
+  for (int u = 0; u < QPT; ++u) {
+    const int y0 = blockIdx.y * 32 + 2 * (qy0 + QROWS * u), x0 = blockIdx.x * 32 + 2 * qx;
 #pragma unroll
     for (int d = 0; d < 4; ++d)
-      in[u][d] = __ldg(reinterpret_cast<const float4*>(x + ((size_t)(y0 + (d >> 1)) * W + x0 + (d & 1)) * 4));
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+        in[u][d][v] = __ldg(reinterpret_cast<const float4*>(
+                              x + ((size_t)(y0 + (d >> 1)) * W + x0 + (d & 1)) * CIN) + v);
   }
 #pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    const int qy = qy0 + 8 * u;
+  for (int u = 0; u < QPT; ++u) {
+    const int qy = qy0 + QROWS * u;
     const int y0 = blockIdx.y * 32 + 2 * qy, x0 = blockIdx.x * 32 + 2 * qx;
-    float hq[4][4];  // head outputs of the quad: TL, TR, BL, BR
+    float hq[4][CIN];  // head outputs of the quad: TL, TR, BL, BR
 #pragma unroll
     for (int d = 0; d < 4; ++d) {
-      const float v[4] = {in[u][d].x, in[u][d].y, in[u][d].z, in[u][d].w};
+      float v[CIN];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int q = 0; q < NV; ++q) {
+        v[4 * q] = in[u][d][q].x;
+        v[4 * q + 1] = in[u][d][q].y;
+        v[4 * q + 2] = in[u][d][q].z;
+        v[4 * q + 3] = in[u][d][q].w;
+      }
+#pragma unroll
+      for (int j = 0; j < CIN; ++j) {
         float acc = v[j];
         if (use_head) {
           acc = bias[j];
 #pragma unroll
-          for (int c = 0; c < 4; ++c) acc = fmaf(v[c], wgt[c * 4 + j], acc);
+          for (int c = 0; c < CIN; ++c) acc = fmaf(v[c], wgt[c * CIN + j], acc);
         }
         hq[d][j] = j < cin ? acc : 0.f;
       }
-      if (cp > 8) {
-        __nv_bfloat16* o = out.lvl[0] + ((size_t)(y0 + (d >> 1)) * (W + out.pad) + x0 + (d & 1)) * cp;
-        *reinterpret_cast<uint4*>(o) = pack8_bf16(hq[d], cin);
-        *reinterpret_cast<uint4*>(o + 8) = make_uint4(0u, 0u, 0u, 0u);
-      }
     }
-    if (cp == 8) {  // the quad's two pixels of each row in one 32-byte store (full sectors;
-                    // rows are 32-byte aligned: pitch W + 2)
+    // the quad's two pixels of each row in one 32-byte store (full sectors)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint4 a = pack8_bf16(hq[2 * h], cin), b = pack8_bf16(hq[2 * h + 1], cin);
-        const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-        __nv_bfloat16* o = out.lvl[0] + ((size_t)(y0 + h) * (W + out.pad) + x0) * 8;
-        asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(o), "r"(w[0]),
-                     "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
-                     : "memory");
-      }
+    for (int h = 0; h < 2; ++h) {
+      const uint4 a = CIN == 4 ? pack8_bf16(hq[2 * h], cin) : pack8f_bf16(hq[2 * h]);
+      const uint4 b = CIN == 4 ? pack8_bf16(hq[2 * h + 1], cin) : pack8f_bf16(hq[2 * h + 1]);
+      const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      __nv_bfloat16* o = out.lvl[0] + ((size_t)(y0 + h) * (W + out.pad) + x0) * 8;
+      asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(o), "r"(w[0]),
+                   "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+                   : "memory");
     }
-    float sum[4];  // the reference's 2x2 mean: ((TL + TR) + (BL + BR)) * 0.25
+    float sum[CIN];  // the reference's 2x2 mean: ((TL + TR) + (BL + BR)) * 0.25
 #pragma unroll
-    for (int j = 0; j < 4; ++j) sum[j] = ((hq[0][j] + hq[1][j]) + (hq[2][j] + hq[3][j])) * 0.25f;
+    for (int j = 0; j < CIN; ++j) sum[j] = ((hq[0][j] + hq[1][j]) + (hq[2][j] + hq[3][j])) * 0.25f;
     // level 1 from registers
     if (levels > 1) {
       const int W1 = W >> 1;
-      __nv_bfloat16* o = out.lvl[1] + ((size_t)(blockIdx.y * 16 + qy) * (W1 + out.pad) + blockIdx.x * 16 + qx) * cp;
-      *reinterpret_cast<uint4*>(o) = pack8_bf16(sum, cin);
-      if (cp > 8) *reinterpret_cast<uint4*>(o + 8) = make_uint4(0u, 0u, 0u, 0u);
+      __nv_bfloat16* o = out.lvl[1] + ((size_t)(blockIdx.y * 16 + qy) * (W1 + out.pad) + blockIdx.x * 16 + qx) * 8;
+      *reinterpret_cast<uint4*>(o) = CIN == 4 ? pack8_bf16(sum, cin) : pack8f_bf16(sum);
     }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) tile[(qy * 16 + qx) * 4 + j] = sum[j];
+    for (int j = 0; j < CIN; ++j) tile[(qy * 16 + qx) * CIN + j] = sum[j];
   }
   __syncthreads();
   int side = 16;
@@ -273,23 +295,24 @@ __global__ void __launch_bounds__(128)
   for (int k = 2; k < 5; ++k) {
     if (k >= levels) break;
     const int ns = side >> 1;
-    float m[4] = {0.f, 0.f, 0.f, 0.f};
+    float m[CIN];
+#pragma unroll
+    for (int c = 0; c < CIN; ++c) m[c] = 0.f;
     const bool act = t < ns * ns;
     const int py = act ? t / ns : 0, pxx = act ? t % ns : 0;
     if (act) {
-      const float* a0 = tile + ((2 * py) * side + 2 * pxx) * 4;
+      const float* a0 = tile + ((2 * py) * side + 2 * pxx) * CIN;
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
-        m[c] = ((a0[c] + a0[4 + c]) + (a0[side * 4 + c] + a0[side * 4 + 4 + c])) * 0.25f;
+      for (int c = 0; c < CIN; ++c)
+        m[c] = ((a0[c] + a0[CIN + c]) + (a0[side * CIN + c] + a0[side * CIN + CIN + c])) * 0.25f;
     }
     __syncthreads();
     if (act) {
 #pragma unroll
-      for (int c = 0; c < 4; ++c) tile[t * 4 + c] = m[c];
+      for (int c = 0; c < CIN; ++c) tile[t * CIN + c] = m[c];
       const int Wk = W >> k;
-      __nv_bfloat16* o = out.lvl[k] + ((size_t)(blockIdx.y * ns + py) * (Wk + out.pad) + blockIdx.x * ns + pxx) * cp;
-      *reinterpret_cast<uint4*>(o) = pack8_bf16(m, cin);
-      if (cp > 8) *reinterpret_cast<uint4*>(o + 8) = make_uint4(0u, 0u, 0u, 0u);
+      __nv_bfloat16* o = out.lvl[k] + ((size_t)(blockIdx.y * ns + py) * (Wk + out.pad) + blockIdx.x * ns + pxx) * 8;
+      *reinterpret_cast<uint4*>(o) = CIN == 4 ? pack8_bf16(m, cin) : pack8f_bf16(m);
     }
     __syncthreads();
     side = ns;
@@ -815,8 +838,13 @@ int nar_unet_forward(nar_unet* n, const float* in, int32_t H, int32_t W, float* 
     const bool aligned = (reinterpret_cast<uintptr_t>(in) & 15) == 0;
     if (cin == 4 && !aligned) kern = head_pyramid_kernel<8>;  // no float4 loads
     nar::count_launch();
-    if (cin == 4 && aligned && L <= 5 && W % 32 == 0 && H % 32 == 0)
-      head_pyramid_quad_kernel<<<dim3(W / 32, H / 32), 128, 0, st>>>(
+    const bool quad = (cin == 4 || cin == 8) && p.cinp == 8 && aligned && L <= 5 &&
+                      W % 32 == 0 && H % 32 == 0;
+    if (quad && cin == 4)
+      head_pyramid_quad_kernel<4><<<dim3(W / 32, H / 32), 128, 0, st>>>(
+          in, H, W, cin, p.cinp, n->d_head_w, n->d_head_b, n->cfg.use_descriptor_head, L, po);
+    else if (quad)
+      head_pyramid_quad_kernel<8><<<dim3(W / 32, H / 32), 256, 0, st>>>(
           in, H, W, cin, p.cinp, n->d_head_w, n->d_head_b, n->cfg.use_descriptor_head, L, po);
     else
       kern<<<dim3(W / T, H / T), T * T, sm, st>>>(in, H, W, cin, p.cinp, n->d_head_w,

@@ -335,3 +335,19 @@ def test_forward_with_poisoned_workspace(cuda):
     assert np.isfinite(y).all()
     ref = oracle.forward(x[None], params, cfg)[0]
     assert oracle.psnr(y, ref) >= PSNR_MIN
+
+
+@pytest.mark.parametrize("cin", [4, 8])
+def test_forward_quad_head_pyramid(cuda, cin):
+    """Frames whose sides are multiples of 32 take the quad head/pyramid kernel (4 or 8
+    input channels: C2/C4's RGB+D, C3's RGB+D+Vel2D); the full forward matches the f32
+    oracle."""
+    from paper_2407_19097_b200.neural import UNetConfig, forward, init_params
+
+    cfg = UNetConfig(input_channels=cin, init_seed=cin)
+    params = init_params(cfg)
+    x = np.random.default_rng(cin).uniform(-1, 1, (1, 128, 192, cin)).astype(np.float32)
+    y = forward(x, params, cfg)
+    ref = oracle.forward(x, params, cfg)
+    assert oracle.psnr(y, ref) >= PSNR_MIN
+    assert np.abs(y - ref).max() <= MAX_ABS
