@@ -826,6 +826,14 @@ def main_ours(args):
                     "unet_ms_median": un,
                     "unet_tflops": (413.7e9 / 1e12 / (un * 1e-3)) if len(names) == 4 else None,
                     "frames": kp, "api": "paper_2407_19097_b200.pipeline.NeuralRenderer.frame"}
+        # the U-Net against the tensor roofline (413.7 / 423.1 GFLOP at 1920x1088
+        # for 4 / 8 input channels; burst bf16 peak: the U-Net is timed per frame, not for seconds)
+        gflop = {4: 413.7, 8: 423.1}.get(len(names))
+        if gflop and (pw, ph) == (1920, 1088):
+            tf = gflop / (un * 1e-3) / 1e3
+            pipeline["unet_roofline"] = {"bound": "tensor", "achieved": tf,
+                                         "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                                         "frac": tf / peaks["bf16_tflops"], "gflop": gflop}
         del nr
 
     # ---- the same frame on the Morton-ordered cloud ------------
