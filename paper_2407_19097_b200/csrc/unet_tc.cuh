@@ -292,6 +292,13 @@ __host__ __device__ constexpr uint32_t umma_idesc_bf16(int M, int N) {
          ((uint32_t)(M >> 4) << 24);
 }
 
+// descriptor + byte offset: the start-address field is addr >> 4 in bits [0,14),
+// and every shared-memory address < 256 KB fits it, so adding offset >> 4 never
+// carries out of the field (one integer add instead of re-encoding the address)
+__device__ __forceinline__ uint64_t desc_add(uint64_t d, uint32_t bytes) {
+  return d + (uint64_t)(bytes >> 4);
+}
+
 __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
                                           uint32_t idesc, uint32_t accum) {
   asm volatile(
@@ -384,6 +391,11 @@ __device__ __forceinline__ float ex2_approx(float x) {
 // sigmoid(g) = (1 + tanh(g/2))/2, the gate is e + e*tanh(gh) -- 2 MUFU + 4
 // FMA-pipe ops per output.
 __device__ __forceinline__ float gate_h(float fh, float gh) {
+#if defined(NAR_TC_GATE_MUFU0)  // timing experiments only (wrong numerics)
+  return fmaf(fh, gh, fh);
+#elif defined(NAR_TC_GATE_MUFU1)
+  return fmaf(fh, tanh_approx(gh), fh);
+#endif
   const float ex = ex2_approx(fh * 2.88539008177792681f);  // 2^(2 fh log2 e) = e^f
   const float e = fh > 0.0f ? fh : fmaf(0.5f, ex, -0.5f);
   const float t = tanh_approx(gh);
@@ -594,15 +606,17 @@ __global__ void __maxnreg__(96)
               constexpr int H0 = decltype(h0c)::value, H1 = decltype(h1c)::value;
 #pragma unroll 1
               for (int kx = 0; kx < 3; ++kx) {
-                const uint32_t bk = sb + kx * (3 * N * 32);  // [k8][3N][8]: LBO = 3N*16
+                // [k8][3N][8]: LBO = 3N*16; descriptors encoded once, offsets added
+                const uint64_t bk = umma_desc(sb + kx * (3 * N * 32), 3 * N * 16, 128);
+                const uint64_t ak = umma_desc_sw32(sa + kx * 32);
 #pragma unroll
                 for (int h = H0; h < H1; ++h) {
                   const int kymax = h < 2 ? h : 2;
                   const int kymin = h - (R - 1) > 0 ? h - (R - 1) : 0;
                   const int nb = kymax - kymin + 1;
-                  const uint64_t bdesc = umma_desc(bk + (2 - kymax) * N * 16, 3 * N * 16, 128);
+                  const uint64_t bdesc = desc_add(bk, (2 - kymax) * N * 16);
                   const uint64_t adesc =
-                      umma_desc_sw32(sa + ((h + par) >> sh) * kHaloRowBytes + kx * 32);
+                      desc_add(ak, (sh ? ((h + par) >> 1) : h) * kHaloRowBytes);
                   umma_bf16(dcol + (h - kymax) * N, adesc, bdesc, umma_idesc_bf16(128, nb * N), 1u);
                 }
               }
@@ -668,14 +682,16 @@ __global__ void __maxnreg__(96)
               slot = rg;
             }
           } else {
+            const uint64_t b0 = umma_desc(sb, N * 16, 128);
+            const uint64_t a0 = umma_desc_sw32(sa);
 #pragma unroll 1
             for (int r = 0; r < R; ++r) {
 #pragma unroll
               for (int tap = 0; tap < 9; ++tap) {
                 const int ky = tap / 3, kx = tap % 3;
-                const uint64_t bdesc = umma_desc(sb + tap * (N * 32), N * 16, 128);
+                const uint64_t bdesc = desc_add(b0, tap * (N * 32));
                 const uint64_t adesc =
-                    umma_desc_sw32(sa + ((r + ky + par) >> sh) * kHaloRowBytes + kx * 32);
+                    desc_add(a0, ((r + ky + par) >> sh) * kHaloRowBytes + kx * 32);
                 umma_bf16(dcol + r * N, adesc, bdesc, IDESC, 1u);
               }
               if (last)
