@@ -266,14 +266,17 @@ __device__ __forceinline__ void red_key(uint64_t* keybuf, uint32_t pix, uint64_t
 
 // Atomic half of fold_key, given a previously loaded current value.
 template <bool kSigned>
-__device__ __forceinline__ void fold_loaded(uint64_t* keybuf, uint32_t pix, uint64_t key,
+__device__ __forceinline__ bool fold_loaded(uint64_t* keybuf, uint32_t pix, uint64_t key,
                                             uint64_t cur) {
   if (kSigned) {
     const long long k = (long long)(key ^ NAR_SIGN_FLIP);
-    if (k < (long long)cur) atomicMin(reinterpret_cast<long long*>(keybuf) + pix, k);
+    const bool win = k < (long long)cur;
+    if (win) atomicMin(reinterpret_cast<long long*>(keybuf) + pix, k);
+    return win;
   } else {
-    if (key < cur) atomicMin(reinterpret_cast<unsigned long long*>(keybuf) + pix,
-                             (unsigned long long)key);
+    const bool win = key < cur;
+    if (win) atomicMin(reinterpret_cast<unsigned long long*>(keybuf) + pix, (unsigned long long)key);
+    return win;
   }
 }
 
@@ -349,6 +352,9 @@ struct HizArgs {
 };
 
 constexpr int kPassStats = 8;  // passes with statistics (see PassState)
+// counters per render: [0, kPassStats) points past the coarse test, [kPassStats, 2 kPassStats)
+// points past the exact kernel's early-z read (an atomic issued; exact-kernel passes only)
+constexpr int kStatCtrs = 2 * kPassStats;
 
 // Sum of a per-thread count over the warp, added once by lane 0.
 __device__ __forceinline__ void add_warp_count(unsigned long long* ctr, uint32_t v) {
@@ -385,7 +391,7 @@ __device__ __forceinline__ void flush_queue(const QEntry* q, int n, int lane, ui
 //     chunk's hits, whose keybuf reads were issued one step ago, so the
 //     random-L2 read latency overlaps a chunk of math, and
 // (5) issue this chunk's keybuf reads.
-template <bool kSigned, bool kRed>
+template <bool kSigned, bool kRed, bool kStats = false>
 __global__ void __launch_bounds__(kRenderThreads, 1)
     render_tma_kernel(uint64_t* __restrict__ keybuf, const float* __restrict__ pos,
                       const ChunkMap cm, uint64_t base_index, const DevCam cam, const HizArgs hz) {
@@ -419,7 +425,7 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
     }
   }
   const bool use_hiz = hz.zmax != nullptr;
-  if (hz.stats_clear && blockIdx.x == 0 && threadIdx.x < kPassStats) hz.stats_clear[threadIdx.x] = 0ull;
+  if (hz.stats_clear && blockIdx.x == 0 && threadIdx.x < kStatCtrs) hz.stats_clear[threadIdx.x] = 0ull;
   if (use_hiz) {
     const uint4* src = reinterpret_cast<const uint4*>(hz.zmax);
     uint4* dst = reinterpret_cast<uint4*>(zs);
@@ -434,6 +440,7 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
   uint64_t pkey[kPtsPerThread], pcur[kPtsPerThread];
   uint32_t pmask = 0;
   uint32_t n_surv = 0;  // points past the coarse test (pass statistics)
+  uint32_t n_win = 0;   // ... and past the early-z read (kStats)
 #pragma unroll
   for (int j = 0; j < kPtsPerThread; ++j) {
     ppix[j] = 0;
@@ -526,7 +533,10 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
     // (4) + (5)
 #pragma unroll
     for (int j = 0; j < kPtsPerThread; ++j)
-      if ((pmask >> j) & 1u) fold_loaded<kSigned>(keybuf, ppix[j], pkey[j], pcur[j]);
+      if ((pmask >> j) & 1u) {
+        const bool w = fold_loaded<kSigned>(keybuf, ppix[j], pkey[j], pcur[j]);
+        if constexpr (kStats) n_win += w;
+      }
 #pragma unroll
     for (int j = 0; j < kPtsPerThread; ++j) {
       if ((okmask >> j) & 1u)
@@ -539,9 +549,13 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
   }
 #pragma unroll
   for (int j = 0; j < kPtsPerThread; ++j)
-    if ((pmask >> j) & 1u) fold_loaded<kSigned>(keybuf, ppix[j], pkey[j], pcur[j]);
+    if ((pmask >> j) & 1u) {
+      const bool w = fold_loaded<kSigned>(keybuf, ppix[j], pkey[j], pcur[j]);
+      if constexpr (kStats) n_win += w;
+    }
   flush_queue<kSigned>(wq, qn, lane, keybuf, cam);
   add_warp_count(hz.stats, n_surv);
+  if constexpr (kStats) add_warp_count(hz.stats ? hz.stats + kPassStats : nullptr, n_win);
 }
 
 // Hi-Z passes: the f32 pre-test rejects most points in ~25 instructions; the
@@ -620,7 +634,7 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
     render_pre_kernel(uint64_t* __restrict__ keybuf, const float* __restrict__ pos,
                       const ChunkMap cm, uint64_t base_index, const DevCam cam, const HizArgs hz) {
   static_assert(kMode >= 0 && kMode <= 2, "ChunkMap mode");
-  if (hz.stats_clear && blockIdx.x == 0 && threadIdx.x < kPassStats) hz.stats_clear[threadIdx.x] = 0ull;
+  if (hz.stats_clear && blockIdx.x == 0 && threadIdx.x < kStatCtrs) hz.stats_clear[threadIdx.x] = 0ull;
   extern __shared__ __align__(128) uint8_t smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t pol = l2_evict_first_policy();  // the point stream (see bulk_g2s_stream)
@@ -1251,6 +1265,10 @@ static int device_init() {
                          cudaFuncAttributeMaxDynamicSharedMemorySize, kRenderSmem);
     cudaFuncSetAttribute(render_tma_kernel<true, true>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, kRenderSmem);
+    cudaFuncSetAttribute(render_tma_kernel<false, false, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, kRenderSmem);
+    cudaFuncSetAttribute(render_tma_kernel<true, false, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, kRenderSmem);
     for (auto k : {render_pre_kernel<false, 0, false>, render_pre_kernel<false, 1, false>,
                    render_pre_kernel<false, 2, false>, render_pre_kernel<true, 0, false>,
                    render_pre_kernel<true, 1, false>, render_pre_kernel<true, 2, false>,
@@ -1281,7 +1299,10 @@ struct PassState {
   bool pending = false;
   int64_t pts[kPassStats] = {};        // points of each pass in the copied frame
   bool exact[kPassStats] = {};         // current choice per pass
+  bool was_exact[kPassStats] = {};     // ... in the copied frame
+  double win[kPassStats] = {-1, -1, -1, -1, -1, -1, -1, -1};  // last exact-pass win fraction
   uint32_t calls = 0;
+  uint32_t reads = 0;  // statistics copies read (win fractions re-sampled every 8th)
 };
 static std::mutex g_pass_mu;
 struct PassKeyHash {
@@ -1291,6 +1312,7 @@ struct PassKeyHash {
 };
 static std::unordered_map<std::pair<const void*, const void*>, PassState, PassKeyHash> g_pass;
 static double g_dense_frac = -1.0;  // exact kernel above this survivor fraction
+static double g_win_frac = -1.0;    // ... unless more than this share of its survivors won
 
 static double dense_frac() {
   if (g_dense_frac < 0.0) {
@@ -1298,6 +1320,14 @@ static double dense_frac() {
     g_dense_frac = e ? atof(e) : 0.60;
   }
   return g_dense_frac;
+}
+
+static double win_frac() {
+  if (g_win_frac < 0.0) {
+    const char* e = getenv("NAR_RENDER_WIN_FRAC");
+    g_win_frac = e ? atof(e) : 0.10;
+  }
+  return g_win_frac;
 }
 
 // Renders n points.  With a Hi-Z scratch (zmax), the aligned part is split
@@ -1348,8 +1378,8 @@ static int launch_render(uint64_t* keybuf, const float* pos, int64_t n, uint64_t
       auto it = g_pass.find(key);
       if (it == g_pass.end() && g_pass.size() < 256) {
         PassState st0;
-        if (cudaMalloc(reinterpret_cast<void**>(&st0.dev), kPassStats * 8) != cudaSuccess ||
-            cudaHostAlloc(reinterpret_cast<void**>(&st0.host), kPassStats * 8,
+        if (cudaMalloc(reinterpret_cast<void**>(&st0.dev), kStatCtrs * 8) != cudaSuccess ||
+            cudaHostAlloc(reinterpret_cast<void**>(&st0.host), kStatCtrs * 8,
                           cudaHostAllocDefault) != cudaSuccess ||
             cudaEventCreateWithFlags(&st0.ev, cudaEventDisableTiming) != cudaSuccess)
           return set_error(NAR_ERR_NOMEM, "pass statistics");
@@ -1358,26 +1388,37 @@ static int launch_render(uint64_t* keybuf, const float* pos, int64_t n, uint64_t
       if (it != g_pass.end()) ps = &it->second;
       if (ps && ps->pending && cudaEventQuery(ps->ev) == cudaSuccess) {
         static const bool verbose = getenv("NAR_RENDER_STATS") != nullptr;
+        if (++ps->reads % 8 == 0)  // let passes that left the exact kernel re-measure it
+          for (int p = 0; p < kPassStats; ++p) ps->win[p] = -1.0;
         for (int p = 0; p < kPassStats; ++p) {
           if (ps->pts[p] <= 0) continue;
           const double f = (double)ps->host[p] / (double)ps->pts[p];
-          ps->exact[p] = f > dense_frac();
-          if (verbose) fprintf(stderr, "nar pass %d: %.4f of %lld points past the coarse test\n", p,
-                               f, (long long)ps->pts[p]);
+          if (ps->was_exact[p] && ps->host[p] > 0)
+            ps->win[p] = (double)ps->host[kPassStats + p] / (double)ps->host[p];
+          // the exact kernel's early-z read pays where most survivors lose at their
+          // pixel (dense 2.5-D clouds); where many still win, the pre-test kernel's
+          // plain atomics are cheaper (measured on sparse shards, bench c5 / nar1b)
+          ps->exact[p] = f > dense_frac() && !(ps->win[p] > win_frac());
+          if (verbose)
+            fprintf(stderr, "nar pass %d: %.4f of %lld points past the coarse test, win %.4f%s\n",
+                    p, f, (long long)ps->pts[p], ps->win[p], ps->was_exact[p] ? " (exact)" : "");
         }
         ps->pending = false;
       }
       if (ps) {
         for (int p = 0; p < kPassStats; ++p) exact_now[p] = ps->exact[p];
-        // one render in 16 collects statistics (the seed pass zeroes the
-        // counters, the copy back is amortised)
-        if (ps->calls++ % 16 == 0 && !ps->pending) dstats = ps->dev;
+        // the first renders, then one in 16, collect statistics (the seed pass
+        // zeroes the counters, the copy back is amortised); the second measures
+        // the win fractions of the passes the first moved to the exact kernel
+        const uint32_t call = ps->calls++;
+        if ((call < 4 || call % 16 == 0) && !ps->pending) dstats = ps->dev;
       }
     }
     if (n_tiles > 0) {
       const int64_t sms = g_num_sms;
       auto kern = sgn ? render_tma_kernel<true, false> : render_tma_kernel<false, false>;
       auto kseed = sgn ? render_tma_kernel<true, true> : render_tma_kernel<false, true>;
+      auto kern_st = sgn ? render_tma_kernel<true, false, true> : render_tma_kernel<false, false, true>;
       decltype(&render_pre_kernel<false, 0, false>) kpres[2][2][3] = {
           {{render_pre_kernel<false, 0, false>, render_pre_kernel<false, 1, false>,
             render_pre_kernel<false, 2, false>},
@@ -1418,7 +1459,8 @@ static int launch_render(uint64_t* keybuf, const float* pos, int64_t n, uint64_t
           kseed<<<grid, kRenderThreads, kRenderSmem, st>>>(keybuf, pos, cm, base, cam, hz);
         } else {
           nar::count_launch();
-          kern<<<grid, kRenderThreads, kRenderSmem, st>>>(keybuf, pos, cm, base, cam, hz);
+          (hz.stats ? kern_st : kern)<<<grid, kRenderThreads, kRenderSmem, st>>>(keybuf, pos, cm, base,
+                                                                               cam, hz);
         }
       };
       // Hi-Z schedule: a seed pass over every S-th chunk (spread over the whole
@@ -1474,9 +1516,12 @@ static int launch_render(uint64_t* keybuf, const float* pos, int64_t n, uint64_t
       if (ps && dstats && pass_no > 1) {  // hand the counters to later renders (no sync)
         std::lock_guard<std::mutex> lk(g_pass_mu);
         if (!ps->pending) {
-          cudaMemcpyAsync(ps->host, dstats, kPassStats * 8, cudaMemcpyDeviceToHost, st);
+          cudaMemcpyAsync(ps->host, dstats, kStatCtrs * 8, cudaMemcpyDeviceToHost, st);
           cudaEventRecord(ps->ev, st);
-          for (int p = 0; p < kPassStats; ++p) ps->pts[p] = pass_pts[p];
+          for (int p = 0; p < kPassStats; ++p) {
+            ps->pts[p] = pass_pts[p];
+            ps->was_exact[p] = exact_now[p];
+          }
           ps->pending = true;
         }
       }

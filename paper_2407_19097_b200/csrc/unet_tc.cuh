@@ -635,14 +635,16 @@ __global__ void __maxnreg__(96)
               // to the tile); halo rows 0 and R+1 stay single (W0 -> row 0, W2 -> row R-1)
 #pragma unroll 1
               for (int kx = 0; kx < 3; ++kx) {
-                const uint32_t bk = sb + kx * (4 * N * 32);  // [k8][4N][8]: LBO = 4N*16
+                // [k8][4N][8]: LBO = 4N*16
+                const uint64_t bk = umma_desc(sb + kx * (4 * N * 32), 4 * N * 16, 128);
+                const uint64_t ak = umma_desc_sw32(sa + kx * 32);
 #pragma unroll
                 for (int g = 0; g < R / 2 + 2; ++g) {
                   const int blk0 = g == 0 ? 3 : (3 - 2 * g > 0 ? 3 - 2 * g : 0);
                   const int blk1 = g == R / 2 + 1 ? 0 : (R + 2 - 2 * g < 3 ? R + 2 - 2 * g : 3);
                   const int drow = g == 0 ? 0 : (g == R / 2 + 1 ? R - 1 : 2 * g - 3 + blk0);
-                  const uint64_t bdesc = umma_desc(bk + blk0 * N * 16, 4 * N * 16, 128);
-                  const uint64_t adesc = umma_desc_sw32(sa + g * kHaloRowBytes + kx * 32);
+                  const uint64_t bdesc = desc_add(bk, blk0 * N * 16);
+                  const uint64_t adesc = desc_add(ak, g * kHaloRowBytes);
                   umma_bf16(dcol + drow * N, adesc, bdesc, umma_idesc_bf16(128, (blk1 - blk0 + 1) * N), 1u);
                 }
               }
@@ -667,14 +669,14 @@ __global__ void __maxnreg__(96)
               const uint64_t b12 = umma_desc(bk + 1 * N * 16, 4 * N * 16, 128);
               const uint64_t b3 = umma_desc(bk + 3 * N * 16, 4 * N * 16, 128);
               const uint64_t b0 = umma_desc(bk, 4 * N * 16, 128);
-              const uint32_t ax = sa + kx * 32;
+              const uint64_t ax = umma_desc_sw32(sa + kx * 32);
 #pragma unroll
               for (int pr = 0; pr < R / 2; ++pr) {
-                umma_bf16(dcol + 2 * pr * N, umma_desc_sw32(ax + (pr + 1) * kHaloRowBytes), b12,
+                umma_bf16(dcol + 2 * pr * N, desc_add(ax, (pr + 1) * kHaloRowBytes), b12,
                           umma_idesc_bf16(128, 2 * N), 1u);
-                umma_bf16(dcol + 2 * pr * N, umma_desc_sw32(ax + pr * kHaloRowBytes), b3, IDESC, 1u);
-                umma_bf16(dcol + (2 * pr + 1) * N, umma_desc_sw32(ax + (pr + 2) * kHaloRowBytes), b0,
-                          IDESC, 1u);
+                umma_bf16(dcol + 2 * pr * N, desc_add(ax, pr * kHaloRowBytes), b3, IDESC, 1u);
+                umma_bf16(dcol + (2 * pr + 1) * N, desc_add(ax, (pr + 2) * kHaloRowBytes), b0, IDESC,
+                          1u);
               }
             }
             if (last) {  // (decoder layers end with the skip chunk; kept for completeness)
