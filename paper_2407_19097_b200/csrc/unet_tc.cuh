@@ -96,7 +96,10 @@ constexpr int kEpiGroups = 4;   // epilogue warps per TMEM lane quarter
 constexpr int kMmaWarp = kProdWarps + 4 * kEpiGroups;
 constexpr int kTcThreads = (kMmaWarp + 1) * 32;  // 1 producer + 16 epilogue + 1 MMA warps
 constexpr int kHaloPx = 130;                 // pixels a tile row reads (128 + 2 halo)
-constexpr int kHaloPitch = 136;              // loaded per row: 136 x 32 B = 17 swizzle atoms
+#ifndef NAR_TC_HALO_PITCH
+#define NAR_TC_HALO_PITCH 136
+#endif
+constexpr int kHaloPitch = NAR_TC_HALO_PITCH;  // loaded per row: 136 x 32 B = 17 swizzle atoms
 constexpr int kHaloRowBytes = kHaloPitch * 32;  // one 16-channel halo row, SWIZZLE_32B
 
 // NB = TMEM accumulator buffers.  2: the epilogue of tile i overlaps the MMAs
