@@ -910,7 +910,7 @@ def main_ours(args):
                          "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
                          "frac_nominal_8tbs": achieved / 8000.0,
                          "traffic": traffic, "peak_kind": peak_kind,
-                         "kernel": "render passes (render_pre_kernel + seed render_tma_kernel + hiz_kernel)",
+                         "kernel": "render passes (seed + pre-test passes: render_pre_kernel; dense passes: render_tma_kernel; Hi-Z refreshes: hiz_rows_kernel)",
                          "bytes_per_point": BYTES_PER_POINT},
             "parity": parity,
             "cpu_baseline": cpu,
