@@ -168,6 +168,9 @@ __host__ __device__ constexpr int tc_fixed_smem(int N) {
   return 512 + kTcOnesBytes + kTcBiasBytes + kTcParamFloats * 4;
 }
 // stages: as many (<= NAR_TC_MAX_STAGES) as fit the 227 KB opt-in shared memory
+#ifndef NAR_TC_WEIGHT_PREFETCH
+#define NAR_TC_WEIGHT_PREFETCH 1
+#endif
 #ifndef NAR_TC_MAX_STAGES
 #define NAR_TC_MAX_STAGES 3
 #endif
@@ -513,6 +516,29 @@ __global__ void __maxnreg__(96)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tbase_slot;
+  // chunk q's packed weights: paired up2 chunks (4 stacked blocks) first
+  constexpr uint32_t B3 = tc_b3_bytes(N), B4 = tc_b4_bytes(N);
+  auto wchunk = [&](int q, size_t& boff) -> uint32_t {
+    const bool in_a = q < nqa;
+    boff = a.up2pair ? (in_a ? (size_t)q * B4 : (size_t)nqa * B4 + (size_t)(q - nqa) * B3)
+                     : (size_t)q * B3;
+    return a.up2pair && in_a ? B4 : B3;
+  };
+  // The weights do not depend on the previous layer: the first stages' weight
+  // copies go out before the grid dependency wait (expect_tx without arrival; the
+  // stage's arrive.expect_tx for its halo follows in the producer loop).
+  int n_pre = 0;
+  if (warp == 0 && lane == 0 && !(a.debug & 4) && NAR_TC_WEIGHT_PREFETCH) {
+    const int my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    n_pre = my_tiles * nq < S ? my_tiles * nq : S;
+    for (int it = 0; it < n_pre; ++it) {
+      size_t boff;
+      const uint32_t bbytes = wchunk(it % nq, boff);
+      mbar_expect_tx_only(&full[it], bbytes);
+      bulk_g2s(smem + it * STAGE + A_BYTES, reinterpret_cast<const uint8_t*>(a.wtc) + boff, bbytes,
+               &full[it]);
+    }
+  }
   // Everything above touches only this launch's constant parameters; the
   // activations are the previous layer's output (and our output may still be
   // read by an earlier layer): wait for the prerequisite grid to complete.
@@ -546,15 +572,13 @@ __global__ void __maxnreg__(96)
           mbar_arrive(&full[s]);
           continue;
         }
-        // chunk q's packed weights: paired up2 chunks (4 stacked blocks) first
-        constexpr uint32_t B3 = tc_b3_bytes(N), B4 = tc_b4_bytes(N);
-        const bool pq = a.up2pair && in_a;
-        const uint32_t bbytes = pq ? B4 : B3;
-        const size_t boff = a.up2pair ? (in_a ? (size_t)q * B4 : (size_t)nqa * B4 + (size_t)(q - nqa) * B3)
-                                      : (size_t)q * B3;
-        mbar_expect_tx(&full[s], (up ? UP_TX : A_TX) + bbytes);
+        size_t boff;
+        const uint32_t bbytes = wchunk(q, boff);
+        const bool pre = it < n_pre;  // weights already in flight (before the grid wait)
+        mbar_expect_tx(&full[s], (up ? UP_TX : A_TX) + (pre ? 0u : bbytes));
         tma_load_3d(stA, map, cbase, x0 - 1, yr, &full[s]);
-        bulk_g2s(stA + A_BYTES, reinterpret_cast<const uint8_t*>(a.wtc) + boff, bbytes, &full[s]);
+        if (!pre)
+          bulk_g2s(stA + A_BYTES, reinterpret_cast<const uint8_t*>(a.wtc) + boff, bbytes, &full[s]);
       }
     }
   } else if (warp == kMmaWarp) {
