@@ -424,6 +424,7 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
       }
     }
   }
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // (see render_pre_kernel)
   const bool use_hiz = hz.zmax != nullptr;
   if (hz.stats_clear && blockIdx.x == 0 && threadIdx.x < kStatCtrs) hz.stats_clear[threadIdx.x] = 0ull;
   if (use_hiz) {
@@ -665,6 +666,9 @@ __global__ void __launch_bounds__(kRenderThreads, 1)
       }
     }
   }
+  // the point stream above does not depend on the previous kernel; the coarse depth
+  // and the keybuf do (a no-op unless launched as a programmatic dependent)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (hz.zmax) {
     const uint4* src = reinterpret_cast<const uint4*>(hz.zmax);
     uint4* dst = reinterpret_cast<uint4*>(zs);
@@ -858,6 +862,9 @@ template <bool kSigned, int S>
 __global__ void __launch_bounds__(256)
     hiz_rows_kernel(const uint64_t* __restrict__ keybuf, int W, int H, int zw, int zh,
                     uint16_t* __restrict__ zmax) {
+  // the next render pass may be launched now (programmatic dependent launch): its
+  // CTAs take SMs as our blocks drain and start their point streams, then wait
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   constexpr int kHalf = S / 2, kNb = 255 / kHalf;
   __shared__ uint32_t cm[256];
   const int by = blockIdx.y;
@@ -1446,10 +1453,30 @@ static int launch_render(uint64_t* keybuf, const float* pos, int64_t n, uint64_t
         const int64_t need = (nj + kRenderWarps - 1) / kRenderWarps;
         const int grid = (int)(need < sms ? need : sms);
         if (grid <= 0) return;
+        // a pass right after its Hi-Z refresh is a programmatic dependent of it: its
+        // CTAs start their point streams while the refresh drains (NAR_RENDER_PDL=0: off)
+        static const bool pdl_on = [] {
+          const char* e = getenv("NAR_RENDER_PDL");
+          return !(e && e[0] == '0');
+        }();
+        cudaLaunchAttribute pattr[1];
+        pattr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        pattr[0].val.programmaticStreamSerializationAllowed = 1;
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3((unsigned)grid);
+        lc.blockDim = dim3(kRenderThreads);
+        lc.stream = st;
+        lc.attrs = pattr;
+        lc.numAttrs = (with_hiz && pdl_on) ? 1 : 0;
         if (with_hiz && pre && !(pno < kPassStats && exact_now[pno])) {
           nar::count_launch();
-          kpres[sgn ? 1 : 0][hz.stats ? 1 : 0][cm.mode]<<<grid, kRenderThreads, kPreSmem, st>>>(
-              keybuf, pos, cm, base, cam, hz);
+          lc.dynamicSmemBytes = kPreSmem;
+          cudaLaunchKernelEx(&lc, kpres[sgn ? 1 : 0][hz.stats ? 1 : 0][cm.mode], keybuf, pos, cm,
+                             base, cam, hz);
+        } else if (with_hiz && !(cm.mode == 1 && pre)) {
+          nar::count_launch();
+          lc.dynamicSmemBytes = kRenderSmem;
+          cudaLaunchKernelEx(&lc, hz.stats ? kern_st : kern, keybuf, pos, cm, base, cam, hz);
         } else if (cm.mode == 1 && pre) {  // seed units: the direct path of the pre kernel
           nar::count_launch();
           kpres[sgn ? 1 : 0][0][1]<<<grid, kRenderThreads, kPreSmem, st>>>(keybuf, pos, cm, base,
