@@ -15,6 +15,7 @@ from __future__ import annotations
 import ctypes as C
 import hashlib
 import json
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -242,6 +243,8 @@ class UNet:
                 a = _host_param(params[name])
                 _lib.check(lib.nar_unet_set_param(self._h, name.encode(), a.ctypes.data, a.size))
         self._ws = {}
+        self._graphs: dict = {}  # (x, out, H, W) -> CUDA graph of one forward (or False)
+        self._seen: set = set()
 
     def _workspace(self, H: int, W: int):
         import torch
@@ -274,10 +277,51 @@ class UNet:
         if x.numel() != H * W * int(x.shape[-1]):
             raise ValueError("forward_into takes one image (H, W, C) or (1, H, W, C)")
         ws = self._workspace(H, W)
+        # graphs need a torch stream (None: the current one); raw handles stay eager
+        # (and not while the caller captures a graph of its own: the launches join it)
+        graphs = (_UNET_GRAPHS and (stream is None or isinstance(stream, torch.cuda.Stream))
+                  and not torch.cuda.is_current_stream_capturing())
+        key = (x.data_ptr(), out.data_ptr(), H, W)
+        g = self._graphs.get(key) if graphs else None
+        if g is None and graphs and key in self._seen:
+            # second call on the same buffers: capture the 20 launches once and
+            # replay them from now on (no per-launch host cost; the programmatic
+            # dependent edges between the convs are kept in the graph)
+            g = self._capture(x, out, ws, H, W, stream)
+        if g is not None and g is not False:
+            with torch.cuda.stream(stream or torch.cuda.current_stream(self.device)):
+                g.replay()  # on the caller's stream, like the eager launches
+            return
+        if graphs:
+            self._seen.add(key)
+        self._launch(x, out, ws, H, W, stream)
+
+    def _launch(self, x, out, ws, H: int, W: int, stream) -> None:
         with _lib.on_device(self.device.index):  # weights upload + launches on self.device
             _lib.check(_lib.load().nar_unet_forward(
                 self._h, x.data_ptr(), H, W, out.data_ptr(), ws.data_ptr(), ws.numel(),
                 _lib.stream_handle(stream, self.device.index)))
+
+    def _capture(self, x, out, ws, H: int, W: int, stream):
+        """A CUDA graph of one forward on these exact buffers (the weights and the
+        workspace are the network's own and never move), or False (not retried)."""
+        import torch
+
+        key = (x.data_ptr(), out.data_ptr(), H, W)
+        if len(self._graphs) >= 8:
+            self._graphs.pop(next(iter(self._graphs)))
+        caller = stream or torch.cuda.current_stream(self.device)
+        try:
+            g = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream(self.device)
+            side.wait_stream(caller)
+            with torch.cuda.stream(side), torch.cuda.graph(g, stream=side):
+                self._launch(x, out, ws, H, W, None)
+            caller.wait_stream(side)
+        except Exception:  # capture not possible here: stay eager for this key
+            g = False
+        self._graphs[key] = g
+        return g
 
     def __call__(self, x):
         import torch
@@ -304,6 +348,9 @@ class UNet:
 
 
 _nets: dict = {}
+# UNet.forward_into replays a CUDA graph of the forward on buffers it has seen
+# before (NAR_UNET_GRAPH=0: plain launches every call)
+_UNET_GRAPHS = os.environ.get("NAR_UNET_GRAPH", "1") != "0"
 
 
 def _host_param(v) -> np.ndarray:

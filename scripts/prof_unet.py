@@ -17,6 +17,8 @@ def main():
     ap.add_argument("--cin", type=int, default=4)
     ap.add_argument("--h", type=int, default=1088)
     ap.add_argument("--w", type=int, default=1920)
+    ap.add_argument("--graph", action="store_true",
+                    help="capture one forward in a CUDA graph and time replays (no host launch cost)")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     cfg = UNetConfig(input_channels=a.cin)
@@ -26,10 +28,24 @@ def main():
     for _ in range(2):
         net.forward_into(x, y)
     torch.cuda.synchronize()
+    run = lambda: net.forward_into(x, y)
+    if a.graph:
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                net.forward_into(x, y)
+        torch.cuda.current_stream().wait_stream(s)
+        run = g.replay
+        for _ in range(2):
+            run()
+        torch.cuda.synchronize()
+    print("forward_into graphs:", {k[2:]: type(v).__name__ for k, v in net._graphs.items()})
     for _ in range(a.frames):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        net.forward_into(x, y)
+        run()
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)

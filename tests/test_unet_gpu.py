@@ -351,3 +351,56 @@ def test_forward_quad_head_pyramid(cuda, cin):
     ref = oracle.forward(x, params, cfg)
     assert oracle.psnr(y, ref) >= PSNR_MIN
     assert np.abs(y - ref).max() <= MAX_ABS
+
+
+def test_forward_into_graph_replay(cuda):
+    """forward_into on buffers it has seen before replays a CUDA graph of the forward:
+    new input contents each call, outputs bitwise equal to plain launches."""
+    import torch
+
+    from paper_2407_19097_b200.neural import UNet, UNetConfig, init_params
+
+    cfg = UNetConfig(input_channels=4)
+    net = UNet(cfg, init_params(cfg), device=cuda)
+    H, W = 96, 160
+    x = torch.empty((H, W, 4), device=cuda)
+    y = torch.empty((H, W, 3), device=cuda)
+    y_eager = torch.empty_like(y)
+    ws = net._workspace(H, W)
+    gen = torch.Generator(device=cuda).manual_seed(5)
+    for _ in range(4):
+        x.copy_(torch.rand((H, W, 4), device=cuda, generator=gen))
+        net.forward_into(x, y)
+        net._launch(x, y_eager, ws, H, W, None)
+        torch.cuda.synchronize()
+        assert torch.equal(y.view(torch.int32), y_eager.view(torch.int32))
+    g = net._graphs.get((x.data_ptr(), y.data_ptr(), H, W))
+    assert g is not None and g is not False, "the repeated forward was not captured"
+
+
+def test_forward_into_inside_caller_graph(cuda):
+    """A caller capturing its own CUDA graph gets the plain launches captured (no
+    nested capture / replay inside the capture)."""
+    import torch
+
+    from paper_2407_19097_b200.neural import UNet, UNetConfig, init_params
+
+    cfg = UNetConfig(input_channels=4)
+    net = UNet(cfg, init_params(cfg), device=cuda)
+    H, W = 64, 96
+    x = torch.rand((H, W, 4), device=cuda)
+    y = torch.empty((H, W, 3), device=cuda)
+    ref = torch.empty_like(y)
+    for _ in range(2):  # seen + captured by forward_into itself
+        net.forward_into(x, ref)
+    net.forward_into(x, y)  # warm the (x, y) key too: the next call would capture
+    g = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream(cuda)
+    side.wait_stream(torch.cuda.current_stream(cuda))
+    with torch.cuda.stream(side), torch.cuda.graph(g, stream=side):
+        net.forward_into(x, y)
+    torch.cuda.current_stream(cuda).wait_stream(side)
+    y.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(y.view(torch.int32), ref.view(torch.int32))
