@@ -795,10 +795,20 @@ def main_ours(args):
         # PointCloud(..., pinned=True): points DMA'd, rgb gathered in place (zero-copy)
         pc_pin = PointCloud(host_pos, [Stream("rgb", "u8", host_rgb)], pinned=True)
         pin_ms, fi, _ = timed_rasterize(pc_pin)
-        gathered = int(fi.coverage.astype(bool).sum()) * 3
+        from paper_2407_19097_b200 import msr as _msr
+
+        if _msr._HOST_GATHER:  # keys down, per-pixel rgb words up (msr._host_gather)
+            npix = W * H
+            gathered, d2h_extra = 4 * npix, 8 * npix
+            note = ("positions DMA (12 B/pt) + the winners' rgb gathered by host threads "
+                    "(keybuf 8 B/px down, packed rgb 4 B/px up)")
+        else:
+            gathered, d2h_extra = int(fi.coverage.astype(bool).sum()) * 3, 0
+            note = "positions DMA (12 B/pt) + zero-copy gather of winners' rgb"
+        d2h += d2h_extra
         e2e = {"value": cloud.count / (pin_ms * 1e-3) / 1e9, "unit": "Gpts/s",
                "h2d_bytes_per_step": int(host_pos.nbytes + gathered),
-               "h2d_note": "positions DMA (12 B/pt) + zero-copy gather of winners' rgb",
+               "h2d_note": note,
                "d2h_bytes_per_step": int(d2h), "ms_per_step": pin_ms,
                "api": "paper_2407_19097_b200.msr.rasterize(PointCloud(..., pinned=True))",
                "pageable": {"value": cloud.count / (pg_ms * 1e-3) / 1e9, "unit": "Gpts/s",

@@ -3,10 +3,14 @@
 // returns a status and leaves a thread-local message (nar_last_error).
 #include <cuda_runtime.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include <atomic>
+#include <condition_variable>
 #include <mutex>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "common.cuh"
 #include "nar_b200.h"
@@ -44,6 +48,88 @@ void keep_pool_memory() {
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
   });
+}
+
+// A persistent pool of host threads for host-side passes over a frame (the
+// attribute gather of nar_host_gather_rgb): the calling thread works too, and a
+// call returns once every range is done.  Calls are serialised.
+namespace {
+struct HostPool {
+  std::mutex mu, call_mu;
+  std::condition_variable cv, done_cv;
+  std::vector<std::thread> workers;
+  const std::function<void(int64_t, int64_t)>* fn = nullptr;
+  int64_t n = 0, chunk = 1;
+  std::atomic<int64_t> next{0};
+  int active = 0;
+  uint64_t gen = 0;
+  bool stop = false;
+
+  explicit HostPool(int nt) {
+    for (int t = 0; t < nt; ++t) workers.emplace_back([this] { loop(); });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      stop = true;
+    }
+    cv.notify_all();
+    for (auto& w : workers) w.join();
+  }
+  void work() {
+    for (;;) {
+      const int64_t b = next.fetch_add(chunk);
+      if (b >= n) return;
+      (*fn)(b, b + chunk < n ? b + chunk : n);
+    }
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      std::unique_lock<std::mutex> lk(mu);
+      cv.wait(lk, [&] { return stop || gen != seen; });
+      if (stop) return;
+      seen = gen;
+      lk.unlock();
+      work();
+      lk.lock();
+      if (--active == 0) done_cv.notify_all();
+    }
+  }
+  void run(int64_t count, const std::function<void(int64_t, int64_t)>& f) {
+    std::lock_guard<std::mutex> call(call_mu);
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      fn = &f;
+      n = count;
+      const int64_t parts = 8 * (int64_t)(workers.size() + 1);
+      chunk = count / parts > 4096 ? count / parts : 4096;
+      next.store(0);
+      active = (int)workers.size();
+      ++gen;
+    }
+    cv.notify_all();
+    work();
+    std::unique_lock<std::mutex> lk(mu);
+    done_cv.wait(lk, [&] { return active == 0; });
+    fn = nullptr;
+  }
+};
+}  // namespace
+
+void host_parallel_for(int64_t n, const std::function<void(int64_t, int64_t)>& f) {
+  if (n <= 0) return;
+  static HostPool pool([] {
+    const char* e = getenv("NAR_HOST_THREADS");
+    const int hw = (int)std::thread::hardware_concurrency();
+    const int t = e ? atoi(e) : (hw > 0 ? hw : 1);
+    return (t > 64 ? 64 : (t < 1 ? 1 : t)) - 1;  // + the calling thread
+  }());
+  if (n < 65536) {
+    f(0, n);
+    return;
+  }
+  pool.run(n, f);
 }
 
 }  // namespace nar

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <functional>
+
 #include "nar_b200.h"
 
 namespace nar {
@@ -17,6 +19,8 @@ void count_launch();
 uint64_t launch_total();
 // keeps cudaMallocAsync scratch mapped across calls (default pool threshold)
 void keep_pool_memory();
+// f(begin, end) over [0, n) on a persistent pool of host threads (NAR_HOST_THREADS)
+void host_parallel_for(int64_t n, const std::function<void(int64_t, int64_t)>& f);
 
 // Per-device state (kernel attributes, SM counts, staging buffers) is indexed
 // by the calling thread's current device: the library works on whichever

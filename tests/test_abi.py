@@ -159,3 +159,29 @@ def test_plain_c_consumer(cuda, tmp_path):
     want = oracle.rasterize(PointCloud(pos, [Stream("rgb", "u8", rgb)]), cam,
                             StreamSelection(rgb=True, depth=True))["data"]
     assert np.array_equal(data, want)
+
+
+def test_host_gather_rgb_semantics():
+    """nar_host_gather_rgb (host code, no GPU): per pixel the winner's rgb bytes packed
+    c0 | c1 << 8 | c2 << 16; 0 for empty keys and winners outside [begin, begin+count);
+    signed-domain keys are un-flipped first.  Large enough to run on the thread pool."""
+    rng = np.random.default_rng(11)
+    count, begin, arity = 50_000, 1000, 4
+    rgb = rng.integers(0, 256, (count, arity), dtype=np.uint8)
+    npix = 300_000
+    idx = rng.integers(0, begin + count + 500, npix).astype(np.uint64)
+    depth = rng.integers(1, 2**31, npix).astype(np.uint64)
+    keys = (depth << np.uint64(32)) | idx
+    empty = rng.random(npix) < 0.1
+    keys[empty] = np.uint64(0xFFFFFFFFFFFFFFFF)
+    inside = ~empty & (idx >= begin) & (idx < begin + count)
+    rows = np.where(inside, idx.astype(np.int64) - begin, 0)
+    want = np.where(inside, rgb[rows, 0].astype(np.uint32) | (rgb[rows, 1].astype(np.uint32) << 8)
+                    | (rgb[rows, 2].astype(np.uint32) << 16), 0).astype(np.uint32)
+    lib = _lib.load()
+    for domain, k in ((_lib.KEYS_UNSIGNED, keys), (_lib.KEYS_SIGNED, keys ^ np.uint64(_lib.SIGN_FLIP))):
+        k = np.ascontiguousarray(k)
+        out = np.full(npix, 0xDEADBEEF, np.uint32)
+        assert lib.nar_host_gather_rgb(k.ctypes.data, npix, domain, rgb.ctypes.data, arity,
+                                       C.c_uint64(begin), count, out.ctypes.data) == 0
+        np.testing.assert_array_equal(out, want)

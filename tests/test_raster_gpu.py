@@ -559,3 +559,38 @@ def test_hiz_refresh_kernels_agree(cuda, monkeypatch, W, H):
         keys.append(r.keys())
     assert np.array_equal(keys[0], keys[1])
     assert torch.equal(tables[0], tables[1])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("pinned", [False, True])
+def test_rasterize_host_gather_matches_zero_copy(cuda, monkeypatch, pinned):
+    """rasterize()'s host-side gather of the winners' rgb (nar_host_gather_rgb +
+    nar_resolve_pixrgb) gives the same FeatureImage as the resolve kernel's own
+    zero-copy gather, and both equal the oracle."""
+    from paper_2407_19097_b200 import msr
+    from paper_2407_19097_b200.geometry import Intrinsics, PointCloud, Stream, look_at
+
+    rng = np.random.default_rng(21)
+    n = 3_000_000
+    pc = PointCloud(rng.uniform(-1, 1, (n, 3)).astype(np.float32),
+                    [Stream("rgb", "u8", rng.integers(0, 256, (n, 3), dtype=np.uint8))],
+                    pinned=pinned)
+    cam = look_at((0.3, -2.4, 1.1), (0, 0, 0), Intrinsics(width=640, height=360))
+    sel = msr.StreamSelection(rgb=True, depth=True)
+    monkeypatch.setattr(msr, "_HOST_GATHER", False)
+    a = msr.rasterize(pc, cam, sel)
+    a = (a.data.copy(), a.index_plane.copy())
+    monkeypatch.setattr(msr, "_HOST_GATHER", True)
+    b = msr.rasterize(pc, cam, sel)
+    assert getattr(msr._renderer_for(640, 360, torch_device()), "_hg", None) is not None
+    np.testing.assert_array_equal(b.index_plane, a[1])
+    assert np.array_equal(b.data.view(np.uint32), a[0].view(np.uint32))
+    ref = oracle.rasterize(pc, cam, sel)
+    np.testing.assert_array_equal(b.index_plane, ref["index_plane"])
+    assert np.array_equal(b.data, ref["data"])
+
+
+def torch_device():
+    import torch
+
+    return torch.device("cuda", torch.cuda.current_device())
