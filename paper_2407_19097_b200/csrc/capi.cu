@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <unistd.h>
 
 #include <atomic>
 #include <condition_variable>
@@ -125,7 +126,9 @@ void host_parallel_for(int64_t n, const std::function<void(int64_t, int64_t)>& f
     const int t = e ? atoi(e) : (hw > 0 ? hw : 1);
     return (t > 64 ? 64 : (t < 1 ? 1 : t)) - 1;  // + the calling thread
   }());
-  if (n < 65536) {
+  // small passes inline; after a fork the pool's threads do not exist in the child
+  static const pid_t owner = getpid();
+  if (n < 65536 || getpid() != owner) {
     f(0, n);
     return;
   }
