@@ -562,18 +562,18 @@ def test_hiz_refresh_kernels_agree(cuda, monkeypatch, W, H):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("pinned", [False, True])
-def test_rasterize_host_gather_matches_zero_copy(cuda, monkeypatch, pinned):
+@pytest.mark.parametrize("pinned,arity", [(False, 3), (True, 3), (False, 4)])
+def test_rasterize_host_gather_matches_zero_copy(cuda, monkeypatch, pinned, arity):
     """rasterize()'s host-side gather of the winners' rgb (nar_host_gather_rgb +
     nar_resolve_pixrgb) gives the same FeatureImage as the resolve kernel's own
-    zero-copy gather, and both equal the oracle."""
+    zero-copy gather, and both equal the oracle (RGB and RGBA u8 streams)."""
     from paper_2407_19097_b200 import msr
     from paper_2407_19097_b200.geometry import Intrinsics, PointCloud, Stream, look_at
 
     rng = np.random.default_rng(21)
     n = 3_000_000
     pc = PointCloud(rng.uniform(-1, 1, (n, 3)).astype(np.float32),
-                    [Stream("rgb", "u8", rng.integers(0, 256, (n, 3), dtype=np.uint8))],
+                    [Stream("rgb", "u8", rng.integers(0, 256, (n, arity), dtype=np.uint8))],
                     pinned=pinned)
     cam = look_at((0.3, -2.4, 1.1), (0, 0, 0), Intrinsics(width=640, height=360))
     sel = msr.StreamSelection(rgb=True, depth=True)
