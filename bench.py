@@ -819,7 +819,14 @@ def main_ours(args):
                             "d2h_bytes_per_step": int(d2h),
                             "api": "paper_2407_19097_b200.msr.rasterize(PointCloud(numpy arrays)) "
                                    "-- the stock drop-in caller"}}
-        del host_pos, host_rgb, pc_pin, fi
+        # the host-buffer path's FeatureImage equals the device path's G-buffer of the
+        # same frame (whose keybuf / G-buffer the parity check compares with the oracle)
+        r.render(cloud, cam)
+        r.resolve(cloud, cam, sel, out=out)
+        dev_data = out["data"][:H, :W].cpu().numpy()
+        e2e["matches_device_frame"] = bool(np.array_equal(fi.data.view(np.uint32),
+                                                          dev_data.view(np.uint32)))
+        del host_pos, host_rgb, pc_pin, fi, dev_data
 
     # ---- full NAR frame on the same cloud: render + resolve + U-Net ----------
     pipeline = None
