@@ -1055,6 +1055,7 @@ __global__ void __launch_bounds__(256)
   if (P.coverage) P.coverage[pix] = covered ? 1 : 0;
   if (P.index_plane) P.index_plane[pix] = idx;
   if (P.depth) P.depth[pix] = dep;
+  if (!dst) return;  // planes only (no channel data requested)
 
   int s = -1;
   if (covered) {
@@ -1088,10 +1089,9 @@ __global__ void __launch_bounds__(256)
       v.z = __fdiv_rn((float)(uint32_t)((w >> 16) & 0xFFu), 255.0f);
       v.w = fminf(fmaxf(__fdiv_rn(P.near_f, dep), 0.0f), 1.0f);
     }
-    if (dst) *reinterpret_cast<float4*>(dst) = v;
+    *reinterpret_cast<float4*>(dst) = v;
     return;
   }
-  if (!dst) return;
   if (s < 0) {  // empty, or (owner_only) won by another rank's points
     for (int c = 0; c < P.C; ++c) dst[c] = 0.0f;
     return;

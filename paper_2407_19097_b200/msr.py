@@ -406,8 +406,9 @@ class Renderer:
         else:
             _check_outputs(out, len(names), self.height, self.width)
         ro = _lib.ResolveOut()
-        ro.data = out["data"].data_ptr()
-        ro.data_h, ro.data_w = int(out["data"].shape[0]), int(out["data"].shape[1])
+        if "data" in out:  # (absent: the planes alone)
+            ro.data = out["data"].data_ptr()
+            ro.data_h, ro.data_w = int(out["data"].shape[0]), int(out["data"].shape[1])
         # planes are optional (nar_resolve_out: NULL = not written)
         ro.coverage = out["coverage"].data_ptr() if "coverage" in out else None
         ro.index_plane = out["index_plane"].data_ptr() if "index_plane" in out else None
@@ -422,8 +423,8 @@ class Renderer:
                           _lib.stream_handle(stream, self.device.index))
             else:
                 self._resolve_call(kc, s, segs, len(cloud.segments), ro, stream, peers, rows)
-        return DeviceFeatureImage(self.width, self.height, names, out["data"], out.get("coverage"),
-                                  out.get("index_plane"), out.get("depth"))
+        return DeviceFeatureImage(self.width, self.height, names, out.get("data"),
+                                  out.get("coverage"), out.get("index_plane"), out.get("depth"))
 
     def _resolve_call(self, kc, s, segs, nseg, ro, stream, peers, rows) -> None:
         if peers is None:
@@ -477,15 +478,18 @@ def _check_outputs(out: dict, n_channels: int, H: int, W: int) -> None:
     the kernel writes through raw pointers, so a mismatch would corrupt memory."""
     import torch
 
-    d = out["data"]
-    ds = tuple(d.shape)
-    if len(ds) != 3 or ds[2] != n_channels or ds[0] < H or ds[1] < W:
-        raise ValueError(f"out['data'] must be (>= {H}, >= {W}, {n_channels}) for this selection, "
-                         f"got {ds}")
+    if not any(k in out for k in ("data", "coverage", "index_plane", "depth")):
+        raise ValueError("out needs 'data' and / or planes")
+    d = out.get("data")
+    if d is not None:
+        ds = tuple(d.shape)
+        if len(ds) != 3 or ds[2] != n_channels or ds[0] < H or ds[1] < W:
+            raise ValueError(f"out['data'] must be (>= {H}, >= {W}, {n_channels}) for this "
+                             f"selection, got {ds}")
     want = {"data": torch.float32, "coverage": torch.uint8, "index_plane": torch.int64,
             "depth": torch.float32}
     for k, dt in want.items():
-        if k not in out and k != "data":  # optional planes (not written)
+        if k not in out:  # optional: data or planes not written
             continue
         t = out[k]
         if k != "data" and tuple(t.shape) != (H, W):
@@ -567,14 +571,32 @@ def _rasterize(pc: PointCloud, cam: CameraPose, sel: StreamSelection, r: "Render
     meta = {n: _StreamMeta(n, pc.stream(n).format, pc.stream(n).arity) for n in names}
     cloud = DeviceCloud([{"begin": 0, "count": pc.count, "positions": pos_dev,
                           "streams": segs_streams}], meta, dev)
-    pix = _host_gather(r, pc, sel, main)
-    res = r.resolve(cloud, cam, sel, stream=main, pix_rgb=pix)
     # D2H straight into pinned arrays that the returned FeatureImage owns: a
     # pool of output sets on the renderer, recycled once no FeatureImage views
     # them any more (no host-side copy, no page faults on fresh memory)
-    host = _pinned_outputs(r, res)
-    for k in _OUT_KEYS:
-        torch.from_numpy(host[k]).copy_(getattr(res, k), non_blocking=True)
+    if _host_gather_applies(pc, sel):
+        # the planes do not need the attributes: they are resolved and go down
+        # while the host threads gather the winners' rgb (_host_gather)
+        chans = sel.channel_names(pc)
+        devo = getattr(r, "_dev_out", None)
+        if devo is None or devo["data"].shape[-1] != len(chans):
+            devo = r._dev_out = r.alloc_outputs(len(chans))
+        ev = _keys_to_host(r, main)
+        r.resolve(cloud, cam, sel, out={k: devo[k] for k in _OUT_KEYS[1:]}, stream=main,
+                  clear=False)
+        res = DeviceFeatureImage(W, H, chans, devo["data"], devo["coverage"], devo["index_plane"],
+                                 devo["depth"])
+        host = _pinned_outputs(r, res)
+        for k in _OUT_KEYS[1:]:
+            torch.from_numpy(host[k]).copy_(devo[k], non_blocking=True)
+        pix = _host_gather(r, pc, sel, main, ev)
+        r.resolve(cloud, cam, sel, out={"data": devo["data"]}, stream=main, pix_rgb=pix)
+        torch.from_numpy(host["data"]).copy_(devo["data"], non_blocking=True)
+    else:
+        res = r.resolve(cloud, cam, sel, stream=main)
+        host = _pinned_outputs(r, res)
+        for k in _OUT_KEYS:
+            torch.from_numpy(host[k]).copy_(getattr(res, k), non_blocking=True)
     main.synchronize()  # also keeps the uploaded tensors alive until consumed
     names_out = sel.channel_names(pc)
     data = host["data"]
@@ -590,31 +612,53 @@ _OUT_KEYS = ("data", "coverage", "index_plane", "depth")
 _HOST_GATHER = os.environ.get("NAR_HOST_GATHER", "1") != "0"
 
 
-def _host_gather(r: "Renderer", pc: PointCloud, sel: StreamSelection, main):
-    """The winners' rgb for an RGB+D frame of a host cloud, gathered by host threads:
-    the keybuf comes down (8 B per pixel), ``nar_host_gather_rgb`` reads each winner's
-    3 bytes from the caller's array (~1.6 ms for 2M pixels on 16 cores) and the packed
-    per-pixel words go back up (4 B per pixel) -- instead of ~2M zero-copy PCIe reads
-    by the resolve kernel (~4.7 ms).  None where it does not apply (the kernel then
-    gathers in place).  NAR_HOST_GATHER=0 disables it."""
-    import torch
-
+def _host_gather_applies(pc: PointCloud, sel: StreamSelection) -> bool:
+    """RGB+D frames of a host cloud with a contiguous u8 rgb stream (NAR_HOST_GATHER)."""
     if not (_HOST_GATHER and sel.rgb and sel.depth and not (sel.vel2d or sel.vel3d)
             and not sel.coverage_channel and not sel.scalars and pc.count > 0):
-        return None
+        return False
     st = pc.stream(sel.rgb_stream)
-    if st.format != "u8" or st.arity < 3 or st.data.dtype != np.uint8 or not st.data.flags.c_contiguous:
-        return None
+    return (st.format == "u8" and st.arity >= 3 and st.data.dtype == np.uint8
+            and st.data.flags.c_contiguous)
+
+
+def _hg_buffers(r: "Renderer") -> dict:
+    import torch
+
     npix = r.width * r.height
     hg = getattr(r, "_hg", None)
     if hg is None or hg["keys"].numel() != npix:
         hg = r._hg = {"keys": torch.empty(npix, dtype=torch.int64, pin_memory=True),
                       "pix": torch.empty(npix, dtype=torch.int32, pin_memory=True),
                       "dev": torch.empty(npix, dtype=torch.int32, device=r.device)}
-    hg["keys"].copy_(r.keybuf, non_blocking=True)
-    main.synchronize()
-    _lib.call("nar_host_gather_rgb", hg["keys"].data_ptr(), npix, r.domain, st.data.ctypes.data,
-              st.arity, C.c_uint64(0), pc.count, hg["pix"].data_ptr())
+    return hg
+
+
+def _keys_to_host(r: "Renderer", main):
+    """The frame's keybuf copied down on ``main``; returns the event of that copy."""
+    import torch
+
+    hg = _hg_buffers(r)
+    with torch.cuda.stream(main):
+        hg["keys"].copy_(r.keybuf, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(main)
+    return ev
+
+
+def _host_gather(r: "Renderer", pc: PointCloud, sel: StreamSelection, main, keys_ready):
+    """The winners' rgb for an RGB+D frame of a host cloud, gathered by host threads:
+    once the keybuf copy (8 B per pixel) has landed, ``nar_host_gather_rgb`` reads each
+    winner's 3 bytes from the caller's array (~1.6 ms for 2M pixels on 16 cores) and
+    the packed per-pixel words go back up (4 B per pixel) on ``main`` -- instead of
+    ~2M zero-copy PCIe reads by the resolve kernel (~4.7 ms)."""
+    import torch
+
+    hg = _hg_buffers(r)
+    st = pc.stream(sel.rgb_stream)
+    keys_ready.synchronize()
+    _lib.call("nar_host_gather_rgb", hg["keys"].data_ptr(), r.width * r.height, r.domain,
+              st.data.ctypes.data, st.arity, C.c_uint64(0), pc.count, hg["pix"].data_ptr())
     with torch.cuda.stream(main):
         hg["dev"].copy_(hg["pix"], non_blocking=True)
     return hg["dev"]
