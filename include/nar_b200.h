@@ -207,13 +207,16 @@ int nar_resolve_peers(const uint64_t* const* keybufs, int32_t n_keybufs, int32_t
  * pixel, the winner's rgb bytes c0 | c1 << 8 | c2 << 16 (0 where the pixel is empty
  * or the winner lies outside [begin, begin + count)) on a pool of host threads
  * (NAR_HOST_THREADS); nar_resolve_pixrgb is nar_resolve with the rgb taken from that
- * per-pixel array (device copy) -- RGB+D u8 selections only, identical results. */
+ * per-pixel array (device copy) -- RGB+D u8 selections only, identical results --
+ * for the padded-output rows [row_begin, row_end) (row_end < 0: to the last row), so
+ * a frame can be gathered, resolved and copied down in bands that overlap. */
 int nar_host_gather_rgb(const uint64_t* keys, int64_t npix, int32_t key_domain,
                         const uint8_t* rgb, int32_t arity, uint64_t begin, int64_t count,
                         uint32_t* out);
-int nar_resolve_pixrgb(uint64_t* keybuf_dev, const nar_camera* cam, int32_t key_domain,
-                       const nar_selection* sel, const nar_segment* segments, int32_t n_segments,
-                       const nar_resolve_out* out, const uint32_t* pix_rgb_dev, void* stream);
+int nar_resolve_pixrgb(uint64_t* keybuf_dev, int32_t row_begin, int32_t row_end,
+                       const nar_camera* cam, int32_t key_domain, const nar_selection* sel,
+                       const nar_segment* segments, int32_t n_segments, const nar_resolve_out* out,
+                       const uint32_t* pix_rgb_dev, void* stream);
 
 /* ---- gated U-Net (neural/model.py) -------------------------------------------------- */
 /* Standalone ops of the network (model.py:135-163), f32 device tensors in/out.

@@ -135,7 +135,7 @@ SIGNATURES = {
     "nar_host_gather_rgb": (C.c_int, [_vp, _i64, _i32, _vp, _i32, _u64, _i64, _vp]),
     "nar_resolve_pixrgb": (
         C.c_int,
-        [_vp, C.POINTER(Camera), _i32, C.POINTER(Selection), C.POINTER(Segment), _i32,
+        [_vp, _i32, _i32, C.POINTER(Camera), _i32, C.POINTER(Selection), C.POINTER(Segment), _i32,
          C.POINTER(ResolveOut), _vp, _vp],
     ),
     "nar_unet_create": (C.c_int, [C.POINTER(UNetConfigC), C.POINTER(C.c_void_p)]),

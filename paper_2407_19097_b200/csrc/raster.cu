@@ -1902,12 +1902,13 @@ int nar_resolve(uint64_t* keybuf_dev, const nar_camera* cam, int32_t key_domain,
                       out, stream);
 }
 
-int nar_resolve_pixrgb(uint64_t* keybuf_dev, const nar_camera* cam, int32_t key_domain,
-                       const nar_selection* sel, const nar_segment* segments, int32_t n_segments,
-                       const nar_resolve_out* out, const uint32_t* pix_rgb_dev, void* stream) {
+int nar_resolve_pixrgb(uint64_t* keybuf_dev, int32_t row_begin, int32_t row_end,
+                       const nar_camera* cam, int32_t key_domain, const nar_selection* sel,
+                       const nar_segment* segments, int32_t n_segments, const nar_resolve_out* out,
+                       const uint32_t* pix_rgb_dev, void* stream) {
   if (!pix_rgb_dev) return set_error(NAR_ERR_INVALID, "NULL per-pixel rgb");
-  return resolve_impl(keybuf_dev, nullptr, 0, 0, -1, cam, key_domain, sel, segments, n_segments,
-                      out, stream, pix_rgb_dev);
+  return resolve_impl(keybuf_dev, nullptr, 0, row_begin, row_end, cam, key_domain, sel, segments,
+                      n_segments, out, stream, pix_rgb_dev);
 }
 
 // Host side of the gather: one pass over the frame's keys on a persistent pool of

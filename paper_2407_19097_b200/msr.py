@@ -418,8 +418,10 @@ class Renderer:
         segs = _segments_struct(cloud, sel)
         with _lib.on_device(self.device.index):
             if pix_rgb is not None:
-                _lib.call("nar_resolve_pixrgb", self.keybuf.data_ptr(), C.byref(kc), self.domain,
-                          C.byref(s), segs, len(cloud.segments), C.byref(ro), pix_rgb.data_ptr(),
+                r0, r1 = rows if rows is not None else (0, -1)
+                _lib.call("nar_resolve_pixrgb", self.keybuf.data_ptr(), int(r0), int(r1),
+                          C.byref(kc), self.domain, C.byref(s), segs, len(cloud.segments),
+                          C.byref(ro), pix_rgb.data_ptr(),
                           _lib.stream_handle(stream, self.device.index))
             else:
                 self._resolve_call(kc, s, segs, len(cloud.segments), ro, stream, peers, rows)
@@ -581,7 +583,13 @@ def _rasterize(pc: PointCloud, cam: CameraPose, sel: StreamSelection, r: "Render
         devo = getattr(r, "_dev_out", None)
         if devo is None or devo["data"].shape[-1] != len(chans):
             devo = r._dev_out = r.alloc_outputs(len(chans))
-        ev = _keys_to_host(r, main)
+        # in row bands: the keys of every band go down first; then, band by band, the
+        # host threads gather while the previous band's words go up, resolve and come
+        # back down (NAR_GATHER_BANDS, default 4)
+        data_h = int(devo["data"].shape[0])
+        nb = max(1, min(_GATHER_BANDS, H))
+        edges = [H * b // nb for b in range(nb + 1)]
+        evs = [_keys_to_host(r, main, edges[b] * W, edges[b + 1] * W) for b in range(nb)]
         r.resolve(cloud, cam, sel, out={k: devo[k] for k in _OUT_KEYS[1:]}, stream=main,
                   clear=False)
         res = DeviceFeatureImage(W, H, chans, devo["data"], devo["coverage"], devo["index_plane"],
@@ -589,9 +597,12 @@ def _rasterize(pc: PointCloud, cam: CameraPose, sel: StreamSelection, r: "Render
         host = _pinned_outputs(r, res)
         for k in _OUT_KEYS[1:]:
             torch.from_numpy(host[k]).copy_(devo[k], non_blocking=True)
-        pix = _host_gather(r, pc, sel, main, ev)
-        r.resolve(cloud, cam, sel, out={"data": devo["data"]}, stream=main, pix_rgb=pix)
-        torch.from_numpy(host["data"]).copy_(devo["data"], non_blocking=True)
+        for b in range(nb):
+            y0, y1 = edges[b], (edges[b + 1] if b + 1 < nb else data_h)  # (+ padding rows)
+            pix = _host_gather(r, pc, sel, main, evs[b], edges[b] * W, edges[b + 1] * W)
+            r.resolve(cloud, cam, sel, out={"data": devo["data"]}, stream=main, pix_rgb=pix,
+                      rows=(y0, y1))
+            torch.from_numpy(host["data"][y0:y1]).copy_(devo["data"][y0:y1], non_blocking=True)
     else:
         res = r.resolve(cloud, cam, sel, stream=main)
         host = _pinned_outputs(r, res)
@@ -610,6 +621,7 @@ def _rasterize(pc: PointCloud, cam: CameraPose, sel: StreamSelection, r: "Render
 
 _OUT_KEYS = ("data", "coverage", "index_plane", "depth")
 _HOST_GATHER = os.environ.get("NAR_HOST_GATHER", "1") != "0"
+_GATHER_BANDS = int(os.environ.get("NAR_GATHER_BANDS", "4"))
 
 
 def _host_gather_applies(pc: PointCloud, sel: StreamSelection) -> bool:
@@ -634,33 +646,37 @@ def _hg_buffers(r: "Renderer") -> dict:
     return hg
 
 
-def _keys_to_host(r: "Renderer", main):
-    """The frame's keybuf copied down on ``main``; returns the event of that copy."""
+def _keys_to_host(r: "Renderer", main, p0: int = 0, p1: int | None = None):
+    """Keybuf words [p0, p1) copied down on ``main``; returns the event of that copy."""
     import torch
 
     hg = _hg_buffers(r)
+    p1 = r.width * r.height if p1 is None else p1
     with torch.cuda.stream(main):
-        hg["keys"].copy_(r.keybuf, non_blocking=True)
+        hg["keys"][p0:p1].copy_(r.keybuf[p0:p1], non_blocking=True)
         ev = torch.cuda.Event()
         ev.record(main)
     return ev
 
 
-def _host_gather(r: "Renderer", pc: PointCloud, sel: StreamSelection, main, keys_ready):
-    """The winners' rgb for an RGB+D frame of a host cloud, gathered by host threads:
-    once the keybuf copy (8 B per pixel) has landed, ``nar_host_gather_rgb`` reads each
-    winner's 3 bytes from the caller's array (~1.6 ms for 2M pixels on 16 cores) and
-    the packed per-pixel words go back up (4 B per pixel) on ``main`` -- instead of
-    ~2M zero-copy PCIe reads by the resolve kernel (~4.7 ms)."""
+def _host_gather(r: "Renderer", pc: PointCloud, sel: StreamSelection, main, keys_ready,
+                 p0: int = 0, p1: int | None = None):
+    """The winners' rgb of pixels [p0, p1) of an RGB+D frame of a host cloud, gathered
+    by host threads: once the keybuf copy (8 B per pixel) has landed,
+    ``nar_host_gather_rgb`` reads each winner's 3 bytes from the caller's array (~1.6 ms
+    for 2M pixels on 16 cores) and the packed per-pixel words go back up (4 B per pixel)
+    on ``main`` -- instead of ~2M zero-copy PCIe reads by the resolve kernel (~4.7 ms)."""
     import torch
 
     hg = _hg_buffers(r)
+    p1 = r.width * r.height if p1 is None else p1
     st = pc.stream(sel.rgb_stream)
     keys_ready.synchronize()
-    _lib.call("nar_host_gather_rgb", hg["keys"].data_ptr(), r.width * r.height, r.domain,
-              st.data.ctypes.data, st.arity, C.c_uint64(0), pc.count, hg["pix"].data_ptr())
+    _lib.call("nar_host_gather_rgb", hg["keys"].data_ptr() + 8 * p0, p1 - p0, r.domain,
+              st.data.ctypes.data, st.arity, C.c_uint64(0), pc.count,
+              hg["pix"].data_ptr() + 4 * p0)
     with torch.cuda.stream(main):
-        hg["dev"].copy_(hg["pix"], non_blocking=True)
+        hg["dev"][p0:p1].copy_(hg["pix"][p0:p1], non_blocking=True)
     return hg["dev"]
 
 
