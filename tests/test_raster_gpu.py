@@ -594,3 +594,24 @@ def torch_device():
     import torch
 
     return torch.device("cuda", torch.cuda.current_device())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("wh", [(31, 7), (1, 1), (97, 3)])
+def test_rasterize_host_gather_odd_frames(cuda, wh):
+    """The banded host gather on tiny / odd frames (fewer rows than bands, one pixel)
+    equals the oracle."""
+    from paper_2407_19097_b200 import msr
+    from paper_2407_19097_b200.geometry import Intrinsics, PointCloud, Stream, look_at
+
+    W, H = wh
+    rng = np.random.default_rng(W * 100 + H)
+    n = 20_000
+    pc = PointCloud(rng.uniform(-1, 1, (n, 3)).astype(np.float32),
+                    [Stream("rgb", "u8", rng.integers(0, 256, (n, 3), dtype=np.uint8))])
+    cam = look_at((0.2, -2.5, 0.9), (0, 0, 0), Intrinsics(width=W, height=H))
+    sel = msr.StreamSelection(rgb=True, depth=True)
+    fi = msr.rasterize(pc, cam, sel)
+    ref = oracle.rasterize(pc, cam, sel)
+    np.testing.assert_array_equal(fi.index_plane, ref["index_plane"])
+    assert np.array_equal(fi.data, ref["data"])
