@@ -20,7 +20,7 @@ int main() {
   printf("hardware threads %u\n", hw);
   for (int T : {1, 4, 8, 16, 32, 64}) {
     if ((unsigned)T > hw) break;
-    for (int D : {0, 16}) {
+    for (int D : {0, 16, 32, 64}) {
       double best = 1e9;
       for (int rep = 0; rep < 3; ++rep) {
         auto t0 = std::chrono::steady_clock::now();
