@@ -534,6 +534,46 @@ def test_resolve_without_planes(cuda):
         lean.to_host()
 
 
+def test_resolve_planes_only_and_row_bands(cuda):
+    """resolve(out={planes}) writes the coverage / index / depth planes alone (no channel
+    data, no attribute reads) and leaves the keybuf when clear=False; the per-pixel-rgb
+    resolve over row bands then reproduces a full resolve's channel data band by band."""
+    import torch
+
+    from paper_2407_19097_b200 import _lib
+    from paper_2407_19097_b200.geometry import Intrinsics, PointCloud, Stream, look_at
+    from paper_2407_19097_b200.msr import DeviceCloud, Renderer, StreamSelection
+
+    rng = np.random.default_rng(12)
+    n = 300_000
+    rgb = rng.integers(0, 256, (n, 3), dtype=np.uint8)
+    pc = PointCloud(rng.uniform(-1, 1, (n, 3)).astype(np.float32), [Stream("rgb", "u8", rgb)])
+    cloud = DeviceCloud.from_clouds([pc], device=cuda)
+    W, H = 200, 136
+    cam = look_at((0.0, -2.2, 1.0), (0, 0, 0), Intrinsics(width=W, height=H))
+    sel = StreamSelection(rgb=True, depth=True)
+    r = Renderer(W, H, device=cuda, pad_multiple=16)
+    r.render(cloud, cam)
+    full = r.resolve(cloud, cam, sel, clear=False)
+    planes = {k: v for k, v in r.alloc_outputs(4).items() if k != "data"}
+    p = r.resolve(cloud, cam, sel, out=planes, clear=False)
+    keys = r.keybuf.cpu().numpy().view(np.uint64)
+    for k in ("coverage", "index_plane", "depth"):
+        assert torch.equal(getattr(p, k), getattr(full, k)), k
+    assert p.data is None
+    # per-pixel rgb words (the host gather's output) + banded resolves
+    pix = np.zeros(W * H, np.uint32)
+    assert _lib.load().nar_host_gather_rgb(keys.ctypes.data, W * H, r.domain, rgb.ctypes.data, 3,
+                                           0, n, pix.ctypes.data) == 0
+    pix_dev = torch.from_numpy(pix.view(np.int32)).to(cuda)
+    data = torch.full_like(full.data, float("nan"))
+    rows_pad = full.data.shape[0]
+    for y0, y1 in ((0, 50), (50, 51), (51, H), (H, rows_pad)):
+        r.resolve(cloud, cam, sel, out={"data": data}, pix_rgb=pix_dev, rows=(y0, y1), clear=False)
+    torch.cuda.synchronize()
+    assert torch.equal(data.view(torch.int32), full.data.view(torch.int32))
+
+
 @pytest.mark.parametrize("W,H", [(640, 360), (1920, 1080), (3840, 2160)])
 def test_hiz_refresh_kernels_agree(cuda, monkeypatch, W, H):
     """The coalesced Hi-Z refresh (hiz_rows_kernel, default for even widths) writes the
