@@ -171,6 +171,9 @@ __host__ __device__ constexpr int tc_fixed_smem(int N) {
 #ifndef NAR_TC_WEIGHT_PREFETCH
 #define NAR_TC_WEIGHT_PREFETCH 1
 #endif
+#ifndef NAR_TC_LD64
+#define NAR_TC_LD64 1
+#endif
 #ifndef NAR_TC_MAX_STAGES
 #define NAR_TC_MAX_STAGES 3
 #endif
@@ -353,6 +356,19 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
       : "memory");
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// x64: two consecutive rows of an N = 32 layer ([f16 g16] x 2) in one load -- one
+// instruction, so both rows' TMEM latency is paid once (ptxas sinks separate loads)
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, float* v) {
+  uint32_t r[64];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]), "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 64; ++i) v[i] = __uint_as_float(r[i]);
 }
 
 // 32-byte global store (sm_100 STG.256): one full sector per lane
@@ -823,6 +839,51 @@ __global__ void __maxnreg__(96)
             for (int k = 0; k < 4; ++k)
               if (k < a.head_n)
                 dst[k] = fmaf(0.5f, tanh_approx(0.5f * (lg[k] + a.head_bv[k])), 0.5f);  // sigmoid
+          }
+        }
+      } else if constexpr (!kHead && N == 32 && R == 8 && NAR_TC_LD64) {
+        // N = 32 (16 channels): every warp owns two consecutive rows (4 row slots of
+        // 8 rows, or of 4 pooled pairs); both rows' f and g come in one x64 load
+        const int r0 = u0 * rstep;
+        float v[64];
+        tmem_ld64(tbase + (uint32_t)(b * R * N + r0 * N) + lane_off, v);
+        tmem_wait_ld();
+        float pacc[16];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          float o[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) o[e] = gate_h(v[32 * h + e], v[32 * h + 16 + e]);
+          const int y = y0 + r0 + h;
+          if (a.out != nullptr && y < a.H && xok) {
+            uint32_t pw[8];
+#pragma unroll
+            for (int e = 0; e < 16; e += 2) {
+              __nv_bfloat162 hh = __floats2bfloat162_rn(o[e], o[e + 1]);
+              pw[e / 2] = *reinterpret_cast<uint32_t*>(&hh);
+            }
+            const int wsh = a.out_wide;
+            __nv_bfloat16* d = a.out + (((size_t)y * a.W + x) << wsh) * a.cout_stride;
+            st_global_v8(d, pw);
+            if (wsh) st_global_v8(d + a.cout_stride, pw);
+          }
+          if (do_pool) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) pacc[e] = h == 0 ? o[e] : pacc[e] + o[e];
+          }
+        }
+        if (do_pool) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) pacc[e] += __shfl_xor_sync(0xffffffffu, pacc[e], 1);
+          const int y = y0 + r0;
+          if ((m & 1) == 0 && y < a.H && xok) {
+            uint32_t pw[8];
+#pragma unroll
+            for (int e = 0; e < 16; e += 2) {
+              __nv_bfloat162 hh = __floats2bfloat162_rn(0.25f * pacc[e], 0.25f * pacc[e + 1]);
+              pw[e / 2] = *reinterpret_cast<uint32_t*>(&hh);
+            }
+            st_global_v8(a.pool_out + ((size_t)(y >> 1) * (a.W >> 1) + (x >> 1)) * a.cout_stride, pw);
           }
         }
       } else if constexpr (!kHead && COUTP % 16 == 0) {
