@@ -308,19 +308,25 @@ __device__ __forceinline__ uint64_t desc_add(uint64_t d, uint32_t bytes) {
   return d + (uint64_t)(bytes >> 4);
 }
 
+// MMA issue and commit are called by the whole (converged) MMA warp: elect.sync in
+// the asm picks the issuing lane (with the compile-time TMEM base this keeps the
+// issue loop short; from a lane-0 branch every MMA sat in its own uniform retry loop)
 __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
                                           uint32_t idesc, uint32_t accum) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\t"
+      "{\n\t.reg .pred p, e;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
       : "memory");
 }
 
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
           smem_u32(bar))
       : "memory");
 }
@@ -532,6 +538,7 @@ __global__ void __maxnreg__(96)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tbase_slot;
+  if (tbase != 0u) __trap();  // a 512-column allocation is always column 0 (the MMA issuer relies on it)
   // chunk q's packed weights: paired up2 chunks (4 stacked blocks) first
   constexpr uint32_t B3 = tc_b3_bytes(N), B4 = tc_b4_bytes(N);
   auto wchunk = [&](int q, size_t& boff) -> uint32_t {
@@ -611,7 +618,9 @@ __global__ void __maxnreg__(96)
       mbar_wait(&tempty[b], (((uint32_t)(tl / NB)) & 1u) ^ 1u);
       tc_fence_after();
       if (lane == 0) TC_TRACE(tl, 1);
-      const uint32_t dcol = tbase + (uint32_t)(b * R * N);
+      // one CTA per SM allocates all 512 TMEM columns, so the allocation is column 0
+      // (checked at allocation): a compile-time base keeps the D addresses uniform
+      const uint32_t dcol = (uint32_t)(b * R * N);
       const int y0 = (tile / tiles_x) * R;
       for (int q = 0; q < nq; ++q, ++it) {
         // halo row h -> smem row (h + par) >> sh: a wide up2 chunk holds each
@@ -623,11 +632,11 @@ __global__ void __maxnreg__(96)
         mbar_wait(&full[s], (uint32_t)(it / S) & 1u);
         tc_fence_after();
         if (lane == 0 && q < 4) TC_TRACE(tl, 2 + 2 * q);
-        if (lane == 0 && (a.debug & 2)) {
+        if (a.debug & 2) {  // (the whole warp: umma_commit elects one lane)
           umma_commit(&empty[s]);
           if (last)
             for (int g = 0; g < rg; ++g) umma_commit(&tf[g]);  // (all barriers: timing mode)
-        } else if (lane == 0) {
+        } else {  // the whole warp; one lane elected per MMA / commit
           const uint32_t sa = smem_u32(smem + s * STAGE);
           const uint32_t sb = sa + A_BYTES;
           if (q == 0) {  // this tile's R*N accumulator columns start at the bias
