@@ -43,6 +43,7 @@
 #include <string.h>
 
 #include <type_traits>
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -173,6 +174,9 @@ __host__ __device__ constexpr int tc_fixed_smem(int N) {
 #endif
 #ifndef NAR_TC_LD64
 #define NAR_TC_LD64 1
+#endif
+#ifndef NAR_TC_ACOLL
+#define NAR_TC_ACOLL 1
 #endif
 #ifndef NAR_TC_MAX_STAGES
 #define NAR_TC_MAX_STAGES 3
@@ -320,6 +324,34 @@ __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint6
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
       : "memory");
+}
+
+// The same MMA with an A-collector hint: 1 = fill (keep A for the next MMA), 2 = use
+// (reuse the kept A, keep it), 3 = lastuse (reuse, then release) -- consecutive MMAs on
+// the same A tile read it from shared memory once (A_KEEP / A_REUSE in SASS)
+template <int kColl>
+__device__ __forceinline__ void umma_bf16_c(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                            uint32_t idesc) {
+  static_assert(kColl >= 0 && kColl <= 3, "collector op");
+#define NAR_UMMA_COLL(OP)                                                                  \
+  asm volatile("{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, 1, 0;\n\telect.sync _|e, 0xffffffff;\n\t" \
+               "@e tcgen05.mma.cta_group::1.kind::f16" OP " [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d), \
+               "l"(adesc), "l"(bdesc), "r"(idesc)                                          \
+               : "memory")
+  if constexpr (kColl == 0) umma_bf16(tmem_d, adesc, bdesc, idesc, 1u);
+  else if constexpr (kColl == 1) NAR_UMMA_COLL(".collector::a::fill");
+  else if constexpr (kColl == 2) NAR_UMMA_COLL(".collector::a::use");
+  else NAR_UMMA_COLL(".collector::a::lastuse");
+#undef NAR_UMMA_COLL
+}
+
+// compile-time loop: f(integral_constant<int, I>) for I in [I0, I1)
+template <int I0, int I1, typename F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (I0 < I1) {
+    f(std::integral_constant<int, I0>{});
+    static_for<I0 + 1, I1>(f);
+  }
 }
 
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
@@ -738,6 +770,36 @@ __global__ void __maxnreg__(96)
           } else {
             const uint64_t b0 = umma_desc(sb, N * 16, 128);
             const uint64_t a0 = umma_desc_sw32(sa);
+#if NAR_TC_ACOLL
+            if (!up) {
+              // halo row hr and shift kx outer, the output rows r = hr - ky it feeds inner:
+              // each A tile is read from shared memory once per (hr, kx) (A collector)
+              auto hrow = [&](auto hc) {
+                constexpr int HR = decltype(hc)::value;
+                constexpr int KYLO = HR - (R - 1) > 0 ? HR - (R - 1) : 0;
+                constexpr int KYHI = HR < 2 ? HR : 2;
+#pragma unroll
+                for (int kx = 0; kx < 3; ++kx) {
+                  const uint64_t adesc = desc_add(a0, HR * kHaloRowBytes + kx * 32);
+                  auto one = [&](auto kyc) {
+                    constexpr int KY = decltype(kyc)::value;
+                    constexpr int C = KYLO == KYHI ? 0 : (KY == KYLO ? 1 : (KY == KYHI ? 3 : 2));
+                    umma_bf16_c<C>(dcol + (HR - KY) * N, adesc,
+                                   desc_add(b0, (3 * KY + kx) * (N * 32)), IDESC);
+                  };
+                  if constexpr (KYLO <= 0 && 0 <= KYHI) one(std::integral_constant<int, 0>{});
+                  if constexpr (KYLO <= 1 && 1 <= KYHI) one(std::integral_constant<int, 1>{});
+                  if constexpr (KYLO <= 2 && 2 <= KYHI) one(std::integral_constant<int, 2>{});
+                }
+                if (last)  // rows <= HR - 2 are complete
+                  while (slot < rg && HR - 2 >= tc_epi_last_row(slot, units, rg, rstep))
+                    umma_commit(&tf[slot++]);
+              };
+              static_for<0, R + 2>(hrow);
+              if (last)
+                while (slot < rg) umma_commit(&tf[slot++]);
+            } else
+#endif
 #pragma unroll 1
             for (int r = 0; r < R; ++r) {
 #pragma unroll
