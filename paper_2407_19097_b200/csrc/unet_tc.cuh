@@ -754,6 +754,23 @@ __global__ void __maxnreg__(96)
               const uint64_t b3 = umma_desc(bk + 3 * N * 16, 4 * N * 16, 128);
               const uint64_t b0 = umma_desc(bk, 4 * N * 16, 128);
               const uint64_t ax = umma_desc_sw32(sa + kx * 32);
+#if NAR_TC_ACOLL
+              // low-res row g outer: its (up to) three MMAs -- W0 into row 2g, W1+W2 into
+              // rows 2g-2 / 2g-1, W2 into row 2g-3 -- reuse one A read (A collector)
+              static_for<0, R / 2 + 2>([&](auto gc) {
+                constexpr int G = decltype(gc)::value;
+                constexpr bool U3 = G < R / 2, U12 = G >= 1 && G <= R / 2, U0 = G >= 2;
+                constexpr int NU = (U3 ? 1 : 0) + (U12 ? 1 : 0) + (U0 ? 1 : 0);
+                const uint64_t ag = desc_add(ax, G * kHaloRowBytes);
+                constexpr int C3 = NU == 1 ? 0 : 1;
+                constexpr int C12 = NU == 1 ? 0 : (U3 ? (U0 ? 2 : 3) : 1);
+                constexpr int C0 = NU == 1 ? 0 : 3;
+                if constexpr (U3) umma_bf16_c<C3>(dcol + 2 * G * N, ag, b3, IDESC);
+                if constexpr (U12)
+                  umma_bf16_c<C12>(dcol + 2 * (G - 1) * N, ag, b12, umma_idesc_bf16(128, 2 * N));
+                if constexpr (U0) umma_bf16_c<C0>(dcol + (2 * (G - 2) + 1) * N, ag, b0, IDESC);
+              });
+#else
 #pragma unroll
               for (int pr = 0; pr < R / 2; ++pr) {
                 umma_bf16(dcol + 2 * pr * N, desc_add(ax, (pr + 1) * kHaloRowBytes), b12,
@@ -762,6 +779,7 @@ __global__ void __maxnreg__(96)
                 umma_bf16(dcol + (2 * pr + 1) * N, desc_add(ax, (pr + 2) * kHaloRowBytes), b0, IDESC,
                           1u);
               }
+#endif
             }
             if (last) {  // (decoder layers end with the skip chunk; kept for completeness)
               for (int g = 0; g < rg; ++g) umma_commit(&tf[g]);
