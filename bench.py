@@ -595,7 +595,14 @@ def main_ours(args):
 
         counts = [None] * world
         dist.all_gather_object(counts, n_local)
-        if len(set(counts)) == 1:
+        ok = torch.ones(1, device=dev)
+        try:  # symmetric memory usable here? (else the shard is a plain tensor: NCCL path)
+            symm.empty((16,), dtype=torch.float32, device=dev)
+        except Exception as e:  # noqa: BLE001
+            log(f"[rank {rank}] symmetric memory unavailable ({e})")
+            ok.zero_()
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if len(set(counts)) == 1 and ok.item() == 1.0:
             alloc = lambda shape, dt: symm.empty(shape, dtype=dt, device=dev)
     t_gen = time.time()
     if wl.cloud == "trajectories":
