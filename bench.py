@@ -591,12 +591,16 @@ def main_ours(args):
     if peer_wanted:
         # the shard lives in symmetric memory from the start, so the fused
         # composite maps it into every rank without a copy (equal shapes needed)
-        import torch.distributed._symmetric_memory as symm
-
+        try:
+            import torch.distributed._symmetric_memory as symm
+        except Exception:  # noqa: BLE001
+            symm = None
         counts = [None] * world
         dist.all_gather_object(counts, n_local)
         ok = torch.ones(1, device=dev)
         try:  # symmetric memory usable here? (else the shard is a plain tensor: NCCL path)
+            if symm is None:
+                raise RuntimeError("torch.distributed._symmetric_memory not importable")
             symm.empty((16,), dtype=torch.float32, device=dev)
         except Exception as e:  # noqa: BLE001
             log(f"[rank {rank}] symmetric memory unavailable ({e})")
