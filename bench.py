@@ -571,6 +571,8 @@ def main_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:  # the ranks share the host's cores (host-thread gather of the e2e leg)
+        os.environ.setdefault("NAR_HOST_THREADS", str(max(1, (os.cpu_count() or 1) // world)))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
