@@ -312,17 +312,31 @@ __device__ __forceinline__ uint64_t desc_add(uint64_t d, uint32_t bytes) {
   return d + (uint64_t)(bytes >> 4);
 }
 
-// MMA issue and commit are called by the whole (converged) MMA warp: elect.sync in
-// the asm picks the issuing lane (with the compile-time TMEM base this keeps the
-// issue loop short; from a lane-0 branch every MMA sat in its own uniform retry loop)
+// MMA issue and commit: called by one lane -- the one elect_one() picked (ptxas then
+// knows a single thread issues and emits the UTCHMMAs back to back; behind a lane-0
+// branch, or with elect.sync inside every asm, each MMA carried its own uniform loop or
+// collective sequence)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t e;
+  asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+               : "=r"(e));
+  return e != 0;
+}
+
 __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
                                           uint32_t idesc, uint32_t accum) {
   asm volatile(
-      "{\n\t.reg .pred p, e;\n\t"
+      "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
       : "memory");
 }
 
@@ -334,8 +348,8 @@ __device__ __forceinline__ void umma_bf16_c(uint32_t tmem_d, uint64_t adesc, uin
                                             uint32_t idesc) {
   static_assert(kColl >= 0 && kColl <= 3, "collector op");
 #define NAR_UMMA_COLL(OP)                                                                  \
-  asm volatile("{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, 1, 0;\n\telect.sync _|e, 0xffffffff;\n\t" \
-               "@e tcgen05.mma.cta_group::1.kind::f16" OP " [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d), \
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\t"                          \
+               "tcgen05.mma.cta_group::1.kind::f16" OP " [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d), \
                "l"(adesc), "l"(bdesc), "r"(idesc)                                          \
                : "memory")
   if constexpr (kColl == 0) umma_bf16(tmem_d, adesc, bdesc, idesc, 1u);
@@ -352,15 +366,6 @@ __device__ __forceinline__ void static_for(F&& f) {
     f(std::integral_constant<int, I0>{});
     static_for<I0 + 1, I1>(f);
   }
-}
-
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile(
-      "{\n\t.reg .pred e;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
-          smem_u32(bar))
-      : "memory");
 }
 
 __device__ __forceinline__ void tc_fence_before() {
@@ -664,11 +669,13 @@ __global__ void __maxnreg__(96)
         mbar_wait(&full[s], (uint32_t)(it / S) & 1u);
         tc_fence_after();
         if (lane == 0 && q < 4) TC_TRACE(tl, 2 + 2 * q);
-        if (a.debug & 2) {  // (the whole warp: umma_commit elects one lane)
+        if (!elect_one()) {
+          // the other lanes only follow the loop (waits above, __syncwarp below)
+        } else if (a.debug & 2) {
           umma_commit(&empty[s]);
           if (last)
             for (int g = 0; g < rg; ++g) umma_commit(&tf[g]);  // (all barriers: timing mode)
-        } else {  // the whole warp; one lane elected per MMA / commit
+        } else {  // one elected lane issues this chunk's MMAs and commits
           const uint32_t sa = smem_u32(smem + s * STAGE);
           const uint32_t sb = sa + A_BYTES;
           if (q == 0) {  // this tile's R*N accumulator columns start at the bias
