@@ -374,8 +374,11 @@ def test_forward_into_graph_replay(cuda):
         net._launch(x, y_eager, ws, H, W, None)
         torch.cuda.synchronize()
         assert torch.equal(y.view(torch.int32), y_eager.view(torch.int32))
-    g = net._graphs.get((x.data_ptr(), y.data_ptr(), H, W))
-    assert g is not None and g is not False, "the repeated forward was not captured"
+    from paper_2407_19097_b200 import neural
+
+    if neural._UNET_GRAPHS:  # (NAR_UNET_GRAPH=0 keeps plain launches)
+        g = net._graphs.get((x.data_ptr(), y.data_ptr(), H, W))
+        assert g is not None and g is not False, "the repeated forward was not captured"
 
 
 def test_forward_into_inside_caller_graph(cuda):
